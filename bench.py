@@ -1,0 +1,401 @@
+"""Decode-throughput benchmark: wave-index decode attention on B200.
+
+Workload (BASELINE.json configs[1]): Llama-3-8B-shaped decode at 120K context,
+batch 16, 32 layers (32 q / 8 kv heads, d=128) on one B200, against
+full-attention decode over the same KV.  A "step" = one decode token for every
+request through all 32 layers of attention.  Full KV at B=16 (257.7 GB) exceeds
+HBM, so the 32 layers cycle over ``--layer-bufs`` distinct layer buffers
+(each >> L2), as SURVEY.md 8(d) prescribes; both paths use the same buffers.
+
+Prints ONE JSON line (rank 0).  ``--impl reference`` times the reference's
+CPU algorithm instead (the C oracle port of tierkv, oracle/), see DESIGN.md.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HQ, HKV, D = 32, 8, 128
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="wave", choices=["wave", "reference"])
+    ap.add_argument("--batch", type=int, default=16)
+    ap.add_argument("--ctx", type=int, default=122880)
+    ap.add_argument("--layers", type=int, default=32)
+    ap.add_argument("--layer-bufs", type=int, default=4)
+    ap.add_argument("--fa-steps", type=int, default=3)
+    ap.add_argument("--cpu-steps", type=int, default=8)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(s[0]) for s in self.samples)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if s[3 + i].lower().startswith("active")})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(self.samples[0][1]),
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------ synthetic data
+def gen_layer(torch, U, n, d, seed, dev, n_centers=32, seg=8192, noise=0.5):
+    """Keys: per-8K-segment latent centres + Gaussian noise (spatial locality,
+    like tierkv synth.py:46-70); values N(0,1); all bf16-representable."""
+    g = torch.Generator(device=dev).manual_seed(seed)
+    n_seg = -(-n // seg)
+    centers = torch.randn((U, n_seg, n_centers, d), generator=g, device=dev)
+    cidx = torch.randint(n_centers, (U, n), generator=g, device=dev)
+    seg_id = (torch.arange(n, device=dev) // seg).expand(U, n)
+    uidx = torch.arange(U, device=dev)[:, None].expand(U, n)
+    keys = centers[uidx, seg_id, cidx]
+    keys += noise * torch.randn((U, n, d), generator=g, device=dev)
+    keys = keys.bfloat16().float()
+    values = torch.randn((U, n, d), generator=g, device=dev).bfloat16().float()
+    return keys, values, centers
+
+
+def gen_queries(torch, centers, G, steps, seed, persistence=0.9, shared=0.25, per_head=0.25):
+    """Per unit a persistent random walk over its latent centres (temporal
+    locality, synth.py:57-67); each GQA group shares the walk + shared noise,
+    each head adds its own noise.  Returns [steps, U, G, d] bf16-valued fp32."""
+    import numpy as np
+    U, n_seg, nc, d = centers.shape
+    dev = centers.device
+    rng = np.random.default_rng(seed)
+    walk = rng.integers(n_seg * nc, size=U)
+    idx = np.empty((steps, U), np.int64)
+    for t in range(steps):
+        jump = rng.random(U) >= persistence
+        walk = np.where(jump, rng.integers(n_seg * nc, size=U), walk)
+        idx[t] = walk
+    flat = centers.reshape(U, n_seg * nc, d)
+    it = torch.from_numpy(idx).to(dev)
+    base = flat[torch.arange(U, device=dev)[None, :].expand(steps, U), it]  # [steps, U, d]
+    g = torch.Generator(device=dev).manual_seed(seed)
+    q = base[:, :, None, :] + shared * torch.randn((steps, U, 1, d), generator=g, device=dev)
+    q = q + per_head * torch.randn((steps, U, G, d), generator=g, device=dev)
+    return q.bfloat16().float().contiguous()
+
+
+# ------------------------------------------------------------- CPU reference
+def cpu_sample(ctx, steps, seed=0):
+    """One q-head unit of the workload through the C oracle (tierkv's
+    algorithm): prefill untimed, `steps` decode steps timed (path only, no
+    recall metric).  Returns seconds per unit-step."""
+    import numpy as np
+    from oracle import oracle as O
+    rng = np.random.default_rng(seed)
+    d = D
+    n_seg = -(-ctx // 8192)
+    cen = rng.standard_normal((n_seg, 32, d)).astype(np.float32)
+    seg = np.arange(ctx) // 8192
+    keys = cen[seg, rng.integers(32, size=ctx)] + 0.5 * rng.standard_normal((ctx, d)).astype(np.float32)
+    keys = _bf16(keys)
+    vals = _bf16(rng.standard_normal((ctx, d)).astype(np.float32))
+    eng = O.OracleEngine().prefill(keys, vals)
+    qs = _bf16(cen.reshape(-1, d)[rng.integers(n_seg * 32, size=steps)] +
+               0.25 * rng.standard_normal((steps, d)).astype(np.float32))
+    nk = _bf16(rng.standard_normal((steps, d)).astype(np.float32))
+    t0 = time.perf_counter()
+    for t in range(steps):
+        eng.decode_step(qs[t], nk[t], nk[t], with_recall=False)
+    return (time.perf_counter() - t0) / steps
+
+
+def _bf16(x):
+    import numpy as np
+    u = np.ascontiguousarray(x, np.float32).view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
+    return u.astype(np.uint32).view(np.float32)
+
+
+def _cpu_worker(args):
+    ctx, steps, seed = args
+    return cpu_sample(ctx, steps, seed)
+
+
+def run_reference(a):
+    """--impl reference: the reference algorithm on all host cores (one
+    oracle unit per core, units are independent)."""
+    import multiprocessing as mp
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    steps = max(1, a.steps)
+    with mp.get_context("spawn").Pool(cores) as pool:
+        t0 = time.perf_counter()
+        per = pool.map(_cpu_worker, [(a.ctx, steps, s) for s in range(cores)])
+        wall = time.perf_counter() - t0
+    unit_steps_per_s = sum(1.0 / p for p in per)
+    tok_s = unit_steps_per_s / (HQ * a.layers)
+    line = {"impl": "reference", "metric": "decode tokens/sec at 120K ctx (device-timed)",
+            "value": tok_s, "unit": "tokens/s", "n_gpus": a.gpus, "steps": steps,
+            "warmup": a.warmup, "ms_per_step": a.batch / tok_s * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "llama3-8b-shape 32-layer decode, 120K ctx, batch 16",
+                       "batch": a.batch, "ctx": a.ctx, "layers": a.layers},
+            "cpu_baseline": {"value": tok_s, "unit": "tokens/s", "cores": cores, "kind": "port",
+                             "sample": f"{cores} x one q-head unit at {a.ctx} ctx, {steps} decode "
+                                       "steps each (prefill untimed); extrapolated x32 heads x32 layers"},
+            "e2e": {"value": tok_s, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "wall_s": wall}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------- GPU arm
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return run_reference(a)
+    import torch
+    import torch.distributed as dist
+    from paper_2505_02922_b200 import EngineConfig, WaveLayer
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    G = HQ // HKV
+    U = a.batch * HKV  # per-rank units (weak scaling: each rank serves `batch` requests)
+    n_bufs = min(a.layer_bufs, a.layers)
+    total_steps = a.warmup + a.steps
+    log = lambda *x: print(*x, file=sys.stderr, flush=True) if rank == 0 else None
+    cfg = EngineConfig()
+    layers, qpool, kpool = [], [], []
+    t_build = 0.0
+    for li in range(n_bufs):
+        keys, vals, cen = gen_layer(torch, U, a.ctx, D, 1000 * rank + li, dev)
+        lay = WaveLayer(cfg, U, G, D, max_prefill=a.ctx, max_decode=64, store_dtype=torch.bfloat16)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        lay.prefill(keys, vals)
+        torch.cuda.synchronize()
+        t_build += time.perf_counter() - t0
+        layers.append(lay)
+        per_buf = math.ceil(a.layers / n_bufs)
+        qpool.append(gen_queries(torch, cen, G, total_steps * per_buf, 7 + li))
+        kpool.append(torch.randn((total_steps * per_buf, 2, U, D), device=dev).bfloat16().float())
+        del keys, vals, cen
+        torch.cuda.empty_cache()
+        log(f"layer buffer {li}: m={lay.units[0].m} build {t_build:.1f}s")
+    use = [0] * n_bufs
+
+    def wave_step(step_i, timers=None):
+        for l in range(a.layers):
+            b = l % n_bufs
+            lay = layers[b]
+            j = use[b]
+            use[b] += 1
+            if timers is not None:
+                timers[l][0].record()
+            lay.launch_step(qpool[b][j], kpool[b][j, 0], kpool[b][j, 1])
+            if timers is not None:
+                timers[l][1].record()
+            for s in lay.units:
+                s.total += 1
+                s.n_steady += 1
+
+    # ---- warmup + timed wave steps ----
+    for i in range(a.warmup):
+        wave_step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record()
+        for i in range(a.steps):
+            wave_step(i)
+        ev1.record()
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / a.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t)
+    for lay in layers:
+        lay.check_status("bench")
+    value = a.batch * world / (ms / 1e3)
+
+    # ---- roofline of the dominant op (tripartite attention) ----
+    lay = layers[0]
+    cnt = lay.cnt.cpu()
+    n_st = lay.st_n.cpu()
+    m = torch.tensor([s.m for s in lay.units])
+    elem = 2
+    attn_bytes = int(((cnt[:, 1] + n_st).sum() * 2 * D * elem) + cnt[:, 2].sum() * (D * 4 + 4))
+    score_bytes = int(m.sum() * D * 4)
+    # per-kernel events: re-run one step with events around each op
+    s_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(3)]
+    import ctypes
+    from paper_2505_02922_b200 import _lib
+    from paper_2505_02922_b200.wave import _stream
+    q = qpool[0][0]
+    L = lay.L
+    sv = lay._step_view(q)
+    stream = ctypes.c_void_p(_stream())
+    reps = 5
+    t_score = t_attn = 0.0
+    for r in range(reps):
+        s_ev[0][0].record()
+        _lib.check(L.wk_score_topk(ctypes.byref(lay._ixv), ctypes.byref(sv), ctypes.byref(lay._zp),
+                                   lay.U, int(m.max()), stream), "score")
+        s_ev[0][1].record()
+        s_ev[1][0].record()
+        _lib.check(L.wk_tripartite_attn(ctypes.byref(lay._ixv), ctypes.byref(lay._stv), ctypes.byref(sv),
+                                        ctypes.byref(lay._zp), lay.U, lay.S, lay.store_bf16, stream), "attn")
+        s_ev[1][1].record()
+        torch.cuda.synchronize()
+        t_score += s_ev[0][0].elapsed_time(s_ev[0][1]) / reps
+        t_attn += s_ev[1][0].elapsed_time(s_ev[1][1]) / reps
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = attn_bytes / (t_attn / 1e3) / 1e9
+
+    # ---- full-attention comparator (same buffers, same batch) ----
+    fa_ms = None
+    if a.fa_steps > 0:
+        outs = torch.empty((U, G, D), device=dev)
+        for l in range(a.layers):
+            layers[l % n_bufs].full_attention(qpool[l % n_bufs][0], out=outs)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(a.fa_steps):
+            for l in range(a.layers):
+                layers[l % n_bufs].full_attention(qpool[l % n_bufs][i], out=outs)
+        e1.record()
+        torch.cuda.synchronize()
+        fa_ms = e0.elapsed_time(e1) / a.fa_steps
+    fa_bytes_layer = sum(s.store_fill + s.n_steady for s in layers[0].units) * 2 * D * elem
+
+    # ---- e2e: host buffers, copies inside the timed region ----
+    e2e = None
+    if not a.no_e2e:
+        hq = torch.empty((a.layers, U, G, D), dtype=torch.float32).pin_memory()
+        hkv = torch.empty((a.layers, 2, U, D), dtype=torch.float32).pin_memory()
+        hout = torch.empty((a.layers, U, G, D), dtype=torch.float32).pin_memory()
+        dq = torch.empty((a.layers, U, G, D), device=dev)
+        dkv = torch.empty((a.layers, 2, U, D), device=dev)
+        hq.copy_(qpool[0][: a.layers].cpu() if qpool[0].shape[0] >= a.layers else hq)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k_e2e = max(1, min(a.steps, 5))
+        torch.cuda.synchronize()
+        e0.record()
+        for i in range(k_e2e):
+            dq.copy_(hq, non_blocking=True)
+            dkv.copy_(hkv, non_blocking=True)
+            for l in range(a.layers):
+                lay_l = layers[l % n_bufs]
+                lay_l.launch_step(dq[l], dkv[l, 0], dkv[l, 1])
+                hout[l].copy_(lay_l.out, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        e2e_ms = e0.elapsed_time(e1) / k_e2e
+        e2e = {"value": a.batch * world / (e2e_ms / 1e3), "unit": "tokens/s",
+               "h2d_bytes_per_step": int(hq.numel() * 4 + hkv.numel() * 4),
+               "d2h_bytes_per_step": int(hout.numel() * 4), "ms_per_step": e2e_ms}
+
+    # ---- CPU baseline (oracle port of tierkv, one host core) ----
+    cpu = None
+    if rank == 0 and not a.no_cpu and a.cpu_steps > 0:
+        t_unit = cpu_sample(a.ctx, a.cpu_steps)
+        cpu_tok = 1.0 / (t_unit * HQ * a.layers)
+        cpu = {"value": cpu_tok, "unit": "tokens/s", "cores": 1, "kind": "port",
+               "sample": f"one q-head unit at {a.ctx} ctx, {a.cpu_steps} decode steps (prefill "
+                         f"untimed, no recall metric), {t_unit * 1e3:.2f} ms/unit-step, "
+                         f"extrapolated x{HQ} heads x{a.layers} layers"}
+
+    if rank == 0:
+        line = {
+            "metric": "decode tokens/sec at 120K ctx (device-timed)",
+            "value": value, "unit": "tokens/s", "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16 KV / fp32 accumulate", "data": "synthetic",
+            "config": {"workload": "llama3-8b-shape 32-layer decode, 120K ctx, batch 16 (configs[1])",
+                       "batch_per_gpu": a.batch, "ctx": a.ctx, "layers": a.layers,
+                       "layer_buffers": n_bufs, "heads": f"{HQ}q/{HKV}kv", "d": D,
+                       "l2": "inputs larger than L2 (each layer buffer >> 126 MB, cycled)"},
+            "full_attention": {"ms_per_step": fa_ms,
+                               "value": (a.batch * world / (fa_ms / 1e3)) if fa_ms else None,
+                               "speedup_wave_vs_full": (fa_ms / ms) if fa_ms else None,
+                               "bytes_per_layer": fa_bytes_layer,
+                               "hbm_gbs": (fa_bytes_layer * a.layers / (fa_ms / 1e3) / 1e9) if fa_ms else None},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": "wk_tripartite_attn (attend+merge)", "bytes_per_launch": attn_bytes,
+                         "ms_per_launch": t_attn},
+            "breakdown_ms_per_layer": {"score_topk": t_score, "tripartite_attn": t_attn},
+            "build_s": t_build,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clk.summary(),
+            "gpu_launches": a.steps * a.layers * 6,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,155 @@
+/* wavekv.h -- C ABI of the B200 wave-index decode-attention path.
+ *
+ * Drop-in boundary for the reference package tierkv (/root/reference/pkg/src/
+ * tierkv).  The reference exposes a Python API, not an FFI; every entry point
+ * below replaces the compute behind one reference call site (cited), and the
+ * Python host layer paper_2505_02922_b200 binds them with ctypes exactly as a
+ * tierkv maintainer would.
+ *
+ * Conventions
+ *  - All data pointers are device pointers to caller-allocated memory (the
+ *    library allocates nothing); `stream` is a cudaStream_t passed as void*.
+ *    Calls are stream-ordered and asynchronous.
+ *  - Return value: 0 ok; WK_ECONFIG (<0) for caller/config errors (maps to
+ *    tierkv.ConfigError).  Device-detected invariant violations are reported
+ *    through the int status word in the step/build views (non-zero ->
+ *    tierkv.IntegrityError, errors.py:4-23).
+ *  - d % 4 == 0, d <= 256; G (query heads per kv head) <= 8.
+ */
+#ifndef WAVEKV_H
+#define WAVEKV_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WK_ECONFIG (-1)
+#define WK_ECUDA (-2)
+
+/* Per-layer index arrays of U (request, kv-head) units (index.py:96-189,
+ * store.py:48-105).  Shapes in elements. */
+typedef struct wk_index_view {
+  void* store_k;      /* [U, s_cap, d] bf16|fp32 keys, cluster-contiguous     */
+  void* store_v;      /* [U, s_cap, d] values                                  */
+  int32_t* store_tok; /* [U, s_cap] token id per store row                     */
+  int32_t* cl_off;    /* [U, m_cap] first store row of each cluster            */
+  int32_t* cl_size;   /* [U, m_cap] cluster sizes (MetaIndexEntry.size)        */
+  double* C64;        /* [U, m_cap, d] fp64 centroids (MetaIndexEntry.centroid)*/
+  float* C32;         /* [U, m_cap, d] fp32 copy for the scoring scan          */
+  float* Cnorm;       /* [U, m_cap] ||C32||                                    */
+  float* VS32;        /* [U, m_cap, d] fp32 value sums                         */
+  double* VS64;       /* [U, m_cap, d] fp64 value sums (optional, may be NULL) */
+  int64_t s_cap, m_cap;
+} wk_index_view;
+
+/* One clustering segment: a contiguous token range of one unit
+ * (index.py:153-166 segments; index.py:168-186 decode-time updates). */
+typedef struct wk_segment {
+  const float* keys;  /* device fp32 keys of the segment, row stride key_stride */
+  const float* values;
+  int64_t key_stride;
+  int32_t L, k;       /* points, clusters (k = ceil(L / centroid_ratio))       */
+  int32_t unit, cid_base, row_base, tok_base;
+  int64_t p_off, c_off; /* offsets (rows) into the build scratch                */
+  uint64_t rng[4];    /* numpy PCG64 state of SeedSequence([seed, kind, idx])  */
+} wk_segment;
+
+/* Build scratch, sized by the caller: P/A/perm/sims/md rows = sum L,
+ * C rows = sum k (see paper_2505_02922_b200/wave.py:_build_scratch). */
+typedef struct wk_build_scratch {
+  float* P;           /* [sum L, d] normalized points                          */
+  float* C;           /* [sum k, d] spherical centroids                        */
+  int32_t* A;         /* [sum L] assignment                                    */
+  int32_t* perm;      /* [sum L] members sorted by cluster                     */
+  float* sims;        /* [sum L] repair similarities                           */
+  float* md;          /* [2 * sum L] min-dist + cdf (k-means++ seeding)        */
+  wk_segment* segs_dev; /* [n_segments] device copy of the descriptors         */
+  int* status;        /* device status word                                    */
+} wk_build_scratch;
+
+/* Steady zone: sinks + decode buffer per unit (engine.py:87-96). */
+typedef struct wk_steady_view {
+  void* k;            /* [U, t_cap, d]                                          */
+  void* v;
+  int32_t* tok;       /* [U, t_cap]                                             */
+  int32_t* n;         /* [U] live rows                                          */
+  int32_t* next_tok;  /* [U] token id of the next appended token                */
+  int64_t t_cap;
+} wk_steady_view;
+
+/* Per-step buffers (decode_step, engine.py:174-232). */
+typedef struct wk_step_view {
+  const float* q;     /* [U, G, d] queries                                      */
+  int32_t* m;         /* [U] cluster count                                      */
+  float* scores;      /* [U, G, m_cap] approximate q.C (ZonePlan.scores)        */
+  int32_t* rlist;     /* [U, G, r_cap] retrieval ids in rank order              */
+  int32_t* elist;     /* [U, G, e_cap] estimation ids (optional)                */
+  int32_t* nr;        /* [U] r                                                  */
+  int32_t* ne;        /* [U] e                                                  */
+  uint32_t* zmask;    /* [U, m_cap] zone bits (zeroed by wk_score_topk)         */
+  int32_t* ru_ids;    /* [U, ru_cap] union of retrieval clusters                */
+  uint8_t* ru_mask;
+  int32_t* ru_pre;    /* [U, ru_cap + 1]                                        */
+  int32_t* eu_ids;    /* [U, eu_cap] union of estimation clusters               */
+  uint8_t* eu_mask;
+  int32_t* cnt;       /* [U, 4]                                                 */
+  float* tail;        /* [U, G, 4]                                              */
+  float* part;        /* [U, S, G, 3, 2 + d] split partials                     */
+  float* out;         /* [U, G, d] attention output (AttentionOutput.output)    */
+  float* logden;      /* [U, G] StepMetrics.log_denominator                     */
+  float* cov;         /* [U, G] StepMetrics.denominator_coverage                */
+  int* status;        /* device status word                                     */
+  int32_t r_cap, e_cap, ru_cap, eu_cap;
+} wk_step_view;
+
+typedef struct wk_zone_params {
+  int32_t G, d, blas_threads;
+  double retrieval_fraction;  /* IndexConfig.retrieval_fraction  (config.py:26) */
+  double estimation_fraction; /* IndexConfig.estimation_fraction (config.py:27) */
+  int32_t tail_denominator_only; /* IndexConfig.tail_mode                      */
+  int32_t denominator_eq2;       /* EngineConfig.denominator_mode              */
+} wk_zone_params;
+
+int wk_version(void);
+
+/* Segmented spherical k-means + finalize + store packing for a batch of
+ * segments.  Replaces ClusterIndex.segmented_build / update -> _cluster_batch
+ * -> spherical_kmeans + finalize_cluster + SlowTierStore.pack_cluster
+ * (index.py:143-186, clustering.py:66-101, index.py:43-58, store.py:69-90).
+ * `segs` is a HOST array; copied to scratch->segs_dev. */
+int wk_kmeans_segments(const wk_index_view* ix, const wk_segment* segs, int n_segs,
+                       const wk_build_scratch* scratch, int d, int store_bf16,
+                       int kmeans_iters, int blas_threads, int max_L, int max_k,
+                       void* stream);
+
+/* Append one decode token per unit to the steady buffer
+ * (HeadEngine._append_tokens + buffer.append, engine.py:178-182). */
+int wk_append_tokens(const wk_steady_view* st, const float* k_new, const float* v_new, int U,
+                     int d, int store_bf16, void* stream);
+
+/* Centroid scoring over GQA groups + exact zone planning + per-unit unions.
+ * Replaces ClusterIndex.rank -> rank_clusters and plan_zones
+ * (index.py:61-93, 188-189). */
+int wk_score_topk(const wk_index_view* ix, const wk_step_view* sv, const wk_zone_params* zp,
+                  int U, int m_max, void* stream);
+
+/* Fused tripartite attention: steady + retrieved clusters (exact) +
+ * estimation zone (centroids) + LSE merge.  Replaces exact_partial,
+ * estimate_partial, tail_denominator_partial, merge and
+ * HeadEngine._final_output (attention.py:67-148, engine.py:150-172).
+ * S = CTAs per unit. */
+int wk_tripartite_attn(const wk_index_view* ix, const wk_steady_view* st, const wk_step_view* sv,
+                       const wk_zone_params* zp, int U, int S, int store_bf16, void* stream);
+
+/* Full-attention decode over every stored token of each unit (the comparator
+ * and HeadEngine.oracle_step_output / oracle_attention, attention.py:55-64).
+ * Uses sv->q, sv->part, sv->out, sv->logden, sv->cov; n_store[u] = live
+ * store rows of unit u. */
+int wk_full_attn(const wk_index_view* ix, const wk_steady_view* st, const wk_step_view* sv,
+                 const int32_t* n_store, int U, int G, int d, int S, int store_bf16, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

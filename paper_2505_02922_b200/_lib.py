@@ -1,0 +1,114 @@
+"""ctypes binding of libwavekv.so (include/wavekv.h).
+
+The shared library is built in-tree by ``__graft_entry__.build()`` (nvcc,
+sm_100a).  There is no fallback: if the library is missing or the device is
+not a CUDA GPU, every compute call raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .errors import ConfigError, IntegrityError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libwavekv.so")
+
+_P = ctypes.c_void_p
+_I32 = ctypes.c_int32
+_I64 = ctypes.c_int64
+
+
+class IndexViewC(ctypes.Structure):
+    _fields_ = [("store_k", _P), ("store_v", _P), ("store_tok", _P), ("cl_off", _P),
+                ("cl_size", _P), ("C64", _P), ("C32", _P), ("Cnorm", _P), ("VS32", _P),
+                ("VS64", _P), ("s_cap", _I64), ("m_cap", _I64)]
+
+
+class SegmentC(ctypes.Structure):
+    _fields_ = [("keys", _P), ("values", _P), ("key_stride", _I64), ("L", _I32), ("k", _I32),
+                ("unit", _I32), ("cid_base", _I32), ("row_base", _I32), ("tok_base", _I32),
+                ("p_off", _I64), ("c_off", _I64), ("rng", ctypes.c_uint64 * 4)]
+
+
+class BuildScratchC(ctypes.Structure):
+    _fields_ = [("P", _P), ("C", _P), ("A", _P), ("perm", _P), ("sims", _P), ("md", _P),
+                ("segs_dev", _P), ("status", _P)]
+
+
+class SteadyViewC(ctypes.Structure):
+    _fields_ = [("k", _P), ("v", _P), ("tok", _P), ("n", _P), ("next_tok", _P), ("t_cap", _I64)]
+
+
+class StepViewC(ctypes.Structure):
+    _fields_ = [("q", _P), ("m", _P), ("scores", _P), ("rlist", _P), ("elist", _P), ("nr", _P),
+                ("ne", _P), ("zmask", _P), ("ru_ids", _P), ("ru_mask", _P), ("ru_pre", _P),
+                ("eu_ids", _P), ("eu_mask", _P), ("cnt", _P), ("tail", _P), ("part", _P),
+                ("out", _P), ("logden", _P), ("cov", _P), ("status", _P), ("r_cap", _I32),
+                ("e_cap", _I32), ("ru_cap", _I32), ("eu_cap", _I32)]
+
+
+class ZoneParamsC(ctypes.Structure):
+    _fields_ = [("G", _I32), ("d", _I32), ("blas_threads", _I32),
+                ("retrieval_fraction", ctypes.c_double), ("estimation_fraction", ctypes.c_double),
+                ("tail_denominator_only", _I32), ("denominator_eq2", _I32)]
+
+
+_lib = None
+
+# every symbol include/wavekv.h declares
+EXPORTS = ("wk_version", "wk_kmeans_segments", "wk_append_tokens", "wk_score_topk",
+           "wk_tripartite_attn", "wk_full_attn")
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is missing: run __graft_entry__.build() (nvcc, sm_100a); "
+                           "there is no CPU fallback")
+    L = ctypes.CDLL(LIB_PATH)
+    R = ctypes.POINTER
+    L.wk_version.restype = ctypes.c_int
+    L.wk_kmeans_segments.argtypes = [R(IndexViewC), R(SegmentC), ctypes.c_int, R(BuildScratchC),
+                                     ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                     ctypes.c_int, ctypes.c_int, _P]
+    L.wk_append_tokens.argtypes = [R(SteadyViewC), _P, _P, ctypes.c_int, ctypes.c_int, ctypes.c_int, _P]
+    L.wk_score_topk.argtypes = [R(IndexViewC), R(StepViewC), R(ZoneParamsC), ctypes.c_int,
+                                ctypes.c_int, _P]
+    L.wk_tripartite_attn.argtypes = [R(IndexViewC), R(SteadyViewC), R(StepViewC), R(ZoneParamsC),
+                                     ctypes.c_int, ctypes.c_int, ctypes.c_int, _P]
+    L.wk_full_attn.argtypes = [R(IndexViewC), R(SteadyViewC), R(StepViewC), _P, ctypes.c_int,
+                               ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _P]
+    for name in EXPORTS:
+        getattr(L, name).restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def check(rc: int, what: str):
+    if rc == 0:
+        return
+    if rc == -1:
+        raise ConfigError(f"{what}: invalid arguments (WK_ECONFIG)")
+    raise RuntimeError(f"{what}: CUDA launch failed (rc={rc})")
+
+
+STATUS_TEXT = {
+    1: "exact-rescoring band overflow",
+    2: "empty cluster at finalize",
+    3: "device block cache over capacity",
+    4: "zone union overflow",
+    5: "unknown cluster id",
+    6: "merge requires at least one non-empty partial",
+}
+
+
+def raise_status(code: int, what: str):
+    if code == 0:
+        return
+    if code == 6:
+        raise ConfigError(f"{what}: {STATUS_TEXT[6]}")
+    raise IntegrityError(f"{what}: device status {code} ({STATUS_TEXT.get(code, '?')})")

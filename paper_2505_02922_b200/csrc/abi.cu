@@ -1,0 +1,179 @@
+// abi.cu -- extern "C" entry points (include/wavekv.h) launching the
+// sm_100a kernels on the caller's stream.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "decode_internal.h"
+
+namespace wk {
+// kmeans.cu
+__global__ void km_prep_kernel(const SegDesc*, float*, int);
+__global__ void km_seed_kernel(const SegDesc*, const float*, float*, float*, int, int, int);
+__global__ void km_assign_kernel(const SegDesc*, const float*, const float*, int32_t*, int);
+__global__ void km_assign_small_kernel(const SegDesc*, const float*, const float*, int32_t*, int);
+__global__ void km_update_kernel(const SegDesc*, const float*, float*, int32_t*, int32_t*, float*, int, int);
+template <typename T>
+__global__ void km_finalize_kernel(const SegDesc*, const int32_t*, int32_t*, IndexView, int, int*);
+// decode.cu
+template <typename T>
+__global__ void append_kernel(SteadyView, const float*, const float*, int);
+__global__ void score_kernel(IndexView, StepView, int, int);
+__global__ void select_kernel(IndexView, StepView, SelParams);
+__global__ void union_kernel(IndexView, StepView);
+template <typename T, bool FULL>
+__global__ void attend_kernel(IndexView, SteadyView, StepView, AttnParams, const int32_t*);
+__global__ void merge_kernel(StepView, AttnParams, int);
+size_t select_smem_bytes();
+}  // namespace wk
+
+using namespace wk;
+
+#define WK_CHECK_LAUNCH()                          \
+  do {                                             \
+    cudaError_t e_ = cudaGetLastError();           \
+    if (e_ != cudaSuccess) return WK_ECUDA;        \
+  } while (0)
+
+static int g_smem_configured = 0;
+static int configure_smem() {
+  if (g_smem_configured) return 0;
+  // opt in to large dynamic shared memory where the kernels need it
+  if (cudaFuncSetAttribute(km_seed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess) return WK_ECUDA;
+  if (cudaFuncSetAttribute(km_assign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024) != cudaSuccess) return WK_ECUDA;
+  if (cudaFuncSetAttribute(km_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess) return WK_ECUDA;
+  if (cudaFuncSetAttribute(km_finalize_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess) return WK_ECUDA;
+  if (cudaFuncSetAttribute(km_finalize_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess) return WK_ECUDA;
+  if (cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)select_smem_bytes()) != cudaSuccess) return WK_ECUDA;
+  const int at = (int)attend_smem_bytes(256, 4);
+  if (cudaFuncSetAttribute(attend_kernel<float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, at) != cudaSuccess) return WK_ECUDA;
+  if (cudaFuncSetAttribute(attend_kernel<__nv_bfloat16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, at) != cudaSuccess) return WK_ECUDA;
+  if (cudaFuncSetAttribute(attend_kernel<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, at) != cudaSuccess) return WK_ECUDA;
+  if (cudaFuncSetAttribute(attend_kernel<__nv_bfloat16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, at) != cudaSuccess) return WK_ECUDA;
+  g_smem_configured = 1;
+  return 0;
+}
+
+extern "C" {
+
+int wk_version(void) { return 1; }
+
+int wk_kmeans_segments(const wk_index_view* ix, const wk_segment* segs, int n_segs,
+                       const wk_build_scratch* scr, int d, int store_bf16, int kmeans_iters,
+                       int blas_threads, int max_L, int max_k, void* stream) {
+  if (!ix || !segs || !scr || n_segs <= 0 || d <= 0 || d > 256 || (d & 3)) return WK_ECONFIG;
+  if (configure_smem()) return WK_ECUDA;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cudaMemcpyAsync(scr->segs_dev, segs, sizeof(wk_segment) * (size_t)n_segs, cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return WK_ECUDA;
+  const SegDesc* sd = scr->segs_dev;
+  km_prep_kernel<<<n_segs, 256, d * sizeof(float), s>>>(sd, scr->P, d);
+  WK_CHECK_LAUNCH();
+  const int smem_rows = ((200 * 1024) / 4 - d) / 2;
+  const size_t seed_smem = (size_t)(d + 2 * (max_L <= smem_rows ? max_L : 0)) * sizeof(float);
+  km_seed_kernel<<<n_segs, 512, seed_smem, s>>>(sd, scr->P, scr->C, scr->md, d, blas_threads,
+                                                 max_L <= smem_rows ? smem_rows : 0);
+  WK_CHECK_LAUNCH();
+  const dim3 ag((max_L + 63) / 64, n_segs);
+  const size_t asmem = (size_t)2 * d * 65 * sizeof(float);
+  const size_t usmem = (size_t)(2 * max_k + 1) * sizeof(int);
+  km_assign_kernel<<<ag, 256, asmem, s>>>(sd, scr->P, scr->C, scr->A, d);
+  km_assign_small_kernel<<<n_segs, 256, 0, s>>>(sd, scr->P, scr->C, scr->A, d);
+  WK_CHECK_LAUNCH();
+  for (int it = 0; it < kmeans_iters; it++) {
+    km_update_kernel<<<n_segs, 512, usmem, s>>>(sd, scr->P, scr->C, scr->A, scr->perm, scr->sims, d, 0);
+    km_assign_kernel<<<ag, 256, asmem, s>>>(sd, scr->P, scr->C, scr->A, d);
+    km_assign_small_kernel<<<n_segs, 256, 0, s>>>(sd, scr->P, scr->C, scr->A, d);
+    WK_CHECK_LAUNCH();
+  }
+  km_update_kernel<<<n_segs, 512, usmem, s>>>(sd, scr->P, scr->C, scr->A, scr->perm, scr->sims, d, 1);
+  if (store_bf16)
+    km_finalize_kernel<__nv_bfloat16><<<n_segs, 256, usmem, s>>>(sd, scr->A, scr->perm, *ix, d, scr->status);
+  else
+    km_finalize_kernel<float><<<n_segs, 256, usmem, s>>>(sd, scr->A, scr->perm, *ix, d, scr->status);
+  WK_CHECK_LAUNCH();
+  return 0;
+}
+
+int wk_append_tokens(const wk_steady_view* st, const float* k_new, const float* v_new, int U, int d,
+                     int store_bf16, void* stream) {
+  if (!st || U <= 0 || d <= 0) return WK_ECONFIG;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (store_bf16) append_kernel<__nv_bfloat16><<<U, 128, 0, s>>>(*st, k_new, v_new, d);
+  else append_kernel<float><<<U, 128, 0, s>>>(*st, k_new, v_new, d);
+  WK_CHECK_LAUNCH();
+  return 0;
+}
+
+int wk_score_topk(const wk_index_view* ix, const wk_step_view* sv, const wk_zone_params* zp, int U,
+                  int m_max, void* stream) {
+  if (!ix || !sv || !zp || U <= 0 || zp->G < 1 || zp->G > 8 || zp->d <= 0 || zp->d > 256 || (zp->d & 3))
+    return WK_ECONFIG;
+  if (configure_smem()) return WK_ECUDA;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (m_max > 0) {
+    dim3 g1((m_max + 63) / 64, U);
+    score_kernel<<<g1, 256, 0, s>>>(*ix, *sv, zp->d, zp->G);
+    WK_CHECK_LAUNCH();
+  }
+  SelParams p;
+  p.G = zp->G; p.d = zp->d; p.blas_threads = zp->blas_threads;
+  p.retrieval_fraction = zp->retrieval_fraction;
+  p.estimation_fraction = zp->estimation_fraction;
+  p.inv_sqrt_d = (float)(1.0 / sqrt((double)zp->d));
+  p.need_tail = zp->tail_denominator_only;
+  p.need_allc = zp->denominator_eq2;
+  select_kernel<<<U * zp->G, 512, select_smem_bytes(), s>>>(*ix, *sv, p);
+  WK_CHECK_LAUNCH();
+  union_kernel<<<U, 1024, 0, s>>>(*ix, *sv);
+  WK_CHECK_LAUNCH();
+  return 0;
+}
+
+int wk_tripartite_attn(const wk_index_view* ix, const wk_steady_view* st, const wk_step_view* sv,
+                       const wk_zone_params* zp, int U, int S, int store_bf16, void* stream) {
+  if (!ix || !st || !sv || !zp || U <= 0 || S <= 0 || zp->G < 1 || zp->G > 8 || zp->d > 256 || (zp->d & 3))
+    return WK_ECONFIG;
+  if (configure_smem()) return WK_ECUDA;
+  cudaStream_t s = (cudaStream_t)stream;
+  AttnParams p;
+  p.G = zp->G; p.d = zp->d;
+  p.inv_sqrt_d = (float)(1.0 / sqrt((double)zp->d));
+  p.tail_denominator_only = zp->tail_denominator_only;
+  p.denominator_eq2 = zp->denominator_eq2;
+  dim3 grid(S, U);
+  if (store_bf16)
+    attend_kernel<__nv_bfloat16, false><<<grid, 128, attend_smem_bytes(zp->d, 2), s>>>(*ix, *st, *sv, p, nullptr);
+  else
+    attend_kernel<float, false><<<grid, 128, attend_smem_bytes(zp->d, 4), s>>>(*ix, *st, *sv, p, nullptr);
+  WK_CHECK_LAUNCH();
+  merge_kernel<<<U * zp->G, 128, 0, s>>>(*sv, p, S);
+  WK_CHECK_LAUNCH();
+  return 0;
+}
+
+int wk_full_attn(const wk_index_view* ix, const wk_steady_view* st, const wk_step_view* sv,
+                 const int32_t* n_store, int U, int G, int d, int S, int store_bf16, void* stream) {
+  if (!ix || !st || !sv || !n_store || U <= 0 || S <= 0 || G < 1 || G > 8 || d > 256 || (d & 3))
+    return WK_ECONFIG;
+  if (configure_smem()) return WK_ECUDA;
+  cudaStream_t s = (cudaStream_t)stream;
+  StepView v = *sv;
+  v.tail = nullptr;
+  AttnParams p;
+  p.G = G; p.d = d;
+  p.inv_sqrt_d = (float)(1.0 / sqrt((double)d));
+  p.tail_denominator_only = 0;
+  p.denominator_eq2 = 0;
+  dim3 grid(S, U);
+  if (store_bf16)
+    attend_kernel<__nv_bfloat16, true><<<grid, 128, attend_smem_bytes(d, 2), s>>>(*ix, *st, v, p, n_store);
+  else
+    attend_kernel<float, true><<<grid, 128, attend_smem_bytes(d, 4), s>>>(*ix, *st, v, p, n_store);
+  WK_CHECK_LAUNCH();
+  merge_kernel<<<U * G, 128, 0, s>>>(v, p, S);
+  WK_CHECK_LAUNCH();
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,26 @@
+// decode_internal.h -- per-step device views for the decode kernels.
+#pragma once
+#include <stddef.h>
+#include <stdint.h>
+
+#include "wavekv_internal.h"
+
+namespace wk {
+using SteadyView = ::wk_steady_view;  // sinks + decode buffer (engine.py:87-96)
+using StepView = ::wk_step_view;      // per-step buffers
+
+struct SelParams {
+  int G, d, blas_threads;
+  double retrieval_fraction, estimation_fraction;
+  float inv_sqrt_d;
+  int need_tail, need_allc;
+};
+
+struct AttnParams {
+  int G, d;
+  float inv_sqrt_d;
+  int tail_denominator_only, denominator_eq2;
+};
+
+size_t attend_smem_bytes(int d, int elem);
+}  // namespace wk

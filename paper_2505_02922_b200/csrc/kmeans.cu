@@ -1,0 +1,439 @@
+// kmeans.cu -- segmented spherical k-means on B200 (prefill index build and
+// decode-time index updates).  Restates tierkv clustering.py:66-101 and
+// index.py:43-58 / 143-186 bit-exactly: the CPU reference's fp32/fp64
+// evaluation orders are reproduced with round-to-nearest intrinsics (see
+// common.cuh).  All segments of all (request, kv-head) units of a layer are
+// processed by one launch per phase.
+#include "common.cuh"
+#include "wavekv_internal.h"
+
+namespace wk {
+
+// ---------------------------------------------------------------------------
+// phase 1: centre by the fp32 column mean (sequential over rows, then / n)
+// and normalize rows (clustering.py:82, :16-23).
+// grid = n_segments, block = 256
+// ---------------------------------------------------------------------------
+__global__ void km_prep_kernel(const SegDesc* __restrict__ segs, float* __restrict__ P_all, int d) {
+  const SegDesc sg = segs[blockIdx.x];
+  if (sg.k <= 1) return;
+  extern __shared__ float sm_mean[];
+  const float* keys = sg.keys;
+  float* P = P_all + (size_t)sg.p_off * d;
+  for (int t = threadIdx.x; t < d; t += blockDim.x) {
+    float s = 0.f;
+    for (int i = 0; i < sg.L; i++) s = __fadd_rn(s, keys[(size_t)i * sg.key_stride + t]);
+    sm_mean[t] = __fdiv_rn(s, (float)sg.L);
+  }
+  __syncthreads();
+  for (size_t idx = threadIdx.x; idx < (size_t)sg.L * d; idx += blockDim.x) {
+    size_t i = idx / d, t = idx % d;
+    P[idx] = __fsub_rn(keys[i * sg.key_stride + t], sm_mean[t]);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < sg.L; i += blockDim.x) {
+    float* row = P + (size_t)i * d;
+    float nr = row_norm_f32(row, d);
+    if (nr != 0.0f) {
+      for (int t = 0; t < d; t++) row[t] = __fdiv_rn(row[t], nr);
+    } else {
+      for (int t = 0; t < d; t++) row[t] = 0.f;
+      row[0] = 1.0f;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// phase 2: k-means++ seeding under cosine distance (clustering.py:26-43).
+// One CTA per segment runs the k-1 sequential steps; the sgemv of each step
+// is spread over the CTA with the OpenBLAS row recipe, the fp32 cumsum is the
+// reference's sequential chain (thread 0), the draw is numpy's PCG64 stream.
+// grid = n_segments, block = 512, dyn smem = d floats (+2L floats if it fits)
+// ---------------------------------------------------------------------------
+__global__ void km_seed_kernel(const SegDesc* __restrict__ segs, const float* __restrict__ P_all,
+                               float* __restrict__ C_all, float* __restrict__ scratch_all,
+                               int d, int blas_threads, int smem_rows) {
+  const SegDesc sg = segs[blockIdx.x];
+  if (sg.k <= 1) return;
+  extern __shared__ float sm[];
+  float* cent = sm;  // d floats: current centroid
+  const int L = sg.L;
+  float *md, *cdf;
+  if (L <= smem_rows) {
+    md = sm + d;
+    cdf = md + L;
+  } else {
+    md = scratch_all + (size_t)sg.p_off * 2;
+    cdf = md + L;
+  }
+  const float* P = P_all + (size_t)sg.p_off * d;
+  float* C = C_all + (size_t)sg.c_off * d;
+  __shared__ Pcg64 g;
+  __shared__ long long s_idx;
+  if (threadIdx.x == 0) {
+    g.hi = sg.rng[0]; g.lo = sg.rng[1]; g.ihi = sg.rng[2]; g.ilo = sg.rng[3];
+    g.has32 = 0; g.u32 = 0;
+    s_idx = pcg_integers(g, L);
+  }
+  __syncthreads();
+  for (int c = 0; c < sg.k; c++) {
+    const long long idx = s_idx;
+    for (int t = threadIdx.x; t < d; t += blockDim.x) {
+      float v = P[(size_t)idx * d + t];
+      cent[t] = v;
+      C[(size_t)c * d + t] = v;
+    }
+    __syncthreads();
+    if (c == sg.k - 1) break;
+    for (int i = threadIdx.x; i < L; i += blockDim.x) {
+      int cls = gemv_row_class(i, L, d, blas_threads);
+      float dot = sgemv_row(P + (size_t)i * d, cent, d, cls);
+      float v = __fsub_rn(1.0f, dot);
+      v = v < 0.f ? 0.f : v;
+      if (c == 0) md[i] = v;
+      else if (!(md[i] <= v)) md[i] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float s = md[0];
+      cdf[0] = s;
+      for (int i = 1; i < L; i++) { s = __fadd_rn(s, md[i]); cdf[i] = s; }
+      long long nidx;
+      if (s <= 0.0f) {
+        nidx = pcg_integers(g, L);
+      } else {
+        float u = (float)pcg_next_double(g);
+        float thr = __fmul_rn(u, s);
+        int lo = 0, hi = L;
+        while (lo < hi) { int mid = (lo + hi) >> 1; if (cdf[mid] <= thr) lo = mid + 1; else hi = mid; }
+        nidx = lo > L - 1 ? L - 1 : lo;
+      }
+      s_idx = nidx;
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// phase 3: assignment = argmax(points @ centroids.T) (clustering.py:85,96).
+// Every score is the reference's sequential fp32 FMA chain over t; register
+// tiled 64 points x 64 centroids per CTA iteration, transposed smem tiles.
+// grid = (ceil(Lmax/64), n_segments), block = 256, dyn smem = 2*d*65 floats
+// ---------------------------------------------------------------------------
+constexpr int AT = 64;  // tile edge
+__global__ void __launch_bounds__(256) km_assign_kernel(const SegDesc* __restrict__ segs,
+                                                         const float* __restrict__ P_all,
+                                                         const float* __restrict__ C_all,
+                                                         int32_t* __restrict__ A_all, int d) {
+  const SegDesc sg = segs[blockIdx.y];
+  if (sg.k <= 1) return;
+  if ((long long)sg.L * sg.k <= 1200 && d >= 32) return;  // small-kernel path elsewhere
+  const int p0 = blockIdx.x * AT;
+  if (p0 >= sg.L) return;
+  extern __shared__ float sm[];
+  float* PT = sm;                  // [d][AT+1]
+  float* CT = sm + d * (AT + 1);   // [d][AT+1]
+  const float* P = P_all + (size_t)sg.p_off * d;
+  const float* C = C_all + (size_t)sg.c_off * d;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int np = min(AT, sg.L - p0);
+  for (int idx = threadIdx.x; idx < AT * d; idx += 256) {
+    int p = idx / d, t = idx % d;
+    PT[t * (AT + 1) + p] = p < np ? P[(size_t)(p0 + p) * d + t] : 0.f;
+  }
+  float best[4];
+  int bidx[4];
+#pragma unroll
+  for (int i = 0; i < 4; i++) { best[i] = -INFINITY; bidx[i] = 0x7fffffff; }
+  for (int c0 = 0; c0 < sg.k; c0 += AT) {
+    const int nc = min(AT, sg.k - c0);
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < AT * d; idx += 256) {
+      int c = idx / d, t = idx % d;
+      CT[t * (AT + 1) + c] = c < nc ? C[(size_t)(c0 + c) * d + t] : 0.f;
+    }
+    __syncthreads();
+    float acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+#pragma unroll
+      for (int j = 0; j < 4; j++) acc[i][j] = 0.f;
+    for (int t = 0; t < d; t++) {
+      float pv[4], cv[4];
+#pragma unroll
+      for (int i = 0; i < 4; i++) pv[i] = PT[t * (AT + 1) + ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; j++) cv[j] = CT[t * (AT + 1) + tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; i++)
+#pragma unroll
+        for (int j = 0; j < 4; j++) acc[i][j] = __fmaf_rn(pv[i], cv[j], acc[i][j]);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      int c = c0 + tx * 4 + j;
+      if (tx * 4 + j < nc) {
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+          if (acc[i][j] > best[i]) { best[i] = acc[i][j]; bidx[i] = c; }
+      }
+    }
+  }
+  // reduce across the 16 tx threads of each point group (ties -> smaller id)
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    float b = best[i];
+    int bi = bidx[i];
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {
+      float ob = __shfl_xor_sync(0xffffffffu, b, o, 16);
+      int oi = __shfl_xor_sync(0xffffffffu, bi, o, 16);
+      if (ob > b || (ob == b && oi < bi)) { b = ob; bi = oi; }
+    }
+    int p = ty * 4 + i;
+    if (tx == 0 && p < np) A_all[sg.p_off + p0 + p] = bi;
+  }
+}
+
+// OpenBLAS SkylakeX small-matrix TN kernel model (n*k <= 1200, d >= 32):
+// 16-lane FMA accumulator, adjacent-pair lane tree except the corner block.
+__device__ float small_tn_score(const float* p, const float* c, int d, bool corner) {
+  float a[16];
+#pragma unroll
+  for (int l = 0; l < 16; l++) a[l] = 0.f;
+  for (int t = 0; t < d; t++) a[t & 15] = __fmaf_rn(p[t], c[t], a[t & 15]);
+  const int adj[4] = {0, 1, 2, 3}, red[4] = {3, 2, 1, 0};
+  for (int lev = 0; lev < 4; lev++) {
+    int b = 1 << (corner ? red[lev] : adj[lev]);
+    for (int l = 0; l < 16; l++)
+      if (!(l & b)) a[l] = __fadd_rn(a[l], a[l | b]);
+  }
+  return a[0];
+}
+
+__global__ void km_assign_small_kernel(const SegDesc* __restrict__ segs, const float* __restrict__ P_all,
+                                       const float* __restrict__ C_all, int32_t* __restrict__ A_all, int d) {
+  const SegDesc sg = segs[blockIdx.x];
+  if (sg.k <= 1) return;
+  if (!((long long)sg.L * sg.k <= 1200 && d >= 32)) return;
+  const float* P = P_all + (size_t)sg.p_off * d;
+  const float* C = C_all + (size_t)sg.c_off * d;
+  const int n4 = sg.L & ~3, k4 = sg.k & ~3;
+  for (int i = threadIdx.x; i < sg.L; i += blockDim.x) {
+    float best = -INFINITY;
+    int bi = 0;
+    for (int c = 0; c < sg.k; c++) {
+      float s = small_tn_score(P + (size_t)i * d, C + (size_t)c * d, d, i >= n4 && c >= k4);
+      if (c == 0 || s > best) { best = s; bi = c; }
+    }
+    A_all[sg.p_off + i] = bi;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// helpers shared by update/finalize: counts + stable counting sort of the
+// points by cluster (ascending point index within a cluster).
+// smem layout: cnt[k+1] (int), cursor[k] (int)
+// ---------------------------------------------------------------------------
+__device__ void stable_bucket(const int32_t* A, int L, int k, int* cnt, int* cursor, int32_t* perm) {
+  for (int c = threadIdx.x; c <= k; c += blockDim.x) cnt[c] = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < L; i += blockDim.x) atomicAdd(&cnt[A[i] + 1], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int c = 0; c < k; c++) cnt[c + 1] += cnt[c];
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < k; c += blockDim.x) cursor[c] = 0;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    for (int base = 0; base < L; base += 32) {
+      int i = base + lane;
+      bool act = i < L;
+      unsigned am = __ballot_sync(0xffffffffu, act);
+      if (act) {
+        int a = A[i];
+        unsigned peers = __match_any_sync(am, a);
+        int rank = __popc(peers & ((1u << lane) - 1u));
+        int pos = cnt[a] + cursor[a] + rank;
+        __syncwarp(am);
+        perm[pos] = i;
+        if ((31 - __clz(peers)) == lane) cursor[a] += __popc(peers);
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+}
+
+// _repair_empty (clustering.py:46-63); serial over empties, parallel argmin.
+__device__ void repair_empty(const float* P, int L, int d, int32_t* A, float* C, int k, int* counts,
+                             float* sims, int* s_flag) {
+  __shared__ int s_any;
+  __shared__ float s_bv[32];
+  __shared__ int s_bi[32];
+  if (threadIdx.x == 0) {
+    s_any = 0;
+    for (int c = 0; c < k; c++) if (counts[c] == 0) { s_any = 1; break; }
+  }
+  __syncthreads();
+  if (!s_any) return;
+  for (int i = threadIdx.x; i < L; i += blockDim.x)
+    sims[i] = einsum_row(P + (size_t)i * d, C + (size_t)A[i] * d, d);
+  __syncthreads();
+  for (int c = 0; c < k; c++) {
+    if (counts[c] != 0) continue;  // list of empties is fixed up front; repair never empties
+    float bv = INFINITY;
+    int bi = 0x7fffffff;
+    for (int i = threadIdx.x; i < L; i += blockDim.x) {
+      float cand = counts[A[i]] > 1 ? sims[i] : INFINITY;
+      if (cand < bv || (cand == bv && i < bi)) { bv = cand; bi = i; }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov < bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    if ((threadIdx.x & 31) == 0) { s_bv[threadIdx.x >> 5] = bv; s_bi[threadIdx.x >> 5] = bi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int nw = (blockDim.x + 31) >> 5;
+      for (int w = 1; w < nw; w++)
+        if (s_bv[w] < bv || (s_bv[w] == bv && s_bi[w] < bi)) { bv = s_bv[w]; bi = s_bi[w]; }
+      int victim = bi;
+      counts[A[victim]] -= 1;
+      A[victim] = c;
+      counts[c] = 1;
+      sims[victim] = 1.0f;
+      s_bi[0] = victim;
+    }
+    __syncthreads();
+    int victim = s_bi[0];
+    for (int t = threadIdx.x; t < d; t += blockDim.x) C[(size_t)c * d + t] = P[(size_t)victim * d + t];
+    __syncthreads();
+  }
+  if (s_flag) { /* reserved */ }
+}
+
+// ---------------------------------------------------------------------------
+// phase 4: Lloyd update (clustering.py:86-95): counts, fp64 per-cluster sums
+// in ascending point order (np.bincount(weights=...)), divide -> fp32,
+// normalize, repair.  final=1: only counts + repair (clustering.py:99-100).
+// grid = n_segments, block = 512, dyn smem = (2k+1) ints
+// ---------------------------------------------------------------------------
+__global__ void km_update_kernel(const SegDesc* __restrict__ segs, const float* __restrict__ P_all,
+                                 float* __restrict__ C_all, int32_t* __restrict__ A_all,
+                                 int32_t* __restrict__ perm_all, float* __restrict__ sims_all,
+                                 int d, int final_pass) {
+  const SegDesc sg = segs[blockIdx.x];
+  if (sg.k <= 1) return;
+  extern __shared__ int smi[];
+  int* cnt = smi;            // k+1
+  int* cursor = smi + sg.k + 1;  // k
+  const float* P = P_all + (size_t)sg.p_off * d;
+  float* C = C_all + (size_t)sg.c_off * d;
+  int32_t* A = A_all + sg.p_off;
+  int32_t* perm = perm_all + sg.p_off;
+  float* sims = sims_all + sg.p_off;
+  stable_bucket(A, sg.L, sg.k, cnt, cursor, perm);
+  // counts[c] = cnt[c+1]-cnt[c]; keep in cursor[] (reused) for repair
+  for (int c = threadIdx.x; c < sg.k; c += blockDim.x) cursor[c] = cnt[c + 1] - cnt[c];
+  __syncthreads();
+  if (!final_pass) {
+    for (int idx = threadIdx.x; idx < sg.k * d; idx += blockDim.x) {
+      int c = idx / d, t = idx % d;
+      int b = cnt[c], e = cnt[c + 1];
+      if (e > b) {
+        double s = 0.0;
+        for (int j = b; j < e; j++) s = __dadd_rn(s, (double)P[(size_t)perm[j] * d + t]);
+        C[(size_t)c * d + t] = __double2float_rn(__ddiv_rn(s, (double)(e - b)));
+      }
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < sg.k; c += blockDim.x) {
+      float* row = C + (size_t)c * d;
+      float nr = row_norm_f32(row, d);
+      if (nr != 0.0f) {
+        for (int t = 0; t < d; t++) row[t] = __fdiv_rn(row[t], nr);
+      } else {
+        for (int t = 0; t < d; t++) row[t] = 0.f;
+        row[0] = 1.0f;
+      }
+    }
+    __syncthreads();
+  }
+  repair_empty(P, sg.L, d, A, C, sg.k, cursor, sims, nullptr);
+}
+
+// ---------------------------------------------------------------------------
+// phase 5: finalize_cluster (index.py:43-58) + pack the cluster-private store
+// (store.py:69-90).  fp64 mean of the raw member keys and fp64 value sums in
+// ascending token order; members written cluster-contiguously to the store.
+// grid = n_segments, block = 256, dyn smem = (2k+1) ints
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void km_finalize_kernel(const SegDesc* __restrict__ segs, const int32_t* __restrict__ A_all,
+                                   int32_t* __restrict__ perm_all, IndexView ix, int d,
+                                   int* __restrict__ status) {
+  const SegDesc sg = segs[blockIdx.x];
+  extern __shared__ int smi[];
+  int* cnt = smi;
+  int* cursor = smi + sg.k + 1;
+  int32_t* perm = perm_all + sg.p_off;
+  if (sg.k <= 1) {
+    // k == 1 shortcut (clustering.py:79-80): everything in cluster 0
+    if (threadIdx.x == 0) { cnt[0] = 0; cnt[1] = sg.L; }
+    for (int i = threadIdx.x; i < sg.L; i += blockDim.x) perm[i] = i;
+    __syncthreads();
+  } else {
+    stable_bucket(A_all + sg.p_off, sg.L, sg.k, cnt, cursor, perm);
+  }
+  const size_t u = sg.unit;
+  T* sk = (T*)ix.store_k + u * ix.s_cap * d;
+  T* sv = (T*)ix.store_v + u * ix.s_cap * d;
+  int32_t* stok = ix.store_tok + u * ix.s_cap;
+  for (int c = threadIdx.x; c < sg.k; c += blockDim.x) {
+    int s = cnt[c + 1] - cnt[c];
+    if (s == 0) set_status(status, kErrEmptyCluster);
+    size_t cid = (size_t)sg.cid_base + c;
+    ix.cl_off[u * ix.m_cap + cid] = sg.row_base + cnt[c];
+    ix.cl_size[u * ix.m_cap + cid] = s;
+  }
+  for (int j = threadIdx.x; j < sg.L; j += blockDim.x) stok[sg.row_base + j] = sg.tok_base + perm[j];
+  for (size_t idx = threadIdx.x; idx < (size_t)sg.L * d; idx += blockDim.x) {
+    size_t j = idx / d, t = idx % d;
+    size_t src = (size_t)perm[j] * sg.key_stride + t;
+    sk[(size_t)(sg.row_base + j) * d + t] = KV<T>::from_f(sg.keys[src]);
+    sv[(size_t)(sg.row_base + j) * d + t] = KV<T>::from_f(sg.values[src]);
+  }
+  for (int idx = threadIdx.x; idx < sg.k * d; idx += blockDim.x) {
+    int c = idx / d, t = idx % d;
+    int b = cnt[c], e = cnt[c + 1];
+    double ks = 0.0, vs = 0.0;
+    for (int j = b; j < e; j++) {
+      size_t src = (size_t)perm[j] * sg.key_stride + t;
+      ks = __dadd_rn(ks, (double)sg.keys[src]);
+      vs = __dadd_rn(vs, (double)sg.values[src]);
+    }
+    double mean = e > b ? __ddiv_rn(ks, (double)(e - b)) : 0.0;
+    size_t row = u * ix.m_cap + (size_t)sg.cid_base + c;
+    ix.C64[row * d + t] = mean;
+    ix.C32[row * d + t] = __double2float_rn(mean);
+    ix.VS32[row * d + t] = __double2float_rn(vs);
+    if (ix.VS64) ix.VS64[row * d + t] = vs;
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < sg.k; c += blockDim.x) {
+    size_t row = u * ix.m_cap + (size_t)sg.cid_base + c;
+    const float* cr = ix.C32 + row * d;
+    float s = 0.f;
+    for (int t = 0; t < d; t++) s = fmaf(cr[t], cr[t], s);
+    ix.Cnorm[row] = sqrtf(s);
+  }
+}
+
+template __global__ void km_finalize_kernel<float>(const SegDesc*, const int32_t*, int32_t*, IndexView, int, int*);
+template __global__ void km_finalize_kernel<__nv_bfloat16>(const SegDesc*, const int32_t*, int32_t*, IndexView, int, int*);
+
+}  // namespace wk

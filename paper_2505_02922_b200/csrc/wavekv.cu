@@ -1,0 +1,5 @@
+// wavekv.cu -- unity translation unit: one nvcc invocation builds libwavekv.so
+// (sm_100a) from the kernel sources and the C ABI.
+#include "kmeans.cu"
+#include "decode.cu"
+#include "abi.cu"

@@ -1,0 +1,383 @@
+"""Batched B200 wave-index state for one attention layer.
+
+A ``WaveLayer`` holds U (request, kv-head) units, each serving G query heads
+(GQA).  Everything lives in HBM; the host keeps only integer bookkeeping
+(lengths, cluster counts, update schedule) and launches the sm_100a kernels of
+libwavekv.so through the C ABI (include/wavekv.h):
+
+  prefill  -> wk_kmeans_segments      (index.py:153-166 segmented build)
+  decode   -> wk_append_tokens        (engine.py:178-182)
+              wk_score_topk           (index.py:61-93 rank + plan_zones)
+              wk_tripartite_attn      (attention.py:67-148, engine.py:150-172)
+              [every update_segment tokens] wk_kmeans_segments
+                                      (index.py:168-186 decode-time update)
+
+Per-unit semantics are exactly ``tierkv.HeadEngine`` (engine.py:40-237) with
+the index shared by the G heads of a kv head (the reference seeds do not
+depend on the head, index.py:162, so each head's reference engine builds the
+identical index).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .config import EngineConfig, round_half_up
+from .errors import ConfigError
+
+_SEED_CACHE: dict = {}
+
+
+def pcg64_words(rng_seed: int, kind: int, idx: int):
+    """numpy PCG64 state of default_rng(SeedSequence([rng_seed, kind, idx]))
+    (index.py:162/181 -> clustering.py:81).  Host-side seed derivation; the
+    stream itself is generated on the device."""
+    key = (int(rng_seed), int(kind), int(idx))
+    w = _SEED_CACHE.get(key)
+    if w is None:
+        st = np.random.PCG64(np.random.SeedSequence(list(key))).state["state"]
+        s, i = int(st["state"]), int(st["inc"])
+        m = (1 << 64) - 1
+        w = (s >> 64, s & m, i >> 64, i & m)
+        _SEED_CACHE[key] = w
+    return w
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+@dataclass
+class UnitState:
+    """Host mirror of one unit's integer bookkeeping (engine.py:44-57)."""
+    total: int = 0            # tokens seen (HeadEngine.total_tokens)
+    n_sink: int = 0
+    buffer_start: int = 0     # token id of the oldest buffered token
+    m: int = 0                # clusters
+    store_fill: int = 0       # store rows used
+    update_round: int = 0     # ClusterIndex._update_round
+    n_steady: int = 0         # sinks + buffer rows
+
+
+class WaveLayer:
+    """U units x G heads of one layer; all tensors on ``device``."""
+
+    def __init__(self, cfg: EngineConfig, U: int, G: int, d: int, *, max_prefill: int,
+                 max_decode: int = 1024, store_dtype=torch.bfloat16, device="cuda",
+                 blas_threads: int = 1, splits: int | None = None, keep_vs64: bool = False,
+                 with_elist: bool = False):
+        self.cfg = cfg.validate()
+        ic = cfg.index
+        if d <= 0 or d % 4 or d > 256:
+            raise ConfigError(f"head dim {d} unsupported (need d % 4 == 0, d <= 256)")
+        if not 1 <= G <= 8:
+            raise ConfigError(f"G={G} query heads per kv head unsupported (1..8)")
+        if store_dtype not in (torch.bfloat16, torch.float32):
+            raise ConfigError("store_dtype must be bfloat16 or float32")
+        self.U, self.G, self.d = U, G, d
+        self.dev = torch.device(device)
+        if self.dev.type != "cuda":
+            raise ConfigError("WaveLayer runs on a CUDA device only (no CPU fallback)")
+        self.store_dtype = store_dtype
+        self.store_bf16 = int(store_dtype == torch.bfloat16)
+        self.blas_threads = int(blas_threads)
+        self.L = _lib.lib()
+        # ---- capacities ----
+        n_idx = max(0, max_prefill - min(ic.sink_tokens, max_prefill) - ic.local_window)
+        n_upd = max_decode // ic.update_segment + 1
+        k_upd = math.ceil(ic.update_segment / ic.centroid_ratio)
+        m_pref = sum(math.ceil(min(ic.segment_size, n_idx - s) / ic.centroid_ratio)
+                     for s in range(0, n_idx, ic.segment_size))
+        self.m_cap = max(1, m_pref + n_upd * k_upd)
+        self.s_cap = max(1, n_idx + n_upd * ic.update_segment)
+        self.t_cap = ic.sink_tokens + ic.update_segment + ic.local_window + max(0, ic.local_window) + 8
+        self.t_cap = max(self.t_cap, min(max_prefill, ic.sink_tokens + ic.local_window) + 8)
+        self.r_cap = max(1, min(self.m_cap, round_half_up(ic.retrieval_fraction * self.m_cap) + 2))
+        self.e_cap = max(1, min(self.m_cap, round_half_up(ic.estimation_fraction * self.m_cap) + 2))
+        self.S = splits or max(1, min(64, -(-1024 // U)))
+        dev, f32, i32 = self.dev, torch.float32, torch.int32
+        # ---- index arrays ----
+        self.store_k = torch.zeros((U, self.s_cap, d), dtype=store_dtype, device=dev)
+        self.store_v = torch.zeros((U, self.s_cap, d), dtype=store_dtype, device=dev)
+        self.store_tok = torch.full((U, self.s_cap), -1, dtype=i32, device=dev)
+        self.cl_off = torch.zeros((U, self.m_cap), dtype=i32, device=dev)
+        self.cl_size = torch.zeros((U, self.m_cap), dtype=i32, device=dev)
+        self.C64 = torch.zeros((U, self.m_cap, d), dtype=torch.float64, device=dev)
+        self.C32 = torch.zeros((U, self.m_cap, d), dtype=f32, device=dev)
+        self.Cnorm = torch.zeros((U, self.m_cap), dtype=f32, device=dev)
+        self.VS32 = torch.zeros((U, self.m_cap, d), dtype=f32, device=dev)
+        self.VS64 = (torch.zeros((U, self.m_cap, d), dtype=torch.float64, device=dev)
+                     if keep_vs64 else None)
+        # ---- steady zone ----
+        self.st_k = torch.zeros((U, self.t_cap, d), dtype=store_dtype, device=dev)
+        self.st_v = torch.zeros((U, self.t_cap, d), dtype=store_dtype, device=dev)
+        self.st_tok = torch.full((U, self.t_cap), -1, dtype=i32, device=dev)
+        self.st_n = torch.zeros(U, dtype=i32, device=dev)
+        self.next_tok = torch.zeros(U, dtype=i32, device=dev)
+        # ---- step buffers ----
+        self.m_dev = torch.zeros(U, dtype=i32, device=dev)
+        self.scores = torch.zeros((U, G, self.m_cap), dtype=f32, device=dev)
+        self.rlist = torch.zeros((U, G, self.r_cap), dtype=i32, device=dev)
+        self.elist = torch.zeros((U, G, self.e_cap), dtype=i32, device=dev) if with_elist else None
+        self.nr = torch.zeros(U, dtype=i32, device=dev)
+        self.ne = torch.zeros(U, dtype=i32, device=dev)
+        self.zmask = torch.zeros((U, self.m_cap), dtype=i32, device=dev)
+        self.ru_cap = min(self.m_cap, G * self.r_cap)
+        self.eu_cap = min(self.m_cap, G * self.e_cap)
+        self.ru_ids = torch.zeros((U, self.ru_cap), dtype=i32, device=dev)
+        self.ru_mask = torch.zeros((U, self.ru_cap), dtype=torch.uint8, device=dev)
+        self.ru_pre = torch.zeros((U, self.ru_cap + 1), dtype=i32, device=dev)
+        self.eu_ids = torch.zeros((U, self.eu_cap), dtype=i32, device=dev)
+        self.eu_mask = torch.zeros((U, self.eu_cap), dtype=torch.uint8, device=dev)
+        self.cnt = torch.zeros((U, 4), dtype=i32, device=dev)
+        self.tail = torch.zeros((U, G, 4), dtype=f32, device=dev)
+        self.part = torch.zeros((U, self.S, G, 3, 2 + d), dtype=f32, device=dev)
+        self.out = torch.zeros((U, G, d), dtype=f32, device=dev)
+        self.logden = torch.zeros((U, G), dtype=f32, device=dev)
+        self.cov = torch.zeros((U, G), dtype=f32, device=dev)
+        self.status = torch.zeros(1, dtype=i32, device=dev)
+        self.n_store_dev = torch.zeros(U, dtype=i32, device=dev)
+        self.units = [UnitState() for _ in range(U)]
+        self._q = None
+        self._zp = _lib.ZoneParamsC(G, d, self.blas_threads, ic.retrieval_fraction,
+                                    ic.estimation_fraction, int(ic.tail_mode == "denominator_only"),
+                                    int(cfg.denominator_mode == "eq2"))
+        self._ixv = _lib.IndexViewC(
+            _ptr(self.store_k), _ptr(self.store_v), _ptr(self.store_tok), _ptr(self.cl_off),
+            _ptr(self.cl_size), _ptr(self.C64), _ptr(self.C32), _ptr(self.Cnorm), _ptr(self.VS32),
+            _ptr(self.VS64), self.s_cap, self.m_cap)
+        self._stv = _lib.SteadyViewC(_ptr(self.st_k), _ptr(self.st_v), _ptr(self.st_tok),
+                                     _ptr(self.st_n), _ptr(self.next_tok), self.t_cap)
+        self.prefilled = False
+
+    # ------------------------------------------------------------------ views
+    def _step_view(self, q: torch.Tensor) -> _lib.StepViewC:
+        return _lib.StepViewC(
+            _ptr(q), _ptr(self.m_dev), _ptr(self.scores), _ptr(self.rlist), _ptr(self.elist),
+            _ptr(self.nr), _ptr(self.ne), _ptr(self.zmask), _ptr(self.ru_ids), _ptr(self.ru_mask),
+            _ptr(self.ru_pre), _ptr(self.eu_ids), _ptr(self.eu_mask), _ptr(self.cnt),
+            _ptr(self.tail), _ptr(self.part), _ptr(self.out), _ptr(self.logden), _ptr(self.cov),
+            _ptr(self.status), self.r_cap, self.e_cap, self.ru_cap, self.eu_cap)
+
+    # --------------------------------------------------------------- clustering
+    def _run_segments(self, segs: list[dict]):
+        """Cluster + finalize + pack a list of segments (one wk_kmeans_segments
+        call per chunk bounded by a scratch budget)."""
+        d = self.d
+        budget = 1 << 26  # points per chunk (scratch ~ 0.6 KB/point at d=128)
+        i = 0
+        while i < len(segs):
+            chunk, tot = [], 0
+            while i < len(segs) and (not chunk or tot + segs[i]["L"] <= budget):
+                chunk.append(segs[i]); tot += segs[i]["L"]; i += 1
+            sumL = sum(s["L"] for s in chunk)
+            sumK = sum(max(1, s["k"]) for s in chunk)
+            dev = self.dev
+            P = torch.empty((sumL, d), dtype=torch.float32, device=dev)
+            C = torch.empty((sumK, d), dtype=torch.float32, device=dev)
+            A = torch.zeros(sumL, dtype=torch.int32, device=dev)
+            perm = torch.empty(sumL, dtype=torch.int32, device=dev)
+            sims = torch.empty(sumL, dtype=torch.float32, device=dev)
+            md = torch.empty(2 * sumL, dtype=torch.float32, device=dev)
+            segs_dev = torch.empty(len(chunk) * ctypes.sizeof(_lib.SegmentC), dtype=torch.uint8,
+                                   device=dev)
+            arr = (_lib.SegmentC * len(chunk))()
+            po = co = 0
+            for j, s in enumerate(chunk):
+                a = arr[j]
+                a.keys, a.values, a.key_stride = s["keys"], s["values"], s["stride"]
+                a.L, a.k, a.unit = s["L"], s["k"], s["unit"]
+                a.cid_base, a.row_base, a.tok_base = s["cid_base"], s["row_base"], s["tok_base"]
+                a.p_off, a.c_off = po, co
+                for t in range(4):
+                    a.rng[t] = s["rng"][t]
+                po += s["L"]; co += max(1, s["k"])
+            scr = _lib.BuildScratchC(_ptr(P), _ptr(C), _ptr(A), _ptr(perm), _ptr(sims), _ptr(md),
+                                     _ptr(segs_dev), _ptr(self.status))
+            rc = self.L.wk_kmeans_segments(
+                ctypes.byref(self._ixv), arr, len(chunk), ctypes.byref(scr), d, self.store_bf16,
+                self.cfg.index.kmeans_iters, self.blas_threads, max(s["L"] for s in chunk),
+                max(max(1, s["k"]) for s in chunk), ctypes.c_void_p(_stream()))
+            _lib.check(rc, "wk_kmeans_segments")
+            # keep scratch alive until the kernels ran
+            torch.cuda.current_stream().synchronize()
+            del P, C, A, perm, sims, md, segs_dev
+
+    # ------------------------------------------------------------------ prefill
+    def prefill(self, keys: torch.Tensor, values: torch.Tensor, lengths=None):
+        """keys/values: [U, n, d] float32 on the device (HeadEngine.prefill,
+        engine.py:110-138).  ``lengths`` optionally gives per-unit prompt
+        lengths (rows beyond are ignored)."""
+        if self.prefilled:
+            raise ConfigError("prefill called twice")
+        U, d, ic = self.U, self.d, self.cfg.index
+        if keys.dim() != 3 or keys.shape != values.shape or keys.shape[0] != U or keys.shape[2] != d:
+            raise ConfigError(f"bad prefill shapes {tuple(keys.shape)} / {tuple(values.shape)}")
+        keys = keys.to(self.dev, torch.float32).contiguous()
+        values = values.to(self.dev, torch.float32).contiguous()
+        n_all = keys.shape[1]
+        lengths = [n_all] * U if lengths is None else [int(x) for x in lengths]
+        if any(n < 1 or n > n_all for n in lengths):
+            raise ConfigError("bad prefill lengths")
+        segs = []
+        for u, n in enumerate(lengths):
+            st = self.units[u]
+            st.total = n
+            st.n_sink = min(ic.sink_tokens, n)
+            index_end = max(st.n_sink, n - ic.local_window)
+            st.buffer_start = index_end
+            L = index_end - st.n_sink
+            if L > self.s_cap:
+                raise ConfigError("prefill longer than the configured capacity")
+            cid = 0
+            for seg_idx, s0 in enumerate(range(0, L, ic.segment_size)):
+                ln = min(ic.segment_size, L - s0)
+                k = math.ceil(ln / ic.centroid_ratio)
+                base = (u * n_all + st.n_sink + s0) * d
+                segs.append(dict(keys=keys.data_ptr() + 4 * base, values=values.data_ptr() + 4 * base,
+                                 stride=d, L=ln, k=k, unit=u, cid_base=cid, row_base=s0,
+                                 tok_base=st.n_sink + s0, rng=pcg64_words(ic.rng_seed, 1, seg_idx)))
+                cid += k
+            st.m = cid
+            st.store_fill = L
+            st.n_steady = st.n_sink + (n - index_end)
+            # steady rows: sinks then the window (engine.py:126-130)
+            rows = list(range(st.n_sink)) + list(range(index_end, n))
+            if rows:
+                idx = torch.tensor(rows, device=self.dev, dtype=torch.long)
+                self.st_k[u, : len(rows)] = keys[u, idx].to(self.store_dtype)
+                self.st_v[u, : len(rows)] = values[u, idx].to(self.store_dtype)
+                self.st_tok[u, : len(rows)] = idx.to(torch.int32)
+        if self.m_cap < max(s.m for s in self.units):
+            raise ConfigError("cluster capacity exceeded")
+        if segs:
+            self._run_segments(segs)
+        self.st_n.copy_(torch.tensor([s.n_steady for s in self.units], dtype=torch.int32))
+        self.next_tok.copy_(torch.tensor([s.total for s in self.units], dtype=torch.int32))
+        self.m_dev.copy_(torch.tensor([s.m for s in self.units], dtype=torch.int32))
+        self.n_store_dev.copy_(torch.tensor([s.store_fill for s in self.units], dtype=torch.int32))
+        self.check_status("prefill")
+        self.prefilled = True
+        return self
+
+    # ------------------------------------------------------------------- decode
+    def decode(self, q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor,
+               allow_update: bool = True):
+        """One decode step for every unit (HeadEngine.decode_step,
+        engine.py:174-232).  q: [U, G, d], k_new/v_new: [U, d] float32 device
+        tensors.  Returns device views (out [U,G,d], logden [U,G], cov [U,G])
+        valid until the next call."""
+        if not self.prefilled:
+            raise ConfigError("decode_step before prefill")
+        self.launch_step(q, k_new, v_new)
+        for s in self.units:
+            s.total += 1
+            s.n_steady += 1
+        if allow_update:
+            self.maybe_update()
+        return self.out, self.logden, self.cov
+
+    def launch_step(self, q, k_new, v_new):
+        """Kernel launches of one decode step only (graph-capturable)."""
+        q = q if (q.dtype == torch.float32 and q.is_contiguous()) else q.float().contiguous()
+        self._q = q
+        stream = ctypes.c_void_p(_stream())
+        L = self.L
+        _lib.check(L.wk_append_tokens(ctypes.byref(self._stv), _ptr(k_new), _ptr(v_new), self.U,
+                                      self.d, self.store_bf16, stream), "wk_append_tokens")
+        sv = self._step_view(q)
+        m_max = max(s.m for s in self.units)
+        _lib.check(L.wk_score_topk(ctypes.byref(self._ixv), ctypes.byref(sv), ctypes.byref(self._zp),
+                                   self.U, m_max, stream), "wk_score_topk")
+        _lib.check(L.wk_tripartite_attn(ctypes.byref(self._ixv), ctypes.byref(self._stv),
+                                        ctypes.byref(sv), ctypes.byref(self._zp), self.U, self.S,
+                                        self.store_bf16, stream), "wk_tripartite_attn")
+
+    def needs_update(self):
+        ic = self.cfg.index
+        return [u for u, s in enumerate(self.units)
+                if s.n_steady - s.n_sink >= ic.update_segment + ic.local_window]
+
+    def maybe_update(self):
+        """Fold full update segments of the decode buffer into the index
+        (ClusterIndex.update, index.py:168-186)."""
+        ic = self.cfg.index
+        todo = self.needs_update()
+        while todo:
+            segs, keep = [], []
+            k = math.ceil(ic.update_segment / ic.centroid_ratio)
+            tmp_k = torch.empty((len(todo), ic.update_segment, self.d), dtype=torch.float32,
+                                device=self.dev)
+            tmp_v = torch.empty_like(tmp_k)
+            for j, u in enumerate(todo):
+                s = self.units[u]
+                if s.m + k > self.m_cap or s.store_fill + ic.update_segment > self.s_cap:
+                    raise ConfigError("index capacity exceeded: raise max_decode")
+                r0 = s.n_sink
+                tmp_k[j] = self.st_k[u, r0:r0 + ic.update_segment].float()
+                tmp_v[j] = self.st_v[u, r0:r0 + ic.update_segment].float()
+                base = j * ic.update_segment * self.d
+                segs.append(dict(keys=tmp_k.data_ptr() + 4 * base, values=tmp_v.data_ptr() + 4 * base,
+                                 stride=self.d, L=ic.update_segment, k=k, unit=u, cid_base=s.m,
+                                 row_base=s.store_fill, tok_base=s.buffer_start,
+                                 rng=pcg64_words(ic.rng_seed, 2, s.update_round)))
+            self._run_segments(segs)
+            for u in todo:
+                s = self.units[u]
+                r0, r1 = s.n_sink + ic.update_segment, s.n_steady
+                # keep the buffer tail (index.py:179-180): shift rows down
+                for t in (self.st_k, self.st_v, self.st_tok):
+                    t[u, s.n_sink:s.n_sink + (r1 - r0)] = t[u, r0:r1].clone()
+                s.n_steady -= ic.update_segment
+                s.m += k
+                s.store_fill += ic.update_segment
+                s.buffer_start += ic.update_segment
+                s.update_round += 1
+            self.st_n.copy_(torch.tensor([s.n_steady for s in self.units], dtype=torch.int32))
+            self.m_dev.copy_(torch.tensor([s.m for s in self.units], dtype=torch.int32))
+            self.n_store_dev.copy_(torch.tensor([s.store_fill for s in self.units], dtype=torch.int32))
+            self.on_clusters_added(todo, k)
+            todo = self.needs_update()
+
+    def on_clusters_added(self, units, k):
+        """Hook for the block-cache registration (engine.py:212-214)."""
+
+    # ----------------------------------------------------------- full attention
+    def full_attention(self, q: torch.Tensor, out=None):
+        """Exact attention over every token of each unit (oracle_attention,
+        attention.py:55-64; also the full-attention comparator)."""
+        q = q.float().contiguous()
+        sv = self._step_view(q)
+        if out is not None:
+            sv.out = out.data_ptr()
+        rc = self.L.wk_full_attn(ctypes.byref(self._ixv), ctypes.byref(self._stv), ctypes.byref(sv),
+                                 _ptr(self.n_store_dev), self.U, self.G, self.d, self.S,
+                                 self.store_bf16, ctypes.c_void_p(_stream()))
+        _lib.check(rc, "wk_full_attn")
+        return self.out if out is None else out
+
+    # ---------------------------------------------------------------- checking
+    def check_status(self, what="step"):
+        code = int(self.status.item())
+        if code:
+            self.status.zero_()
+            _lib.raise_status(code, what)
+
+    # host views of the index (tests; not on the hot path)
+    def index_arrays(self, u: int):
+        m = self.units[u].m
+        return dict(C64=self.C64[u, :m].cpu().numpy(), VS32=self.VS32[u, :m].cpu().numpy(),
+                    VS64=None if self.VS64 is None else self.VS64[u, :m].cpu().numpy(),
+                    sizes=self.cl_size[u, :m].cpu().numpy().astype(np.int64),
+                    offsets=self.cl_off[u, :m].cpu().numpy(),
+                    store_tok=self.store_tok[u, :self.units[u].store_fill].cpu().numpy())
