@@ -101,6 +101,10 @@ typedef struct wk_step_view {
   float* cov;         /* [U, G] StepMetrics.denominator_coverage                */
   int* status;        /* device status word                                     */
   int32_t r_cap, e_cap, ru_cap, eu_cap;
+  int32_t* rtok_row;  /* [U, rt_cap] store row of every retrieved token (union)  */
+  uint8_t* rtok_mask; /* [U, rt_cap] head mask of that token                     */
+  int32_t* sel_done;  /* [U] zero-initialised counter (last-CTA handoff)        */
+  int32_t rt_cap, pad_;
 } wk_step_view;
 
 typedef struct wk_zone_params {
@@ -110,6 +114,38 @@ typedef struct wk_zone_params {
   int32_t tail_denominator_only; /* IndexConfig.tail_mode                      */
   int32_t denominator_eq2;       /* EngineConfig.denominator_mode              */
 } wk_zone_params;
+
+/* Device block cache (the wave buffer), one state machine per cache unit
+ * (block_cache.py:52-225).  Cache unit = (unit, head) reproduces the
+ * reference's per-head HeadEngine exactly; cache unit = kv-head unit serves
+ * the union access stream of its GQA group.  Arrays sized by the caller. */
+typedef struct wk_cache_view {
+  int32_t* nblk;      /* [C, m_cap] slow-tier blocks per cluster (store.py:38-45) */
+  int32_t* slot_off;  /* [C, m_cap] offset of the cluster's slot list           */
+  int32_t* slot_ids;  /* [C, slot_cap] fast-tier slot ids (ClusterDescriptor)   */
+  uint8_t* cached;    /* [C, m_cap]                                             */
+  int32_t* prev;      /* [C, m_cap] LRU list (oldest first)                     */
+  int32_t* next;
+  int32_t* touched;   /* [C, m_cap] step stamp of the last access               */
+  int64_t* last_access; /* [C, m_cap] ClusterDescriptor.last_access_step        */
+  int32_t* lru_ht;    /* [C, 2] head, tail                                      */
+  int32_t* heap;      /* [C, heap_cap] free slot ids (min-heap)                 */
+  int32_t* heap_n;    /* [C]                                                    */
+  int32_t* next_slot; /* [C]                                                    */
+  int64_t* capacity;  /* [C] capacity_blocks                                    */
+  int64_t* occupied;  /* [C]                                                    */
+  int64_t* counters;  /* [C, 8] hits, misses, bytes_slow_to_fast,
+                         bytes_fast_internal, store bytes_read_total, evictions,
+                         admissions, rejections                                 */
+  int32_t* ids;       /* [C, ids_cap] this step's access stream (rank order)    */
+  int32_t* n_ids;     /* [C]                                                    */
+  uint8_t* snapshot;  /* [C, ids_cap] residency before the commit               */
+  int32_t* events;    /* [C, ev_cap, 4] (type, step, cluster, aux) or NULL      */
+  int64_t* ev_n;      /* [C]                                                    */
+  const int32_t* m_live; /* [U] registered clusters per unit                    */
+  int64_t m_cap, slot_cap, heap_cap, ids_cap, ev_cap;
+  int32_t block_bytes, token_bytes;
+} wk_cache_view;
 
 int wk_version(void);
 
@@ -148,6 +184,24 @@ int wk_tripartite_attn(const wk_index_view* ix, const wk_steady_view* st, const 
  * store rows of unit u. */
 int wk_full_attn(const wk_index_view* ix, const wk_steady_view* st, const wk_step_view* sv,
                  const int32_t* n_store, int U, int G, int d, int S, int store_bf16, void* stream);
+
+/* One lookup + assemble accounting + commit_update for every cache unit
+ * (BlockCache.lookup / assemble / commit_update, block_cache.py:79-213).
+ * rlist/nr come from wk_score_topk; n_steady = steady tokens per unit.
+ * union_mode=0: C = U*G cache units (per head); 1: C = U (GQA union). */
+int wk_cache_step(const wk_cache_view* cv, const int32_t* rlist, const int32_t* nr,
+                  const int32_t* n_steady, int r_cap, int G, int union_mode, int64_t step,
+                  int C, int* status, void* stream);
+
+/* recall@k of each (unit, head) (metrics.py:8-26 as used by
+ * engine.py:200-203): exact top-k tokens by fp64 q.K (dgemv recipe, ties to
+ * the lower token id) intersected with the retrieved set (steady tokens +
+ * this step's retrieval clusters).  Scratch: s [U*G, n_cap] f32,
+ * rflag [U*G, s_cap] u8.  recall_out [U*G] f32. */
+int wk_recall_at_k(const wk_index_view* ix, const wk_steady_view* st, const wk_step_view* sv,
+                   const int32_t* n_store, int U, int G, int d, int metrics_k, int blas_threads,
+                   float* s_scratch, uint8_t* rflag, int64_t n_cap, int store_bf16,
+                   float* recall_out, void* stream);
 
 #ifdef __cplusplus
 }

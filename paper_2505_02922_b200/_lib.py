@@ -46,7 +46,18 @@ class StepViewC(ctypes.Structure):
                 ("ne", _P), ("zmask", _P), ("ru_ids", _P), ("ru_mask", _P), ("ru_pre", _P),
                 ("eu_ids", _P), ("eu_mask", _P), ("cnt", _P), ("tail", _P), ("part", _P),
                 ("out", _P), ("logden", _P), ("cov", _P), ("status", _P), ("r_cap", _I32),
-                ("e_cap", _I32), ("ru_cap", _I32), ("eu_cap", _I32)]
+                ("e_cap", _I32), ("ru_cap", _I32), ("eu_cap", _I32), ("rtok_row", _P),
+                ("rtok_mask", _P), ("sel_done", _P), ("rt_cap", _I32), ("pad_", _I32)]
+
+
+class CacheViewC(ctypes.Structure):
+    _fields_ = [("nblk", _P), ("slot_off", _P), ("slot_ids", _P), ("cached", _P), ("prev", _P),
+                ("next", _P), ("touched", _P), ("last_access", _P), ("lru_ht", _P), ("heap", _P),
+                ("heap_n", _P), ("next_slot", _P), ("capacity", _P), ("occupied", _P),
+                ("counters", _P), ("ids", _P), ("n_ids", _P), ("snapshot", _P), ("events", _P),
+                ("ev_n", _P), ("m_live", _P), ("m_cap", _I64), ("slot_cap", _I64),
+                ("heap_cap", _I64), ("ids_cap", _I64), ("ev_cap", _I64), ("block_bytes", _I32),
+                ("token_bytes", _I32)]
 
 
 class ZoneParamsC(ctypes.Structure):
@@ -59,7 +70,7 @@ _lib = None
 
 # every symbol include/wavekv.h declares
 EXPORTS = ("wk_version", "wk_kmeans_segments", "wk_append_tokens", "wk_score_topk",
-           "wk_tripartite_attn", "wk_full_attn")
+           "wk_tripartite_attn", "wk_full_attn", "wk_cache_step", "wk_recall_at_k")
 
 
 def lib():
@@ -82,6 +93,11 @@ def lib():
                                      ctypes.c_int, ctypes.c_int, ctypes.c_int, _P]
     L.wk_full_attn.argtypes = [R(IndexViewC), R(SteadyViewC), R(StepViewC), _P, ctypes.c_int,
                                ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _P]
+    L.wk_cache_step.argtypes = [R(CacheViewC), _P, _P, _P, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                _I64, ctypes.c_int, _P, _P]
+    L.wk_recall_at_k.argtypes = [R(IndexViewC), R(SteadyViewC), R(StepViewC), _P, ctypes.c_int,
+                                 ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _P, _P, _I64,
+                                 ctypes.c_int, _P, _P]
     for name in EXPORTS:
         getattr(L, name).restype = ctypes.c_int
     _lib = L

@@ -5,6 +5,7 @@
 #include <math.h>
 
 #include "decode_internal.h"
+#include "cache_internal.h"
 
 namespace wk {
 // kmeans.cu
@@ -25,6 +26,22 @@ template <typename T, bool FULL>
 __global__ void attend_kernel(IndexView, SteadyView, StepView, AttnParams, const int32_t*);
 __global__ void merge_kernel(StepView, AttnParams, int);
 size_t select_smem_bytes();
+// decode_v2.cu
+template <int HS>
+__global__ void score_v2_kernel(IndexView, StepView, int, int, int);
+__global__ void select_v2_kernel(IndexView, StepView, SelParams);
+size_t select_v2_smem_bytes();
+template <typename T, int DL, int HS, bool FULL>
+__global__ void attend_v2_kernel(IndexView, SteadyView, StepView, AttnParams, const int32_t*);
+size_t attend_v2_smem_bytes(int d, int HS);
+// metrics.cu
+template <typename T>
+__global__ void recall_kernel(IndexView, SteadyView, StepView, const int32_t*, int, int, int, int, float*,
+                              uint8_t*, int64_t, float*);
+size_t recall_smem_bytes();
+// cache.cu
+__global__ void cache_step_kernel(CacheView, const int32_t*, const int32_t*, const int32_t*, int, int, int,
+                                  int64_t, int, int*);
 }  // namespace wk
 
 using namespace wk;
@@ -50,13 +67,49 @@ static int configure_smem() {
   if (cudaFuncSetAttribute(attend_kernel<__nv_bfloat16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, at) != cudaSuccess) return WK_ECUDA;
   if (cudaFuncSetAttribute(attend_kernel<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, at) != cudaSuccess) return WK_ECUDA;
   if (cudaFuncSetAttribute(attend_kernel<__nv_bfloat16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, at) != cudaSuccess) return WK_ECUDA;
+  if (cudaFuncSetAttribute(select_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)select_v2_smem_bytes()) != cudaSuccess) return WK_ECUDA;
+  const int rs = (int)recall_smem_bytes();
+  if (cudaFuncSetAttribute(recall_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, rs) != cudaSuccess) return WK_ECUDA;
+  if (cudaFuncSetAttribute(recall_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, rs) != cudaSuccess) return WK_ECUDA;
   g_smem_configured = 1;
   return 0;
 }
 
+static int head_slots(int G) { return G <= 4 ? 4 : 8; }
+static bool v2_ok(int d) { return d == 64 || d == 128; }
+static int g_max_smem = 0;
+
+template <typename T, int DL, int HS, bool FULL>
+static int launch_attend_v2(const IndexView& ix, const SteadyView& st, const StepView& sv, const AttnParams& p,
+                            const int32_t* n_store, int U, int S, cudaStream_t s) {
+  const size_t sm = attend_v2_smem_bytes(p.d, HS);
+  if (sm > 48 * 1024 &&
+      cudaFuncSetAttribute(attend_v2_kernel<T, DL, HS, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) !=
+          cudaSuccess)
+    return WK_ECUDA;
+  attend_v2_kernel<T, DL, HS, FULL><<<dim3(S, U), 256, sm, s>>>(ix, st, sv, p, n_store);
+  return cudaGetLastError() == cudaSuccess ? 0 : WK_ECUDA;
+}
+
+template <typename T, bool FULL>
+static int dispatch_attend_v2(const IndexView& ix, const SteadyView& st, const StepView& sv, const AttnParams& p,
+                              const int32_t* n_store, int U, int S, cudaStream_t s) {
+  const int hs = head_slots(p.G);
+  if (p.d == 128) {
+    switch (hs) {
+      case 4: return launch_attend_v2<T, 4, 4, FULL>(ix, st, sv, p, n_store, U, S, s);
+      default: return launch_attend_v2<T, 4, 8, FULL>(ix, st, sv, p, n_store, U, S, s);
+    }
+  }
+  switch (hs) {
+    case 4: return launch_attend_v2<T, 2, 4, FULL>(ix, st, sv, p, n_store, U, S, s);
+    default: return launch_attend_v2<T, 2, 8, FULL>(ix, st, sv, p, n_store, U, S, s);
+  }
+}
+
 extern "C" {
 
-int wk_version(void) { return 1; }
+int wk_version(void) { return 2; }
 
 int wk_kmeans_segments(const wk_index_view* ix, const wk_segment* segs, int n_segs,
                        const wk_build_scratch* scr, int d, int store_bf16, int kmeans_iters,
@@ -111,9 +164,23 @@ int wk_score_topk(const wk_index_view* ix, const wk_step_view* sv, const wk_zone
     return WK_ECONFIG;
   if (configure_smem()) return WK_ECUDA;
   cudaStream_t s = (cudaStream_t)stream;
+  const bool v2 = v2_ok(zp->d) && sv->rtok_row && sv->sel_done;
   if (m_max > 0) {
-    dim3 g1((m_max + 63) / 64, U);
-    score_kernel<<<g1, 256, 0, s>>>(*ix, *sv, zp->d, zp->G);
+    if (v2) {
+      const int hs = head_slots(zp->G);
+      const int rg8 = (32 / hs) * 8;
+      long long want = ((long long)m_max * U + 148 * 8 - 1) / (148 * 8);
+      int rows = (int)((want + rg8 - 1) / rg8) * rg8;
+      if (rows < rg8) rows = rg8;
+      dim3 g1((m_max + rows - 1) / rows, U);
+      switch (hs) {
+        case 4: score_v2_kernel<4><<<g1, 256, 0, s>>>(*ix, *sv, zp->d, zp->G, rows); break;
+        default: score_v2_kernel<8><<<g1, 256, 0, s>>>(*ix, *sv, zp->d, zp->G, rows); break;
+      }
+    } else {
+      dim3 g1((m_max + 63) / 64, U);
+      score_kernel<<<g1, 256, 0, s>>>(*ix, *sv, zp->d, zp->G);
+    }
     WK_CHECK_LAUNCH();
   }
   SelParams p;
@@ -123,6 +190,11 @@ int wk_score_topk(const wk_index_view* ix, const wk_step_view* sv, const wk_zone
   p.inv_sqrt_d = (float)(1.0 / sqrt((double)zp->d));
   p.need_tail = zp->tail_denominator_only;
   p.need_allc = zp->denominator_eq2;
+  if (v2) {
+    select_v2_kernel<<<U * zp->G, 512, select_v2_smem_bytes(), s>>>(*ix, *sv, p);
+    WK_CHECK_LAUNCH();
+    return 0;
+  }
   select_kernel<<<U * zp->G, 512, select_smem_bytes(), s>>>(*ix, *sv, p);
   WK_CHECK_LAUNCH();
   union_kernel<<<U, 1024, 0, s>>>(*ix, *sv);
@@ -142,7 +214,11 @@ int wk_tripartite_attn(const wk_index_view* ix, const wk_steady_view* st, const 
   p.tail_denominator_only = zp->tail_denominator_only;
   p.denominator_eq2 = zp->denominator_eq2;
   dim3 grid(S, U);
-  if (store_bf16)
+  if (v2_ok(zp->d) && sv->rtok_row && sv->sel_done) {
+    const int rc = store_bf16 ? dispatch_attend_v2<__nv_bfloat16, false>(*ix, *st, *sv, p, nullptr, U, S, s)
+                              : dispatch_attend_v2<float, false>(*ix, *st, *sv, p, nullptr, U, S, s);
+    if (rc) return rc;
+  } else if (store_bf16)
     attend_kernel<__nv_bfloat16, false><<<grid, 128, attend_smem_bytes(zp->d, 2), s>>>(*ix, *st, *sv, p, nullptr);
   else
     attend_kernel<float, false><<<grid, 128, attend_smem_bytes(zp->d, 4), s>>>(*ix, *st, *sv, p, nullptr);
@@ -166,12 +242,44 @@ int wk_full_attn(const wk_index_view* ix, const wk_steady_view* st, const wk_ste
   p.tail_denominator_only = 0;
   p.denominator_eq2 = 0;
   dim3 grid(S, U);
-  if (store_bf16)
+  if (v2_ok(d)) {
+    const int rc = store_bf16 ? dispatch_attend_v2<__nv_bfloat16, true>(*ix, *st, v, p, n_store, U, S, s)
+                              : dispatch_attend_v2<float, true>(*ix, *st, v, p, n_store, U, S, s);
+    if (rc) return rc;
+  } else if (store_bf16)
     attend_kernel<__nv_bfloat16, true><<<grid, 128, attend_smem_bytes(d, 2), s>>>(*ix, *st, v, p, n_store);
   else
     attend_kernel<float, true><<<grid, 128, attend_smem_bytes(d, 4), s>>>(*ix, *st, v, p, n_store);
   WK_CHECK_LAUNCH();
   merge_kernel<<<U * G, 128, 0, s>>>(v, p, S);
+  WK_CHECK_LAUNCH();
+  return 0;
+}
+
+int wk_cache_step(const wk_cache_view* cv, const int32_t* rlist, const int32_t* nr,
+                  const int32_t* n_steady, int r_cap, int G, int union_mode, int64_t step, int C,
+                  int* status, void* stream) {
+  if (!cv || !rlist || !nr || !n_steady || C <= 0 || G < 1 || G > 8) return WK_ECONFIG;
+  cudaStream_t s = (cudaStream_t)stream;
+  cache_step_kernel<<<(C + 63) / 64, 64, 0, s>>>(*cv, rlist, nr, n_steady, r_cap, G, union_mode, step, C, status);
+  WK_CHECK_LAUNCH();
+  return 0;
+}
+
+int wk_recall_at_k(const wk_index_view* ix, const wk_steady_view* st, const wk_step_view* sv,
+                   const int32_t* n_store, int U, int G, int d, int metrics_k, int blas_threads,
+                   float* s_scratch, uint8_t* rflag, int64_t n_cap, int store_bf16, float* recall_out,
+                   void* stream) {
+  if (!ix || !st || !sv || !n_store || U <= 0 || G < 1 || G > 8 || d > 256 || metrics_k < 1) return WK_ECONFIG;
+  if (configure_smem()) return WK_ECUDA;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t sm = recall_smem_bytes();
+  if (store_bf16)
+    recall_kernel<__nv_bfloat16><<<U * G, 512, sm, s>>>(*ix, *st, *sv, n_store, G, d, metrics_k, blas_threads,
+                                                        s_scratch, rflag, n_cap, recall_out);
+  else
+    recall_kernel<float><<<U * G, 512, sm, s>>>(*ix, *st, *sv, n_store, G, d, metrics_k, blas_threads, s_scratch,
+                                                rflag, n_cap, recall_out);
   WK_CHECK_LAUNCH();
   return 0;
 }

@@ -2,4 +2,7 @@
 // (sm_100a) from the kernel sources and the C ABI.
 #include "kmeans.cu"
 #include "decode.cu"
+#include "decode_v2.cu"
+#include "cache.cu"
+#include "metrics.cu"
 #include "abi.cu"

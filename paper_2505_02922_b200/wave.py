@@ -104,7 +104,7 @@ class WaveLayer:
         self.t_cap = max(self.t_cap, min(max_prefill, ic.sink_tokens + ic.local_window) + 8)
         self.r_cap = max(1, min(self.m_cap, round_half_up(ic.retrieval_fraction * self.m_cap) + 2))
         self.e_cap = max(1, min(self.m_cap, round_half_up(ic.estimation_fraction * self.m_cap) + 2))
-        self.S = splits or max(1, min(64, -(-1024 // U)))
+        self.S = splits or max(1, min(64, -(-2048 // U)))
         dev, f32, i32 = self.dev, torch.float32, torch.int32
         # ---- index arrays ----
         self.store_k = torch.zeros((U, self.s_cap, d), dtype=store_dtype, device=dev)
@@ -140,6 +140,10 @@ class WaveLayer:
         self.eu_ids = torch.zeros((U, self.eu_cap), dtype=i32, device=dev)
         self.eu_mask = torch.zeros((U, self.eu_cap), dtype=torch.uint8, device=dev)
         self.cnt = torch.zeros((U, 4), dtype=i32, device=dev)
+        self.rt_cap = self.s_cap
+        self.rtok_row = torch.zeros((U, self.rt_cap), dtype=i32, device=dev)
+        self.rtok_mask = torch.zeros((U, self.rt_cap), dtype=torch.uint8, device=dev)
+        self.sel_done = torch.zeros(U, dtype=i32, device=dev)
         self.tail = torch.zeros((U, G, 4), dtype=f32, device=dev)
         self.part = torch.zeros((U, self.S, G, 3, 2 + d), dtype=f32, device=dev)
         self.out = torch.zeros((U, G, d), dtype=f32, device=dev)
@@ -167,7 +171,8 @@ class WaveLayer:
             _ptr(self.nr), _ptr(self.ne), _ptr(self.zmask), _ptr(self.ru_ids), _ptr(self.ru_mask),
             _ptr(self.ru_pre), _ptr(self.eu_ids), _ptr(self.eu_mask), _ptr(self.cnt),
             _ptr(self.tail), _ptr(self.part), _ptr(self.out), _ptr(self.logden), _ptr(self.cov),
-            _ptr(self.status), self.r_cap, self.e_cap, self.ru_cap, self.eu_cap)
+            _ptr(self.status), self.r_cap, self.e_cap, self.ru_cap, self.eu_cap,
+            _ptr(self.rtok_row), _ptr(self.rtok_mask), _ptr(self.sel_done), self.rt_cap, 0)
 
     # --------------------------------------------------------------- clustering
     def _run_segments(self, segs: list[dict]):
