@@ -29,8 +29,17 @@ size_t select_smem_bytes();
 // decode_v2.cu
 template <int HS>
 __global__ void score_v2_kernel(IndexView, StepView, int, int, int);
-__global__ void select_v2_kernel(IndexView, StepView, SelParams);
-size_t select_v2_smem_bytes();
+// decode_v3.cu
+__global__ void select_v3_kernel(IndexView, StepView, SelParams, int, int);
+size_t sel_smem_bytes(int m_max, int r_max);
+template <typename T, int DL, int HS, bool FULL>
+__global__ void attend_v3_kernel(IndexView, SteadyView, StepView, AttnParams, const int32_t*);
+template <typename T, int DL, int HS, bool FULL>
+size_t attend_v3_smem();
+template <int HS, int DL>
+__global__ void score_v3_kernel(IndexView, StepView, int, int);
+template <int HS, int DL>
+size_t score_v3_smem();
 template <typename T, int DL, int HS, bool FULL>
 __global__ void attend_v2_kernel(IndexView, SteadyView, StepView, AttnParams, const int32_t*);
 size_t attend_v2_smem_bytes(int d, int HS);
@@ -67,7 +76,7 @@ static int configure_smem() {
   if (cudaFuncSetAttribute(attend_kernel<__nv_bfloat16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, at) != cudaSuccess) return WK_ECUDA;
   if (cudaFuncSetAttribute(attend_kernel<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, at) != cudaSuccess) return WK_ECUDA;
   if (cudaFuncSetAttribute(attend_kernel<__nv_bfloat16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, at) != cudaSuccess) return WK_ECUDA;
-  if (cudaFuncSetAttribute(select_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)select_v2_smem_bytes()) != cudaSuccess) return WK_ECUDA;
+  if (cudaFuncSetAttribute(select_v3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess) return WK_ECUDA;
   const int rs = (int)recall_smem_bytes();
   if (cudaFuncSetAttribute(recall_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, rs) != cudaSuccess) return WK_ECUDA;
   if (cudaFuncSetAttribute(recall_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, rs) != cudaSuccess) return WK_ECUDA;
@@ -82,12 +91,34 @@ static int g_max_smem = 0;
 template <typename T, int DL, int HS, bool FULL>
 static int launch_attend_v2(const IndexView& ix, const SteadyView& st, const StepView& sv, const AttnParams& p,
                             const int32_t* n_store, int U, int S, cudaStream_t s) {
-  const size_t sm = attend_v2_smem_bytes(p.d, HS);
-  if (sm > 48 * 1024 &&
-      cudaFuncSetAttribute(attend_v2_kernel<T, DL, HS, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) !=
-          cudaSuccess)
-    return WK_ECUDA;
-  attend_v2_kernel<T, DL, HS, FULL><<<dim3(S, U), 256, sm, s>>>(ix, st, sv, p, n_store);
+  const size_t sm = attend_v3_smem<T, DL, HS, FULL>();
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(attend_v3_kernel<T, DL, HS, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sm) != cudaSuccess)
+      return WK_ECUDA;
+    configured = true;
+  }
+  attend_v3_kernel<T, DL, HS, FULL><<<dim3(S, U), 256, sm, s>>>(ix, st, sv, p, n_store);
+  return cudaGetLastError() == cudaSuccess ? 0 : WK_ECUDA;
+}
+
+template <int HS, int DL>
+static int launch_score_v3(const IndexView& ix, const StepView& sv, int G, int U, int m_max, cudaStream_t s) {
+  const size_t sm = score_v3_smem<HS, DL>();
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(score_v3_kernel<HS, DL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) !=
+        cudaSuccess)
+      return WK_ECUDA;
+    configured = true;
+  }
+  const int quantum = 4 * (32 / HS);
+  long long want = ((long long)m_max * U + 148 * 12 - 1) / (148 * 12);
+  int rows = (int)((want + quantum - 1) / quantum) * quantum;
+  if (rows < quantum) rows = quantum;
+  dim3 g((m_max + rows - 1) / rows, U);
+  score_v3_kernel<HS, DL><<<g, 128, sm, s>>>(ix, sv, G, rows);
   return cudaGetLastError() == cudaSuccess ? 0 : WK_ECUDA;
 }
 
@@ -168,15 +199,12 @@ int wk_score_topk(const wk_index_view* ix, const wk_step_view* sv, const wk_zone
   if (m_max > 0) {
     if (v2) {
       const int hs = head_slots(zp->G);
-      const int rg8 = (32 / hs) * 8;
-      long long want = ((long long)m_max * U + 148 * 8 - 1) / (148 * 8);
-      int rows = (int)((want + rg8 - 1) / rg8) * rg8;
-      if (rows < rg8) rows = rg8;
-      dim3 g1((m_max + rows - 1) / rows, U);
-      switch (hs) {
-        case 4: score_v2_kernel<4><<<g1, 256, 0, s>>>(*ix, *sv, zp->d, zp->G, rows); break;
-        default: score_v2_kernel<8><<<g1, 256, 0, s>>>(*ix, *sv, zp->d, zp->G, rows); break;
-      }
+      int rc;
+      if (zp->d == 128) rc = hs == 4 ? launch_score_v3<4, 4>(*ix, *sv, zp->G, U, m_max, s)
+                                     : launch_score_v3<8, 4>(*ix, *sv, zp->G, U, m_max, s);
+      else rc = hs == 4 ? launch_score_v3<4, 2>(*ix, *sv, zp->G, U, m_max, s)
+                        : launch_score_v3<8, 2>(*ix, *sv, zp->G, U, m_max, s);
+      if (rc) return rc;
     } else {
       dim3 g1((m_max + 63) / 64, U);
       score_kernel<<<g1, 256, 0, s>>>(*ix, *sv, zp->d, zp->G);
@@ -191,7 +219,7 @@ int wk_score_topk(const wk_index_view* ix, const wk_step_view* sv, const wk_zone
   p.need_tail = zp->tail_denominator_only;
   p.need_allc = zp->denominator_eq2;
   if (v2) {
-    select_v2_kernel<<<U * zp->G, 512, select_v2_smem_bytes(), s>>>(*ix, *sv, p);
+    select_v3_kernel<<<U * zp->G, 256, sel_smem_bytes(m_max, sv->r_cap), s>>>(*ix, *sv, p, m_max, sv->r_cap);
     WK_CHECK_LAUNCH();
     return 0;
   }

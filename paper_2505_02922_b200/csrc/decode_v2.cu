@@ -87,407 +87,6 @@ __global__ void __launch_bounds__(256) score_v2_kernel(IndexView ix, StepView sv
 }
 
 // ---------------------------------------------------------------------------
-// select_v2
-// ---------------------------------------------------------------------------
-constexpr int S2_THREADS = 512;
-constexpr int S2_BAND = 1024;
-constexpr int S2_RL = 4096;
-constexpr int S2_KEYS = 16384;  // scores cached in smem up to this m
-
-struct Sel2Smem {
-  unsigned int keys[S2_KEYS];
-  unsigned long long rl[S2_RL];
-  double ex[S2_RL];
-  int bid_r[S2_BAND];
-  double bex_r[S2_BAND];
-  int bid_e[S2_BAND];
-  double bex_e[S2_BAND];
-  unsigned char bsel_e[S2_BAND];
-  int hist[2048];
-  double q64[256];
-  float red[32];
-  int wsum[32], wsum2[32], wsum3[32];
-  int n_in_r, n_band_r, n_band_e, n_in_e, n_rl, n_el;
-  int krem, sel, last;
-  int base_r, base_e, base_t;
-  float fred;
-};
-
-__device__ __forceinline__ float s2_block_reduce(float v, bool is_max, Sel2Smem& sm) {
-  v = is_max ? warp_max(v) : warp_sum(v);
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  __syncthreads();
-  if (lane == 0) sm.red[w] = v;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    float r = sm.red[0];
-    for (int i = 1; i < (int)(blockDim.x >> 5); i++) r = is_max ? fmaxf(r, sm.red[i]) : r + sm.red[i];
-    sm.fred = r;
-  }
-  __syncthreads();
-  return sm.fred;
-}
-
-// warp-aggregated append of `val` when `flag`; all lanes of the warp call it
-__device__ __forceinline__ void warp_append(bool flag, int val, int* list, int* counter, int cap) {
-  const unsigned mk = __ballot_sync(FULLMASK, flag);
-  if (!mk) return;
-  const int lane = threadIdx.x & 31;
-  int base = 0;
-  if (lane == __ffs(mk) - 1) base = atomicAdd(counter, __popc(mk));
-  base = __shfl_sync(FULLMASK, base, __ffs(mk) - 1);
-  if (flag) {
-    const int pos = base + __popc(mk & ((1u << lane) - 1u));
-    if (pos < cap) list[pos] = val;
-  }
-}
-
-__device__ unsigned int s2_kth_largest(const unsigned int* keys, const float* sg, int m, int K, Sel2Smem& sm) {
-  // keys: smem-cached order keys, or nullptr to derive them from sg (global)
-  const int shifts[3] = {21, 10, 0};
-  const unsigned widths[3] = {11, 11, 10};
-  unsigned int prefix = 0, pmask = 0;
-  if (threadIdx.x == 0) sm.krem = K;
-  for (int pass = 0; pass < 3; pass++) {
-    const int sh = shifts[pass];
-    const unsigned dm = (1u << widths[pass]) - 1u;
-    const int nb = 1 << widths[pass];
-    for (int b = threadIdx.x; b < nb; b += blockDim.x) sm.hist[b] = 0;
-    __syncthreads();
-    for (int base = 0; base < m; base += blockDim.x) {
-      const int i = base + threadIdx.x;
-      unsigned key = i < m ? (keys ? keys[i] : f2u_ord(sg[i])) : 0u;
-      const bool act = i < m && (key & pmask) == prefix;
-      const unsigned am = __ballot_sync(FULLMASK, act);
-      if (act) {
-        const unsigned dg = (key >> sh) & dm;
-        const unsigned peers = __match_any_sync(am, dg);
-        if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&sm.hist[dg], __popc(peers));
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      const int lane = threadIdx.x, per = nb / 32;
-      int local = 0;
-      for (int j = 0; j < per; j++) local += sm.hist[per * lane + j];
-      int suf = local;
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_down_sync(FULLMASK, suf, o);
-        if (lane + o < 32) suf += t;
-      }
-      const int krem = sm.krem;
-      const int above = suf - local;
-      const unsigned ball = __ballot_sync(FULLMASK, above < krem && suf >= krem);
-      const int owner = __ffs(ball) - 1;
-      if (lane == owner) {
-        int acc = above, sel = per * lane;
-        for (int j = per - 1; j >= 0; j--) {
-          const int h = sm.hist[per * lane + j];
-          if (acc + h >= krem) { sel = per * lane + j; break; }
-          acc += h;
-        }
-        sm.krem = krem - acc;
-        sm.sel = sel;
-      }
-    }
-    __syncthreads();
-    prefix |= (unsigned)sm.sel << sh;
-    pmask |= dm << sh;
-    __syncthreads();
-  }
-  return prefix;
-}
-
-__device__ __forceinline__ double exact_score2(const IndexView& ix, int u, int c, int m, int d, int bt,
-                                               const double* q64) {
-  const double* row = ix.C64 + ((size_t)u * ix.m_cap + c) * d;
-  return dgemv_row(row, q64, d, gemv_row_class(c, m, d, bt));
-}
-
-__device__ __forceinline__ unsigned long long s2_key(float s, int id) {
-  return ((unsigned long long)(~f2u_ord(s)) << 32) | (unsigned int)id;
-}
-__device__ __forceinline__ float s2_score(unsigned long long k) { return u2f_ord(~(unsigned int)(k >> 32)); }
-__device__ __forceinline__ int s2_id(unsigned long long k) { return (int)(k & 0xffffffffu); }
-__device__ __forceinline__ bool s2_better(double a, int ia, double b, int ib) {
-  return a > b || (a == b && ia < ib);
-}
-
-// union of the unit's G zones (runs in the last CTA of the unit)
-__device__ void s2_union(const IndexView& ix, const StepView& sv, int u, int m, Sel2Smem& sm) {
-  uint32_t* zm = sv.zmask + (size_t)u * ix.m_cap;
-  const int* csize = ix.cl_size + (size_t)u * ix.m_cap;
-  const int* coff = ix.cl_off + (size_t)u * ix.m_cap;
-  int32_t* ru = sv.ru_ids + (size_t)u * sv.ru_cap;
-  uint8_t* rmk = sv.ru_mask + (size_t)u * sv.ru_cap;
-  int32_t* rpre = sv.ru_pre + (size_t)u * (sv.ru_cap + 1);
-  int32_t* eu = sv.eu_ids + (size_t)u * sv.eu_cap;
-  uint8_t* emk = sv.eu_mask + (size_t)u * sv.eu_cap;
-  int32_t* trow = sv.rtok_row + (size_t)u * sv.rt_cap;
-  uint8_t* tmk = sv.rtok_mask + (size_t)u * sv.rt_cap;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (threadIdx.x == 0) { sm.base_r = 0; sm.base_e = 0; sm.base_t = 0; }
-  __syncthreads();
-  for (int c0 = 0; c0 < m; c0 += blockDim.x) {
-    const int c = c0 + threadIdx.x;
-    const uint32_t z = c < m ? __ldcg(zm + c) : 0u;
-    if (c < m && z) zm[c] = 0u;
-    const int fr = (z & 0xffu) ? 1 : 0, fe = (z & 0xff00u) ? 1 : 0;
-    const int sz = fr ? csize[c] : 0;
-    int xr = fr, xe = fe, xt = sz;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int a = __shfl_up_sync(FULLMASK, xr, o), b = __shfl_up_sync(FULLMASK, xe, o),
-                t = __shfl_up_sync(FULLMASK, xt, o);
-      if (lane >= o) { xr += a; xe += b; xt += t; }
-    }
-    if (lane == 31) { sm.wsum[w] = xr; sm.wsum2[w] = xe; sm.wsum3[w] = xt; }
-    __syncthreads();
-    if (w == 0) {
-      const int nw = blockDim.x >> 5;
-      int a = lane < nw ? sm.wsum[lane] : 0, b = lane < nw ? sm.wsum2[lane] : 0,
-          t = lane < nw ? sm.wsum3[lane] : 0;
-      int ia = a, ib = b, it = t;
-      for (int o = 1; o < 32; o <<= 1) {
-        const int pa = __shfl_up_sync(FULLMASK, ia, o), pb = __shfl_up_sync(FULLMASK, ib, o),
-                  pt = __shfl_up_sync(FULLMASK, it, o);
-        if (lane >= o) { ia += pa; ib += pb; it += pt; }
-      }
-      if (lane < nw) { sm.wsum[lane] = ia - a; sm.wsum2[lane] = ib - b; sm.wsum3[lane] = it - t; }
-    }
-    __syncthreads();
-    const int pr = sm.base_r + sm.wsum[w] + xr - fr;
-    const int pe = sm.base_e + sm.wsum2[w] + xe - fe;
-    const int pt = sm.base_t + sm.wsum3[w] + xt - sz;
-    if (fr) {
-      if (pr < sv.ru_cap && pt + sz <= sv.rt_cap) {
-        ru[pr] = c;
-        rmk[pr] = (uint8_t)(z & 0xffu);
-        rpre[pr] = pt;
-        const int o = coff[c];
-        for (int j = 0; j < sz; j++) { trow[pt + j] = o + j; tmk[pt + j] = (uint8_t)(z & 0xffu); }
-      } else {
-        set_status(sv.status, kErrUnion);
-      }
-    }
-    if (fe) {
-      if (pe < sv.eu_cap) { eu[pe] = c; emk[pe] = (uint8_t)((z >> 8) & 0xffu); }
-      else set_status(sv.status, kErrUnion);
-    }
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) { sm.base_r = pr + fr; sm.base_e = pe + fe; sm.base_t = pt + sz; }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    const int nr = min(sm.base_r, sv.ru_cap);
-    rpre[nr] = sm.base_t;
-    sv.cnt[u * 4 + 0] = nr;
-    sv.cnt[u * 4 + 1] = min(sm.base_t, sv.rt_cap);
-    sv.cnt[u * 4 + 2] = min(sm.base_e, sv.eu_cap);
-  }
-}
-
-__global__ void __launch_bounds__(S2_THREADS) select_v2_kernel(IndexView ix, StepView sv, SelParams p) {
-  extern __shared__ __align__(16) unsigned char s2_raw[];
-  Sel2Smem& sm = *reinterpret_cast<Sel2Smem*>(s2_raw);
-  const int G = p.G, d = p.d;
-  const int u = blockIdx.x / G, g = blockIdx.x % G;
-  const int m = sv.m[u];
-  const int lane = threadIdx.x & 31;
-  float* tailp = sv.tail + ((size_t)u * G + g) * 4;
-  int r = 0, e = 0;
-  if (m > 0) {
-    r = (int)floor(p.retrieval_fraction * (double)m + 0.5);
-    if (r < 1) r = 1;
-    if (r > m) r = m;
-    e = (int)floor(p.estimation_fraction * (double)m + 0.5);
-    if (e > m - r) e = m - r;
-  }
-  if (threadIdx.x == 0 && g == 0) { sv.nr[u] = r; sv.ne[u] = e; }
-  const float* s = sv.scores + ((size_t)u * G + g) * ix.m_cap;
-  const float* q = sv.q + ((size_t)u * G + g) * d;
-  const int* csize = ix.cl_size + (size_t)u * ix.m_cap;
-  uint32_t* zm = sv.zmask + (size_t)u * ix.m_cap;
-  const bool ok = m > 0 && r <= S2_RL;
-  const bool cached = m <= S2_KEYS;
-  if (m > 0 && !ok) set_status(sv.status, kErrBandOverflow);
-  if (ok) {
-    for (int t = threadIdx.x; t < d; t += blockDim.x) sm.q64[t] = (double)q[t];
-    float cm = 0.f;
-    for (int c = threadIdx.x; c < m; c += blockDim.x) {
-      if (cached) sm.keys[c] = f2u_ord(s[c]);
-      cm = fmaxf(cm, ix.Cnorm[(size_t)u * ix.m_cap + c]);
-    }
-    float qq = 0.f;
-    for (int t = threadIdx.x; t < d; t += blockDim.x) qq = fmaf(q[t], q[t], qq);
-    const float qn2 = s2_block_reduce(qq, false, sm);
-    const float cmax = s2_block_reduce(cm, true, sm);
-    const double uu = 5.9604644775390625e-08;
-    const double gam = (double)d * uu / (1.0 - (double)d * uu);
-    const double B = 2.0 * (gam + uu + 1e-13) * (1.0 + 1e-5) * sqrt((double)qn2) * (1.0 + 1e-5) *
-                     (double)cmax * (1.0 + 1e-5);
-    const double B2 = 2.0 * B;
-    const unsigned* kp = cached ? sm.keys : nullptr;
-    const float tau_r = u2f_ord(s2_kth_largest(kp, s, m, r, sm));
-    const float tau_e = e > 0 ? u2f_ord(s2_kth_largest(kp, s, m, r + e, sm)) : 0.f;
-    if (threadIdx.x == 0) { sm.n_in_r = 0; sm.n_band_r = 0; sm.n_band_e = 0; sm.n_in_e = 0; sm.n_rl = 0; }
-    __syncthreads();
-    int my_in_e = 0;
-    for (int base = 0; base < m; base += blockDim.x) {
-      const int c = base + threadIdx.x;
-      const bool act = c < m;
-      const double sc = act ? (double)s[c] : -INFINITY;
-      const bool in_r = act && sc > (double)tau_r + B2;
-      const bool bd_r = act && !in_r && sc >= (double)tau_r - B2;
-      warp_append(in_r, c, reinterpret_cast<int*>(sm.ex), &sm.n_rl, S2_RL);  // ids staged in ex[]
-      warp_append(bd_r, c, sm.bid_r, &sm.n_band_r, S2_BAND);
-      if (e > 0) {
-        const bool in_e = act && sc > (double)tau_e + B2;
-        const bool bd_e = act && !in_e && sc >= (double)tau_e - B2;
-        my_in_e += in_e ? 1 : 0;
-        warp_append(bd_e, c, sm.bid_e, &sm.n_band_e, S2_BAND);
-      }
-    }
-    my_in_e = __reduce_add_sync(FULLMASK, my_in_e);
-    if (lane == 0 && my_in_e) atomicAdd(&sm.n_in_e, my_in_e);
-    __syncthreads();
-    const int nin_r = sm.n_rl, nbr = sm.n_band_r, nbe = sm.n_band_e, nin_e = sm.n_in_e;
-    const bool bad = nbr > S2_BAND || nbe > S2_BAND || nin_r > r || nin_r + nbr < r ||
-                     (e > 0 && (nin_e > r + e || nin_e + nbe < r + e));
-    if (bad) {
-      set_status(sv.status, kErrBandOverflow);
-    } else {
-      // certain-in ids were staged in ex[] as ints: turn them into sort keys
-      const int* staged = reinterpret_cast<const int*>(sm.ex);
-      for (int i = threadIdx.x; i < nin_r; i += blockDim.x) { const int c = staged[i]; sm.rl[i] = s2_key(s[c], c); }
-      for (int i = threadIdx.x; i < nbr; i += blockDim.x)
-        sm.bex_r[i] = exact_score2(ix, u, sm.bid_r[i], m, d, p.blas_threads, sm.q64);
-      for (int i = threadIdx.x; i < nbe; i += blockDim.x)
-        sm.bex_e[i] = exact_score2(ix, u, sm.bid_e[i], m, d, p.blas_threads, sm.q64);
-      __syncthreads();
-      const int need_r = r - nin_r;
-      for (int i = threadIdx.x; i < nbr; i += blockDim.x) {
-        int rank = 0;
-        for (int j = 0; j < nbr; j++) rank += s2_better(sm.bex_r[j], sm.bid_r[j], sm.bex_r[i], sm.bid_r[i]) ? 1 : 0;
-        if (rank < need_r) sm.rl[nin_r + rank] = s2_key(s[sm.bid_r[i]], sm.bid_r[i]);
-      }
-      const int need_e = r + e - nin_e;
-      for (int i = threadIdx.x; i < nbe; i += blockDim.x) {
-        int rank = 0;
-        for (int j = 0; j < nbe; j++) rank += s2_better(sm.bex_e[j], sm.bid_e[j], sm.bex_e[i], sm.bid_e[i]) ? 1 : 0;
-        sm.bsel_e[i] = rank < need_e ? 1 : 0;
-      }
-      __syncthreads();
-      // bitonic sort of the r retrieval keys
-      int npow = 1;
-      while (npow < r) npow <<= 1;
-      for (int i = r + threadIdx.x; i < npow; i += blockDim.x) sm.rl[i] = ~0ull;
-      __syncthreads();
-      for (int k = 2; k <= npow; k <<= 1)
-        for (int j = k >> 1; j > 0; j >>= 1) {
-          for (int i = threadIdx.x; i < npow; i += blockDim.x) {
-            const int ixj = i ^ j;
-            if (ixj > i) {
-              const unsigned long long a = sm.rl[i], b = sm.rl[ixj];
-              if ((a > b) == ((i & k) == 0)) { sm.rl[i] = b; sm.rl[ixj] = a; }
-            }
-          }
-          __syncthreads();
-        }
-      // clumps of neighbours closer than 2B: exact scores, exact order
-      for (int i = threadIdx.x; i < r; i += blockDim.x) {
-        const double si = (double)s2_score(sm.rl[i]);
-        const bool cl = (i > 0 && (double)s2_score(sm.rl[i - 1]) - si <= B2) ||
-                        (i + 1 < r && si - (double)s2_score(sm.rl[i + 1]) <= B2);
-        sm.ex[i] = cl ? exact_score2(ix, u, s2_id(sm.rl[i]), m, d, p.blas_threads, sm.q64) : 0.0;
-      }
-      __syncthreads();
-      for (int i = threadIdx.x; i < r; i += blockDim.x) {
-        const double si = (double)s2_score(sm.rl[i]);
-        const bool lp = i > 0 && (double)s2_score(sm.rl[i - 1]) - si <= B2;
-        const bool ln = i + 1 < r && si - (double)s2_score(sm.rl[i + 1]) <= B2;
-        if (!lp && ln) {
-          int end = i + 1;
-          while (end + 1 < r && (double)s2_score(sm.rl[end]) - (double)s2_score(sm.rl[end + 1]) <= B2) end++;
-          for (int a = i + 1; a <= end; a++) {
-            const unsigned long long kk = sm.rl[a];
-            const double ev = sm.ex[a];
-            int b = a - 1;
-            while (b >= i && s2_better(ev, s2_id(kk), sm.ex[b], s2_id(sm.rl[b]))) {
-              sm.rl[b + 1] = sm.rl[b];
-              sm.ex[b + 1] = sm.ex[b];
-              b--;
-            }
-            sm.rl[b + 1] = kk;
-            sm.ex[b + 1] = ev;
-          }
-        }
-      }
-      __syncthreads();
-      int32_t* rl_out = sv.rlist + ((size_t)u * G + g) * sv.r_cap;
-      for (int i = threadIdx.x; i < r; i += blockDim.x) {
-        const int c = s2_id(sm.rl[i]);
-        rl_out[i] = c;
-        atomicOr(zm + c, 1u << g);
-      }
-      __threadfence_block();
-      __syncthreads();
-      int32_t* el_out = sv.elist ? sv.elist + ((size_t)u * G + g) * sv.e_cap : nullptr;
-      if (threadIdx.x == 0) sm.n_el = 0;
-      __syncthreads();
-      if (e > 0) {
-        for (int base = 0; base < m; base += blockDim.x) {
-          const int c = base + threadIdx.x;
-          const bool f = c < m && (double)s[c] > (double)tau_e + B2 && !(__ldcg(zm + c) & (1u << g));
-          if (f) atomicOr(zm + c, 1u << (8 + g));
-          if (el_out) warp_append(f, c, el_out, &sm.n_el, sv.e_cap);
-        }
-        for (int i = threadIdx.x; i < nbe; i += blockDim.x) {
-          const int c = sm.bid_e[i];
-          if (sm.bsel_e[i] && !(__ldcg(zm + c) & (1u << g))) {
-            atomicOr(zm + c, 1u << (8 + g));
-            if (el_out) el_out[atomicAdd(&sm.n_el, 1)] = c;
-          }
-        }
-      }
-      __syncthreads();
-      if (p.need_tail || p.need_allc) {
-        const float isd = p.inv_sqrt_d;
-        float mx_t = -INFINITY, mx_a = -INFINITY;
-        for (int c = threadIdx.x; c < m; c += blockDim.x) {
-          const float v = s[c] * isd;
-          mx_a = fmaxf(mx_a, v);
-          if (!(__ldcg(zm + c) & ((1u << g) | (1u << (8 + g))))) mx_t = fmaxf(mx_t, v);
-        }
-        mx_t = s2_block_reduce(mx_t, true, sm);
-        mx_a = s2_block_reduce(mx_a, true, sm);
-        float dt = 0.f, da = 0.f;
-        for (int c = threadIdx.x; c < m; c += blockDim.x) {
-          const float v = s[c] * isd;
-          const float sz = (float)csize[c];
-          da += sz * expf(v - mx_a);
-          if (!(__ldcg(zm + c) & ((1u << g) | (1u << (8 + g))))) dt += sz * expf(v - mx_t);
-        }
-        dt = s2_block_reduce(dt, false, sm);
-        da = s2_block_reduce(da, false, sm);
-        if (threadIdx.x == 0) { tailp[0] = mx_t; tailp[1] = dt; tailp[2] = mx_a; tailp[3] = da; }
-      }
-    }
-  }
-  if (!ok && threadIdx.x == 0) { tailp[0] = -INFINITY; tailp[1] = 0.f; tailp[2] = -INFINITY; tailp[3] = 0.f; }
-  // ---- the last CTA of the unit builds the unions ----
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) sm.last = (atomicAdd(sv.sel_done + u, 1) == G - 1);
-  __syncthreads();
-  if (!sm.last) return;
-  __threadfence();
-  if (threadIdx.x == 0) sv.sel_done[u] = 0;
-  s2_union(ix, sv, u, m, sm);
-}
-
-size_t select_v2_smem_bytes() { return sizeof(Sel2Smem); }
-
-// ---------------------------------------------------------------------------
 // attend_v2
 // grid = (S, U), block = 256 (8 warps); one CTA handles 1/S of its unit's
 // work items [steady tokens | retrieved tokens | estimation rows].

@@ -3,6 +3,7 @@
 #include "kmeans.cu"
 #include "decode.cu"
 #include "decode_v2.cu"
+#include "decode_v3.cu"
 #include "cache.cu"
 #include "metrics.cu"
 #include "abi.cu"
