@@ -105,6 +105,8 @@ typedef struct wk_step_view {
   uint8_t* rtok_mask; /* [U, rt_cap] head mask of that token                     */
   int32_t* sel_done;  /* [U] zero-initialised counter (last-CTA handoff)        */
   int32_t rt_cap, pad_;
+  float* eu_x;        /* [U, eu_cap, G] estimation-row scores (-inf: head not in zone) */
+  float* eu_sz;       /* [U, eu_cap] estimation-row cluster sizes                */
 } wk_step_view;
 
 typedef struct wk_zone_params {

@@ -47,7 +47,8 @@ class StepViewC(ctypes.Structure):
                 ("eu_ids", _P), ("eu_mask", _P), ("cnt", _P), ("tail", _P), ("part", _P),
                 ("out", _P), ("logden", _P), ("cov", _P), ("status", _P), ("r_cap", _I32),
                 ("e_cap", _I32), ("ru_cap", _I32), ("eu_cap", _I32), ("rtok_row", _P),
-                ("rtok_mask", _P), ("sel_done", _P), ("rt_cap", _I32), ("pad_", _I32)]
+                ("rtok_mask", _P), ("sel_done", _P), ("rt_cap", _I32), ("pad_", _I32),
+                ("eu_x", _P), ("eu_sz", _P)]
 
 
 class CacheViewC(ctypes.Structure):

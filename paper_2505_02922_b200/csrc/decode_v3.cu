@@ -41,6 +41,8 @@ struct Sel2Smem {
   int* bid_e;
   double* bex_e;
   unsigned char* bsel_e;
+  unsigned int* rbits;         // [ceil(m/32)] this head's retrieval set
+  unsigned int* ebits;         // [ceil(m/32)] this head's estimation set
   int hist[256];
   double q64[256];
   float red[32];
@@ -150,8 +152,38 @@ __device__ __forceinline__ bool s2_better(double a, int ia, double b, int ib) {
   return a > b || (a == b && ia < ib);
 }
 
-// union of the unit's G zones (runs in the last CTA of the unit)
-__device__ void s2_union(const IndexView& ix, const StepView& sv, int u, int m, Sel2Smem& sm) {
+// block-wide exclusive scan of three ints (blockDim.x <= 1024)
+__device__ __forceinline__ void scan3(int& a, int& b, int& c, int& ta, int& tb, int& tc, Sel2Smem& sm) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  int xa = a, xb = b, xc = c;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int pa = __shfl_up_sync(FULLMASK, xa, o), pb = __shfl_up_sync(FULLMASK, xb, o),
+              pc = __shfl_up_sync(FULLMASK, xc, o);
+    if (lane >= o) { xa += pa; xb += pb; xc += pc; }
+  }
+  if (lane == 31) { sm.wsum[w] = xa; sm.wsum2[w] = xb; sm.wsum3[w] = xc; }
+  __syncthreads();
+  if (w == 0) {
+    int va = lane < nw ? sm.wsum[lane] : 0, vb = lane < nw ? sm.wsum2[lane] : 0, vc = lane < nw ? sm.wsum3[lane] : 0;
+    int ia = va, ib = vb, ic = vc;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int pa = __shfl_up_sync(FULLMASK, ia, o), pb = __shfl_up_sync(FULLMASK, ib, o),
+                pc = __shfl_up_sync(FULLMASK, ic, o);
+      if (lane >= o) { ia += pa; ib += pb; ic += pc; }
+    }
+    if (lane < nw) { sm.wsum[lane] = ia - va; sm.wsum2[lane] = ib - vb; sm.wsum3[lane] = ic - vc; }
+    if (lane == nw - 1) { sm.base_r = ia; sm.base_e = ib; sm.base_t = ic; }
+  }
+  __syncthreads();
+  const int ea = sm.wsum[w] + xa - a, eb = sm.wsum2[w] + xb - b, ec = sm.wsum3[w] + xc - c;
+  ta = sm.base_r; tb = sm.base_e; tc = sm.base_t;
+  a = ea; b = eb; c = ec;
+  __syncthreads();
+}
+
+// union of the unit's G zones (runs in the last CTA of the unit): each thread
+// owns a contiguous slice of cluster ids, so one block scan orders everything.
+__device__ void s2_union(const IndexView& ix, const StepView& sv, int u, int m, int sv_G, Sel2Smem& sm) {
   uint32_t* zm = sv.zmask + (size_t)u * ix.m_cap;
   const int* csize = ix.cl_size + (size_t)u * ix.m_cap;
   const int* coff = ix.cl_off + (size_t)u * ix.m_cap;
@@ -162,64 +194,57 @@ __device__ void s2_union(const IndexView& ix, const StepView& sv, int u, int m, 
   uint8_t* emk = sv.eu_mask + (size_t)u * sv.eu_cap;
   int32_t* trow = sv.rtok_row + (size_t)u * sv.rt_cap;
   uint8_t* tmk = sv.rtok_mask + (size_t)u * sv.rt_cap;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (threadIdx.x == 0) { sm.base_r = 0; sm.base_e = 0; sm.base_t = 0; }
-  __syncthreads();
-  for (int c0 = 0; c0 < m; c0 += blockDim.x) {
-    const int c = c0 + threadIdx.x;
-    const uint32_t z = c < m ? __ldcg(zm + c) : 0u;
-    if (c < m && z) zm[c] = 0u;
-    const int fr = (z & 0xffu) ? 1 : 0, fe = (z & 0xff00u) ? 1 : 0;
-    const int sz = fr ? csize[c] : 0;
-    int xr = fr, xe = fe, xt = sz;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int a = __shfl_up_sync(FULLMASK, xr, o), b = __shfl_up_sync(FULLMASK, xe, o),
-                t = __shfl_up_sync(FULLMASK, xt, o);
-      if (lane >= o) { xr += a; xe += b; xt += t; }
-    }
-    if (lane == 31) { sm.wsum[w] = xr; sm.wsum2[w] = xe; sm.wsum3[w] = xt; }
-    __syncthreads();
-    if (w == 0) {
-      const int nw = blockDim.x >> 5;
-      int a = lane < nw ? sm.wsum[lane] : 0, b = lane < nw ? sm.wsum2[lane] : 0,
-          t = lane < nw ? sm.wsum3[lane] : 0;
-      int ia = a, ib = b, it = t;
-      for (int o = 1; o < 32; o <<= 1) {
-        const int pa = __shfl_up_sync(FULLMASK, ia, o), pb = __shfl_up_sync(FULLMASK, ib, o),
-                  pt = __shfl_up_sync(FULLMASK, it, o);
-        if (lane >= o) { ia += pa; ib += pb; it += pt; }
-      }
-      if (lane < nw) { sm.wsum[lane] = ia - a; sm.wsum2[lane] = ib - b; sm.wsum3[lane] = it - t; }
-    }
-    __syncthreads();
-    const int pr = sm.base_r + sm.wsum[w] + xr - fr;
-    const int pe = sm.base_e + sm.wsum2[w] + xe - fe;
-    const int pt = sm.base_t + sm.wsum3[w] + xt - sz;
-    if (fr) {
-      if (pr < sv.ru_cap && pt + sz <= sv.rt_cap) {
-        ru[pr] = c;
-        rmk[pr] = (uint8_t)(z & 0xffu);
-        rpre[pr] = pt;
+  const int T = blockDim.x, t = threadIdx.x;
+  const int lo = (int)((long long)m * t / T), hi = (int)((long long)m * (t + 1) / T);
+  int nr = 0, ne = 0, nt = 0;
+#pragma unroll 4
+  for (int c = lo; c < hi; c++) {
+    const uint32_t z = __ldcg(zm + c);
+    if (z & 0xffu) { nr++; nt += csize[c]; }
+    if (z & 0xff00u) ne++;
+  }
+  int tr, te, tt;
+  scan3(nr, ne, nt, tr, te, tt, sm);
+  for (int c = lo; c < hi; c++) {
+    const uint32_t z = __ldcg(zm + c);
+    if (!z) continue;
+    zm[c] = 0u;
+    if (z & 0xffu) {
+      const int sz = csize[c];
+      if (nr < sv.ru_cap && nt + sz <= sv.rt_cap) {
+        ru[nr] = c;
+        rmk[nr] = (uint8_t)(z & 0xffu);
+        rpre[nr] = nt;
         const int o = coff[c];
-        for (int j = 0; j < sz; j++) { trow[pt + j] = o + j; tmk[pt + j] = (uint8_t)(z & 0xffu); }
+        for (int j = 0; j < sz; j++) { trow[nt + j] = o + j; tmk[nt + j] = (uint8_t)(z & 0xffu); }
       } else {
         set_status(sv.status, kErrUnion);
       }
+      nr++;
+      nt += sz;
     }
-    if (fe) {
-      if (pe < sv.eu_cap) { eu[pe] = c; emk[pe] = (uint8_t)((z >> 8) & 0xffu); }
-      else set_status(sv.status, kErrUnion);
+    if (z & 0xff00u) {
+      if (ne < sv.eu_cap) {
+        eu[ne] = c;
+        emk[ne] = (uint8_t)((z >> 8) & 0xffu);
+        if (sv.eu_x) {
+          for (int h = 0; h < sv_G; h++)
+            sv.eu_x[((size_t)u * sv.eu_cap + ne) * sv_G + h] =
+                ((z >> (8 + h)) & 1u) ? sv.scores[((size_t)u * sv_G + h) * ix.m_cap + c] : -INFINITY;
+          sv.eu_sz[(size_t)u * sv.eu_cap + ne] = (float)csize[c];
+        }
+      } else {
+        set_status(sv.status, kErrUnion);
+      }
+      ne++;
     }
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) { sm.base_r = pr + fr; sm.base_e = pe + fe; sm.base_t = pt + sz; }
-    __syncthreads();
   }
-  if (threadIdx.x == 0) {
-    const int nr = min(sm.base_r, sv.ru_cap);
-    rpre[nr] = sm.base_t;
-    sv.cnt[u * 4 + 0] = nr;
-    sv.cnt[u * 4 + 1] = min(sm.base_t, sv.rt_cap);
-    sv.cnt[u * 4 + 2] = min(sm.base_e, sv.eu_cap);
+  if (t == 0) {
+    const int n_r = min(tr, sv.ru_cap);
+    rpre[n_r] = tt;
+    sv.cnt[u * 4 + 0] = n_r;
+    sv.cnt[u * 4 + 1] = min(tt, sv.rt_cap);
+    sv.cnt[u * 4 + 2] = min(te, sv.eu_cap);
   }
 }
 
@@ -232,7 +257,8 @@ __host__ __device__ inline size_t sel_smem_bytes(int m_max, int r_max) {
   const size_t hdr = (sizeof(Sel2Smem) + 127) & ~(size_t)127;
   const size_t keys = m_max <= S2_KEYS ? (size_t)m_max * 4 : 0;
   const size_t rl = sel_rlcap(r_max);
-  return hdr + ((keys + 15) & ~(size_t)15) + rl * 16 + (size_t)S2_BAND * (4 + 8 + 4 + 8 + 1) + 64;
+  const size_t bits = ((size_t)(m_max + 31) / 32) * 4 * 2;
+  return hdr + ((keys + 15) & ~(size_t)15) + rl * 16 + (size_t)S2_BAND * (4 + 8 + 4 + 8 + 1) + 64 + bits + 32;
 }
 
 __global__ void __launch_bounds__(S2_THREADS) select_v3_kernel(IndexView ix, StepView sv, SelParams p, int m_max,
@@ -251,7 +277,10 @@ __global__ void __launch_bounds__(S2_THREADS) select_v3_kernel(IndexView ix, Ste
     sm.bex_e = reinterpret_cast<double*>(q); q += S2_BAND * 8;
     sm.bid_r = reinterpret_cast<int*>(q); q += S2_BAND * 4;
     sm.bid_e = reinterpret_cast<int*>(q); q += S2_BAND * 4;
-    sm.bsel_e = q;
+    sm.bsel_e = q; q += S2_BAND;
+    q = reinterpret_cast<unsigned char*>(((size_t)q + 15) & ~(size_t)15);
+    sm.rbits = reinterpret_cast<unsigned int*>(q); q += ((size_t)(m_max + 31) / 32) * 4;
+    sm.ebits = reinterpret_cast<unsigned int*>(q);
   }
   __syncthreads();
   const int G = p.G, d = p.d;
@@ -278,10 +307,12 @@ __global__ void __launch_bounds__(S2_THREADS) select_v3_kernel(IndexView ix, Ste
   if (ok) {
     for (int t = threadIdx.x; t < d; t += blockDim.x) sm.q64[t] = (double)q[t];
     float cm = 0.f;
+#pragma unroll 4
     for (int c = threadIdx.x; c < m; c += blockDim.x) {
       if (cached) sm.keys[c] = f2u_ord(s[c]);
       cm = fmaxf(cm, ix.Cnorm[(size_t)u * ix.m_cap + c]);
     }
+    for (int w = threadIdx.x; w < (m + 31) / 32; w += blockDim.x) { sm.rbits[w] = 0u; sm.ebits[w] = 0u; }
     float qq = 0.f;
     for (int t = threadIdx.x; t < d; t += blockDim.x) qq = fmaf(q[t], q[t], qq);
     const float qn2 = s2_block_reduce(qq, false, sm);
@@ -300,7 +331,7 @@ __global__ void __launch_bounds__(S2_THREADS) select_v3_kernel(IndexView ix, Ste
     for (int base = 0; base < m; base += blockDim.x) {
       const int c = base + threadIdx.x;
       const bool act = c < m;
-      const double sc = act ? (double)s[c] : -INFINITY;
+      const double sc = act ? (double)(cached ? u2f_ord(sm.keys[c]) : s[c]) : -INFINITY;
       const bool in_r = act && sc > (double)tau_r + B2;
       const bool bd_r = act && !in_r && sc >= (double)tau_r - B2;
       warp_append(in_r, c, reinterpret_cast<int*>(sm.ex), &sm.n_rl, (int)sel_rlcap(r_max));  // ids staged in ex[]
@@ -393,6 +424,7 @@ __global__ void __launch_bounds__(S2_THREADS) select_v3_kernel(IndexView ix, Ste
         const int c = s2_id(sm.rl[i]);
         rl_out[i] = c;
         atomicOr(zm + c, 1u << g);
+        atomicOr(sm.rbits + (c >> 5), 1u << (c & 31));
       }
       __threadfence_block();
       __syncthreads();
@@ -402,14 +434,16 @@ __global__ void __launch_bounds__(S2_THREADS) select_v3_kernel(IndexView ix, Ste
       if (e > 0) {
         for (int base = 0; base < m; base += blockDim.x) {
           const int c = base + threadIdx.x;
-          const bool f = c < m && (double)s[c] > (double)tau_e + B2 && !(__ldcg(zm + c) & (1u << g));
-          if (f) atomicOr(zm + c, 1u << (8 + g));
+          const bool f = c < m && (double)(cached ? u2f_ord(sm.keys[c]) : s[c]) > (double)tau_e + B2 &&
+                         !((sm.rbits[c >> 5] >> (c & 31)) & 1u);
+          if (f) { atomicOr(zm + c, 1u << (8 + g)); atomicOr(sm.ebits + (c >> 5), 1u << (c & 31)); }
           if (el_out) warp_append(f, c, el_out, &sm.n_el, sv.e_cap);
         }
         for (int i = threadIdx.x; i < nbe; i += blockDim.x) {
           const int c = sm.bid_e[i];
-          if (sm.bsel_e[i] && !(__ldcg(zm + c) & (1u << g))) {
+          if (sm.bsel_e[i] && !((sm.rbits[c >> 5] >> (c & 31)) & 1u)) {
             atomicOr(zm + c, 1u << (8 + g));
+            atomicOr(sm.ebits + (c >> 5), 1u << (c & 31));
             if (el_out) el_out[atomicAdd(&sm.n_el, 1)] = c;
           }
         }
@@ -421,7 +455,7 @@ __global__ void __launch_bounds__(S2_THREADS) select_v3_kernel(IndexView ix, Ste
         for (int c = threadIdx.x; c < m; c += blockDim.x) {
           const float v = s[c] * isd;
           mx_a = fmaxf(mx_a, v);
-          if (!(__ldcg(zm + c) & ((1u << g) | (1u << (8 + g))))) mx_t = fmaxf(mx_t, v);
+          if (!(((sm.rbits[c >> 5] | sm.ebits[c >> 5]) >> (c & 31)) & 1u)) mx_t = fmaxf(mx_t, v);
         }
         mx_t = s2_block_reduce(mx_t, true, sm);
         mx_a = s2_block_reduce(mx_a, true, sm);
@@ -430,7 +464,7 @@ __global__ void __launch_bounds__(S2_THREADS) select_v3_kernel(IndexView ix, Ste
           const float v = s[c] * isd;
           const float sz = (float)csize[c];
           da += sz * expf(v - mx_a);
-          if (!(__ldcg(zm + c) & ((1u << g) | (1u << (8 + g))))) dt += sz * expf(v - mx_t);
+          if (!(((sm.rbits[c >> 5] | sm.ebits[c >> 5]) >> (c & 31)) & 1u)) dt += sz * expf(v - mx_t);
         }
         dt = s2_block_reduce(dt, false, sm);
         da = s2_block_reduce(da, false, sm);
@@ -447,46 +481,80 @@ __global__ void __launch_bounds__(S2_THREADS) select_v3_kernel(IndexView ix, Ste
   if (!sm.last) return;
   __threadfence();
   if (threadIdx.x == 0) sv.sel_done[u] = 0;
-  s2_union(ix, sv, u, m, sm);
+  s2_union(ix, sv, u, m, G, sm);
 }
 
 
 
 
 // ===========================================================================
-// attend_v3
+// attend_v3 (v4 inner loop)
+//   QK: lane = (token j, head h) computes the full d-dim dot of its pair from
+//       the stage (K rows padded to 16B*odd stride: conflict-free broadcast
+//       reads) against q[h] in smem, with packed FFMA2.
+//   softmax: per head over the group (xor shuffles among same-head lanes).
+//   PV: lane = d/32 contiguous dims; p[j][h] read back from smem as float4
+//       / 2xfloat4 broadcasts; packed FFMA2.
+//   Rows past the end of a zone are bulk-copied from a zero row, so the
+//   hot loop carries no per-row predicates.
 // ===========================================================================
+__device__ __align__(16) unsigned char g_zero_row[1024];
+
 template <typename T, int DL, int HS, bool FULL>
 struct AttV3Cfg {
   static constexpr int RG = 32 / HS;                        // rows per group
   static constexpr int NST = 3;                             // stages per warp
-  static constexpr int ROWT = 32 * DL * (int)sizeof(T);     // K or V row bytes
-  static constexpr int ROWV = 32 * DL * 4;                  // value-sum row bytes
-  static constexpr int SB = RG * (2 * ROWT > ROWV ? 2 * ROWT : ROWV);  // stage bytes
+  static constexpr int D = 32 * DL;
+  static constexpr int ROWT = D * (int)sizeof(T);           // K or V row bytes
+  static constexpr int KST = ROWT + 16;                     // padded K row stride
+  static constexpr int ROWV = D * 4;                        // value-sum row bytes
+  static constexpr int SBT = RG * KST + RG * ROWT;          // token stage bytes
+  static constexpr int SB = ((SBT > RG * ROWV ? SBT : RG * ROWV) + 127) / 128 * 128;
   static constexpr int WARPS = 8;
-  static constexpr size_t META = (size_t)WARPS * NST * 32 * 12;  // per-stage lane metadata
-  static constexpr size_t SMEM = (size_t)WARPS * NST * SB + (size_t)WARPS * NST * 8 + 64 + META;
+  static constexpr int PB = RG * HS * 4;                    // p buffer bytes per warp
+  static constexpr size_t SMEM = (size_t)WARPS * NST * SB + (size_t)WARPS * NST * 8 + 64 +
+                                 (size_t)WARPS * NST * 32 * 12 + (size_t)WARPS * PB + (size_t)HS * D * 4;
+};
+
+template <typename T> struct Cvt8;
+template <> struct Cvt8<__nv_bfloat16> {  // 16 bytes = 8 elements
+  static constexpr int N = 8;
+  static __device__ __forceinline__ void run(const uint4& r, float2 (&o)[4]) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r);
+#pragma unroll
+    for (int i = 0; i < 4; i++) o[i] = __bfloat1622float2(h[i]);
+  }
+};
+template <> struct Cvt8<float> {  // 16 bytes = 4 elements
+  static constexpr int N = 4;
+  static __device__ __forceinline__ void run(const uint4& r, float2 (&o)[4]) {
+    o[0] = make_float2(__uint_as_float(r.x), __uint_as_float(r.y));
+    o[1] = make_float2(__uint_as_float(r.z), __uint_as_float(r.w));
+  }
 };
 
 template <typename T, int DL, int HS, bool FULL>
 __global__ void __launch_bounds__(256, 2) attend_v3_kernel(IndexView ix, SteadyView st, StepView sv, AttnParams p,
                                                             const int32_t* __restrict__ n_store) {
   using CF = AttV3Cfg<T, DL, HS, FULL>;
-  constexpr int RG = CF::RG, NST = CF::NST, ROWT = CF::ROWT, ROWV = CF::ROWV, SB = CF::SB;
-  using LT = RowLoad<T, DL>;
+  constexpr int RG = CF::RG, NST = CF::NST, ROWT = CF::ROWT, KST = CF::KST, ROWV = CF::ROWV, SB = CF::SB;
+  constexpr int D = CF::D;
   const int s_idx = blockIdx.x, u = blockIdx.y, S = gridDim.x;
-  const int G = p.G, d = 32 * DL;
+  const int G = p.G;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   extern __shared__ __align__(128) unsigned char at3[];
   unsigned char* ring = at3 + (size_t)warp * NST * SB;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(at3 + (size_t)CF::WARPS * NST * SB) + warp * NST;
-  int* wkind = reinterpret_cast<int*>(at3 + (size_t)CF::WARPS * NST * SB + (size_t)CF::WARPS * NST * 8);
-  // per-stage metadata of this lane: [NST][32] mask / logit / weight
-  unsigned char* meta = at3 + (size_t)CF::WARPS * NST * SB + (size_t)CF::WARPS * NST * 8 + 64 +
-                        (size_t)warp * NST * 32 * 12;
+  unsigned char* tail_base = at3 + (size_t)CF::WARPS * NST * SB;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(tail_base) + warp * NST;
+  int* wkind = reinterpret_cast<int*>(tail_base + (size_t)CF::WARPS * NST * 8);
+  unsigned char* meta = tail_base + (size_t)CF::WARPS * NST * 8 + 64 + (size_t)warp * NST * 32 * 12;
   int* smask = reinterpret_cast<int*>(meta);
   float* sx = reinterpret_cast<float*>(meta + NST * 32 * 4);
   float* sw = reinterpret_cast<float*>(meta + NST * 32 * 8);
+  float* pbuf = reinterpret_cast<float*>(tail_base + (size_t)CF::WARPS * NST * 8 + 64 +
+                                         (size_t)CF::WARPS * NST * 32 * 12) + warp * RG * HS;
+  float* qs = reinterpret_cast<float*>(tail_base + (size_t)CF::WARPS * NST * 8 + 64 +
+                                       (size_t)CF::WARPS * NST * 32 * 12 + (size_t)CF::WARPS * CF::PB);
 
   const int n_st = st.n[u];
   const int n_rt = FULL ? n_store[u] : sv.cnt[u * 4 + 1];
@@ -494,7 +562,6 @@ __global__ void __launch_bounds__(256, 2) attend_v3_kernel(IndexView ix, SteadyV
   const int g_st = (n_st + RG - 1) / RG, g_rt = (n_rt + RG - 1) / RG, g_eu = (n_eu + RG - 1) / RG;
   const long long NG = (long long)g_st + g_rt + g_eu;
   const int W = S * CF::WARPS, wg = s_idx * CF::WARPS + warp;
-  // warps per zone, proportional to the zone's groups (>= 1 when non-empty)
   int W0 = g_st ? max(1, (int)((long long)W * g_st / max(NG, 1LL))) : 0;
   int W2 = g_eu ? max(1, (int)((long long)W * g_eu / max(NG, 1LL))) : 0;
   int W1 = W - W0 - W2;
@@ -507,175 +574,197 @@ __global__ void __launch_bounds__(256, 2) attend_v3_kernel(IndexView ix, SteadyV
   const int gb = nw > 0 ? (int)((long long)li * gk / nw) : 0;
   const int ge = nw > 0 ? (int)((long long)(li + 1) * gk / nw) : 0;
 
+  const float isd = p.inv_sqrt_d;
+  for (int i = threadIdx.x; i < HS * D; i += blockDim.x) {
+    const int h = i / D;
+    qs[i] = h < G ? sv.q[((size_t)u * G + h) * D + (i % D)] * isd : 0.f;
+  }
   if (lane == 0) {
     for (int i = 0; i < NST; i++) mbar_init(bars + i, 1);
     fence_mbar_init();
     wkind[warp] = (ge > gb) ? kind : -1;
   }
-  __syncwarp();
+  __syncthreads();
 
-  const float isd = p.inv_sqrt_d;
-  float qv[HS][DL];
-#pragma unroll
-  for (int h = 0; h < HS; h++)
-#pragma unroll
-    for (int k = 0; k < DL; k++) qv[h][k] = h < G ? sv.q[((size_t)u * G + h) * d + lane * DL + k] * isd : 0.f;
-
-  const T* stk = (const T*)st.k + (size_t)u * st.t_cap * d;
-  const T* stv = (const T*)st.v + (size_t)u * st.t_cap * d;
-  const T* sk = (const T*)ix.store_k + (size_t)u * ix.s_cap * d;
-  const T* svv = (const T*)ix.store_v + (size_t)u * ix.s_cap * d;
+  const T* stk = (const T*)st.k + (size_t)u * st.t_cap * D;
+  const T* stv = (const T*)st.v + (size_t)u * st.t_cap * D;
+  const T* sk = (const T*)ix.store_k + (size_t)u * ix.s_cap * D;
+  const T* svv = (const T*)ix.store_v + (size_t)u * ix.s_cap * D;
   const int32_t* trow = FULL ? nullptr : sv.rtok_row + (size_t)u * sv.rt_cap;
   const uint8_t* tmk = FULL ? nullptr : sv.rtok_mask + (size_t)u * sv.rt_cap;
   const int32_t* eu = FULL ? nullptr : sv.eu_ids + (size_t)u * sv.eu_cap;
-  const uint8_t* emk = FULL ? nullptr : sv.eu_mask + (size_t)u * sv.eu_cap;
-  const float* scr = FULL ? nullptr : sv.scores + (size_t)u * G * ix.m_cap;
-  const int32_t* csz = ix.cl_size + (size_t)u * ix.m_cap;
-  const float* vsb = ix.VS32 + (size_t)u * ix.m_cap * d;
+  const float* eux = FULL ? nullptr : sv.eu_x + (size_t)u * sv.eu_cap * G;
+  const float* eusz = FULL ? nullptr : sv.eu_sz + (size_t)u * sv.eu_cap;
+  const float* vsb = ix.VS32 + (size_t)u * ix.m_cap * D;
   const int allmask = (1 << G) - 1;
   const int j_own = lane / HS, h_own = lane % HS;
 
   SoftState<HS> ss;
 #pragma unroll
   for (int h = 0; h < HS; h++) { ss.M[h] = -INFINITY; ss.D[h] = 0.f; }
-  float acc[HS][DL];
+  float2 acc[HS][DL / 2];
 #pragma unroll
   for (int h = 0; h < HS; h++)
 #pragma unroll
-    for (int k = 0; k < DL; k++) acc[h][k] = 0.f;
+    for (int k = 0; k < DL / 2; k++) acc[h][k] = make_float2(0.f, 0.f);
 
-
-  // fill stage `sti` with group `g`
-  auto issue = [&](int g, int sti) {
+  struct Meta { const void* k; const void* v; int mk; float x, w; };
+  auto load_meta = [&](int g) {
+    Meta mt{g_zero_row, g_zero_row, 0, -INFINITY, 0.f};
+    if (g >= ge) return mt;
     const int item0 = g * RG;
-    const int nv = min(RG, n_kind - item0);
-    unsigned char* stage = ring + sti * SB;
-    uint32_t bytes = (kind < 2) ? (uint32_t)(nv * 2 * ROWT) : (uint32_t)(nv * ROWV);
-    // metadata / source rows: lane j (< RG) owns row j
-    long long src = 0;
-    int mk = 0;
-    float x = -INFINITY, w = 0.f;
-    const int j = lane < RG ? lane : lane - RG;
-    if (j < nv && lane < 2 * RG) {
-      const int it = item0 + j;
-      if (kind == 0) { src = it; mk = allmask; }
-      else if (kind == 1) { src = FULL ? (long long)it : (long long)trow[it]; mk = FULL ? allmask : (int)tmk[it]; }
-      else { src = eu[it]; mk = emk[it]; w = (float)csz[src]; }
-    }
-    if (lane == 0) mbar_arrive_expect_tx(bars + sti, bytes);
-    __syncwarp();
-    if (j < nv && lane < 2 * RG) {
-      if (kind < 2) {
-        if (kind == 0 || kind == 1) {
-          const T* base = lane < RG ? (kind == 0 ? stk : sk) : (kind == 0 ? stv : svv);
-          bulk_g2s(stage + (lane < RG ? 0 : RG * ROWT) + j * ROWT, base + src * d, ROWT, bars + sti);
-        }
-      } else if (lane < RG) {
-        bulk_g2s(stage + j * ROWV, vsb + src * d, ROWV, bars + sti);
+    const int j = lane % RG;
+    const int it = item0 + j;
+    if (it < n_kind) {
+      if (kind == 0) { mt.k = stk + (size_t)it * D; mt.v = stv + (size_t)it * D; }
+      else if (kind == 1) {
+        const long long row = FULL ? (long long)it : (long long)__ldcg(trow + it);
+        mt.k = sk + (size_t)row * D; mt.v = svv + (size_t)row * D;
+      } else {
+        mt.k = vsb + (size_t)__ldcg(eu + it) * D;
       }
     }
-    // the logit of estimation rows is known now: keep (row j_own, head h_own) per lane
-    const int mk_own = __shfl_sync(0xffffffffu, mk, j_own);
-    const float w_own = __shfl_sync(0xffffffffu, w, j_own);
-    const long long c_own = __shfl_sync(0xffffffffu, src, j_own);
-    smask[sti * 32 + lane] = mk_own;
-    sw[sti * 32 + lane] = w_own;
-    if (kind == 2) {
-      x = -INFINITY;
-      if (j_own < nv && ((mk_own >> h_own) & 1)) x = scr[(size_t)h_own * ix.m_cap + c_own] * isd;
-      sx[sti * 32 + lane] = x;
+    const int io = item0 + j_own;
+    if (io < n_kind) {
+      if (kind == 0 || FULL) mt.mk = allmask;
+      else if (kind == 1) mt.mk = __ldcg(tmk + io);
+      else {
+        mt.x = h_own < G ? __ldcg(eux + (size_t)io * G + h_own) * isd : -INFINITY;
+        mt.w = __ldcg(eusz + io);
+      }
     }
+    return mt;
+  };
+  auto issue = [&](int sti, const Meta& mt) {
+    unsigned char* stage = ring + sti * SB;
+    if (lane == 0) mbar_arrive_expect_tx(bars + sti, kind < 2 ? (uint32_t)(RG * 2 * ROWT) : (uint32_t)(RG * ROWV));
+    __syncwarp();
+    if (lane < RG) {
+      if (kind < 2) {
+        bulk_g2s(stage + lane * KST, mt.k, ROWT, bars + sti);
+        bulk_g2s(stage + RG * KST + lane * ROWT, mt.v, ROWT, bars + sti);
+      } else {
+        bulk_g2s(stage + lane * ROWV, mt.k, ROWV, bars + sti);
+      }
+    }
+    smask[sti * 32 + lane] = mt.mk;
+    sx[sti * 32 + lane] = mt.x;
+    sw[sti * 32 + lane] = mt.w;
   };
 
-  auto compute = [&](int sti, int nv) {
+  auto compute = [&](int sti) {
     const unsigned char* stage = ring + sti * SB;
     float alpha[HS];
     float pw;
     if (kind < 2) {
-      float v[32];
+      // full dot of (token j_own, head h_own)
+      const unsigned char* kr = stage + j_own * KST;
+      const float* qh = qs + h_own * D;
+      float2 a2 = make_float2(0.f, 0.f);
+      constexpr int EPC = Cvt8<T>::N;  // elements per 16-byte chunk
+#pragma unroll 4
+      for (int t = 0; t < D; t += EPC) {
+        const uint4 raw = *reinterpret_cast<const uint4*>(kr + t * (int)sizeof(T));
+        float2 kf[4];
+        Cvt8<T>::run(raw, kf);
 #pragma unroll
-      for (int j = 0; j < RG; j++) {
-        float kf[DL];
-        LT::cvt(*reinterpret_cast<const typename LT::R*>(stage + j * ROWT + lane * DL * (int)sizeof(T)), kf);
-#pragma unroll
-        for (int h = 0; h < HS; h++) {
-          float a = 0.f;
-#pragma unroll
-          for (int k = 0; k < DL; k++) a = fmaf(kf[k], qv[h][k], a);
-          v[j * HS + h] = j < nv ? a : 0.f;
-        }
+        for (int i = 0; i < EPC / 2; i++) a2 = __ffma2_rn(kf[i], *reinterpret_cast<const float2*>(qh + t + 2 * i), a2);
       }
-      float x = transpose_reduce32(v);
-      if (!(j_own < nv && ((smask[sti * 32 + lane] >> h_own) & 1))) x = -INFINITY;
+      float x = a2.x + a2.y;
+      if (!((smask[sti * 32 + lane] >> h_own) & 1)) x = -INFINITY;
       pw = softmax_group<HS>(x, 1.f, ss, alpha);
     } else {
       pw = softmax_group<HS>(sx[sti * 32 + lane], sw[sti * 32 + lane], ss, alpha);
     }
+    pbuf[lane] = pw;  // index j*HS + h == lane
+    __syncwarp();
 #pragma unroll
-    for (int h = 0; h < HS; h++)
+    for (int h = 0; h < HS; h++) {
+      const float2 a = make_float2(alpha[h], alpha[h]);
 #pragma unroll
-      for (int k = 0; k < DL; k++) acc[h][k] *= alpha[h];
+      for (int k = 0; k < DL / 2; k++) acc[h][k] = __fmul2_rn(acc[h][k], a);
+    }
 #pragma unroll
     for (int j = 0; j < RG; j++) {
-      if (j < nv) {
-        float vf[DL];
-        if (kind < 2)
-          LT::cvt(*reinterpret_cast<const typename LT::R*>(stage + RG * ROWT + j * ROWT + lane * DL * (int)sizeof(T)), vf);
-        else
-          RowLoad<float, DL>::cvt(*reinterpret_cast<const typename RowLoad<float, DL>::R*>(stage + j * ROWV + lane * DL * 4), vf);
+      float2 vf[DL / 2];
+      if (kind < 2) {
+        const T* vr = reinterpret_cast<const T*>(stage + RG * KST + j * ROWT) + lane * DL;
+        if constexpr (sizeof(T) == 2) {
+          const __nv_bfloat162* v2 = reinterpret_cast<const __nv_bfloat162*>(vr);
 #pragma unroll
-        for (int h = 0; h < HS; h++) {
-          const float pj = __shfl_sync(0xffffffffu, pw, j * HS + h);
+          for (int k = 0; k < DL / 2; k++) vf[k] = __bfloat1622float2(v2[k]);
+        } else {
 #pragma unroll
-          for (int k = 0; k < DL; k++) acc[h][k] = fmaf(pj, vf[k], acc[h][k]);
+          for (int k = 0; k < DL / 2; k++) vf[k] = *reinterpret_cast<const float2*>(reinterpret_cast<const float*>(vr) + 2 * k);
         }
+      } else {
+        const float* vr = reinterpret_cast<const float*>(stage + j * ROWV) + lane * DL;
+#pragma unroll
+        for (int k = 0; k < DL / 2; k++) vf[k] = *reinterpret_cast<const float2*>(vr + 2 * k);
+      }
+#pragma unroll
+      for (int h = 0; h < HS; h++) {
+        const float pj = pbuf[j * HS + h];
+        const float2 p2 = make_float2(pj, pj);
+#pragma unroll
+        for (int k = 0; k < DL / 2; k++) acc[h][k] = __ffma2_rn(p2, vf[k], acc[h][k]);
       }
     }
   };
 
   if (ge > gb) {
+    Meta mnext = load_meta(gb);
 #pragma unroll
     for (int i = 0; i < NST - 1; i++)
-      if (gb + i < ge) issue(gb + i, i);
+      if (gb + i < ge) {
+        const Meta mcur = mnext;
+        mnext = load_meta(gb + i + 1);
+        issue(i, mcur);
+      }
     for (int g = gb; g < ge; g++) {
       const int k = g - gb;
       const int sti = k % NST;
       const int nxt = g + NST - 1;
       if (nxt < ge) {
+        const Meta mcur = mnext;
+        mnext = load_meta(nxt + 1);
         fence_proxy_async();
-        issue(nxt, (k + NST - 1) % NST);
+        issue((k + NST - 1) % NST, mcur);
       }
       mbar_wait(bars + sti, (uint32_t)((k / NST) & 1));
-      compute(sti, min(RG, n_kind - g * RG));
+      compute(sti);
       __syncwarp();
     }
   }
   // ---- per-warp partial into the warp's own ring, then CTA combine per kind
-  float* slot = reinterpret_cast<float*>(ring);  // [HS][2 + d]
+  float* slot = reinterpret_cast<float*>(ring);  // [HS][2 + D]
 #pragma unroll
   for (int h = 0; h < HS; h++) {
-    if (lane == 0) { slot[h * (2 + d)] = ss.M[h]; slot[h * (2 + d) + 1] = ss.D[h]; }
+    if (lane == 0) { slot[h * (2 + D)] = ss.M[h]; slot[h * (2 + D) + 1] = ss.D[h]; }
 #pragma unroll
-    for (int k = 0; k < DL; k++) slot[h * (2 + d) + 2 + lane * DL + k] = acc[h][k];
+    for (int k = 0; k < DL / 2; k++) {
+      slot[h * (2 + D) + 2 + lane * DL + 2 * k] = acc[h][k].x;
+      slot[h * (2 + D) + 2 + lane * DL + 2 * k + 1] = acc[h][k].y;
+    }
   }
   __syncthreads();
   for (int kk = 0; kk < 3; kk++) {
-    for (int idx = threadIdx.x; idx < G * (2 + d); idx += blockDim.x) {
-      const int h = idx / (2 + d), t = idx % (2 + d);
+    for (int idx = threadIdx.x; idx < G * (2 + D); idx += blockDim.x) {
+      const int h = idx / (2 + D), t = idx % (2 + D);
       float Mx = -INFINITY;
       for (int w = 0; w < CF::WARPS; w++)
         if (wkind[w] == kk) {
-          const float* sl = reinterpret_cast<const float*>(at3 + (size_t)w * NST * SB) + h * (2 + d);
+          const float* sl = reinterpret_cast<const float*>(at3 + (size_t)w * NST * SB) + h * (2 + D);
           if (sl[1] > 0.f) Mx = fmaxf(Mx, sl[0]);
         }
       float a = 0.f;
       if (t > 0 && Mx != -INFINITY)
         for (int w = 0; w < CF::WARPS; w++)
           if (wkind[w] == kk) {
-            const float* sl = reinterpret_cast<const float*>(at3 + (size_t)w * NST * SB) + h * (2 + d);
+            const float* sl = reinterpret_cast<const float*>(at3 + (size_t)w * NST * SB) + h * (2 + D);
             if (sl[1] > 0.f) a += sl[t] * __expf(sl[0] - Mx);
           }
-      float* out = sv.part + ((((size_t)u * S + s_idx) * G + h) * 3 + kk) * (size_t)(2 + d);
+      float* out = sv.part + ((((size_t)u * S + s_idx) * G + h) * 3 + kk) * (size_t)(2 + D);
       out[t] = t == 0 ? Mx : a;
     }
   }

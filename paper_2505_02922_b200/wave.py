@@ -144,6 +144,8 @@ class WaveLayer:
         self.rtok_row = torch.zeros((U, self.rt_cap), dtype=i32, device=dev)
         self.rtok_mask = torch.zeros((U, self.rt_cap), dtype=torch.uint8, device=dev)
         self.sel_done = torch.zeros(U, dtype=i32, device=dev)
+        self.eu_x = torch.zeros((U, self.eu_cap, G), dtype=f32, device=dev)
+        self.eu_sz = torch.zeros((U, self.eu_cap), dtype=f32, device=dev)
         self.tail = torch.zeros((U, G, 4), dtype=f32, device=dev)
         self.part = torch.zeros((U, self.S, G, 3, 2 + d), dtype=f32, device=dev)
         self.out = torch.zeros((U, G, d), dtype=f32, device=dev)
@@ -172,7 +174,8 @@ class WaveLayer:
             _ptr(self.ru_pre), _ptr(self.eu_ids), _ptr(self.eu_mask), _ptr(self.cnt),
             _ptr(self.tail), _ptr(self.part), _ptr(self.out), _ptr(self.logden), _ptr(self.cov),
             _ptr(self.status), self.r_cap, self.e_cap, self.ru_cap, self.eu_cap,
-            _ptr(self.rtok_row), _ptr(self.rtok_mask), _ptr(self.sel_done), self.rt_cap, 0)
+            _ptr(self.rtok_row), _ptr(self.rtok_mask), _ptr(self.sel_done), self.rt_cap, 0,
+            _ptr(self.eu_x), _ptr(self.eu_sz))
 
     # --------------------------------------------------------------- clustering
     def _run_segments(self, segs: list[dict]):
