@@ -128,13 +128,13 @@ static int dispatch_attend_v2(const IndexView& ix, const SteadyView& st, const S
   const int hs = head_slots(p.G);
   if (p.d == 128) {
     switch (hs) {
-      case 4: return launch_attend_v2<T, 4, 4, FULL>(ix, st, sv, p, n_store, U, S, s);
-      default: return launch_attend_v2<T, 4, 8, FULL>(ix, st, sv, p, n_store, U, S, s);
+      case 4: return launch_attend_v2<T, 8, 4, FULL>(ix, st, sv, p, n_store, U, S, s);
+      default: return launch_attend_v2<T, 8, 8, FULL>(ix, st, sv, p, n_store, U, S, s);
     }
   }
   switch (hs) {
-    case 4: return launch_attend_v2<T, 2, 4, FULL>(ix, st, sv, p, n_store, U, S, s);
-    default: return launch_attend_v2<T, 2, 8, FULL>(ix, st, sv, p, n_store, U, S, s);
+    case 4: return launch_attend_v2<T, 4, 4, FULL>(ix, st, sv, p, n_store, U, S, s);
+    default: return launch_attend_v2<T, 4, 8, FULL>(ix, st, sv, p, n_store, U, S, s);
   }
 }
 

@@ -196,19 +196,28 @@ __device__ void s2_union(const IndexView& ix, const StepView& sv, int u, int m, 
   uint8_t* tmk = sv.rtok_mask + (size_t)u * sv.rt_cap;
   const int T = blockDim.x, t = threadIdx.x;
   const int lo = (int)((long long)m * t / T), hi = (int)((long long)m * (t + 1) / T);
+  // stage the zone bits in smem (coalesced batch of independent loads), then
+  // clear them for the next step
+  unsigned int* zb = sm.keys;
+  const bool staged = zb != nullptr;
+  if (staged) {
+    for (int c = t; c < m; c += T) zb[c] = __ldcg(zm + c);
+    __syncthreads();
+    for (int c = t; c < m; c += T)
+      if (zb[c]) zm[c] = 0u;
+  }
   int nr = 0, ne = 0, nt = 0;
-#pragma unroll 4
   for (int c = lo; c < hi; c++) {
-    const uint32_t z = __ldcg(zm + c);
+    const uint32_t z = staged ? zb[c] : __ldcg(zm + c);
     if (z & 0xffu) { nr++; nt += csize[c]; }
     if (z & 0xff00u) ne++;
   }
   int tr, te, tt;
   scan3(nr, ne, nt, tr, te, tt, sm);
   for (int c = lo; c < hi; c++) {
-    const uint32_t z = __ldcg(zm + c);
+    const uint32_t z = staged ? zb[c] : __ldcg(zm + c);
     if (!z) continue;
-    zm[c] = 0u;
+    if (!staged) zm[c] = 0u;
     if (z & 0xffu) {
       const int sz = csize[c];
       if (nr < sv.ru_cap && nt + sz <= sv.rt_cap) {
@@ -227,12 +236,6 @@ __device__ void s2_union(const IndexView& ix, const StepView& sv, int u, int m, 
       if (ne < sv.eu_cap) {
         eu[ne] = c;
         emk[ne] = (uint8_t)((z >> 8) & 0xffu);
-        if (sv.eu_x) {
-          for (int h = 0; h < sv_G; h++)
-            sv.eu_x[((size_t)u * sv.eu_cap + ne) * sv_G + h] =
-                ((z >> (8 + h)) & 1u) ? sv.scores[((size_t)u * sv_G + h) * ix.m_cap + c] : -INFINITY;
-          sv.eu_sz[(size_t)u * sv.eu_cap + ne] = (float)csize[c];
-        }
       } else {
         set_status(sv.status, kErrUnion);
       }
@@ -328,13 +331,14 @@ __global__ void __launch_bounds__(S2_THREADS) select_v3_kernel(IndexView ix, Ste
     if (threadIdx.x == 0) { sm.n_in_r = 0; sm.n_band_r = 0; sm.n_band_e = 0; sm.n_in_e = 0; sm.n_rl = 0; }
     __syncthreads();
     int my_in_e = 0;
+    const int rl_cap = (int)sel_rlcap(r_max);
     for (int base = 0; base < m; base += blockDim.x) {
       const int c = base + threadIdx.x;
       const bool act = c < m;
       const double sc = act ? (double)(cached ? u2f_ord(sm.keys[c]) : s[c]) : -INFINITY;
       const bool in_r = act && sc > (double)tau_r + B2;
       const bool bd_r = act && !in_r && sc >= (double)tau_r - B2;
-      warp_append(in_r, c, reinterpret_cast<int*>(sm.ex), &sm.n_rl, (int)sel_rlcap(r_max));  // ids staged in ex[]
+      warp_append(in_r, c, reinterpret_cast<int*>(sm.ex), &sm.n_rl, rl_cap);  // ids staged in ex[]
       warp_append(bd_r, c, sm.bid_r, &sm.n_band_r, S2_BAND);
       if (e > 0) {
         const bool in_e = act && sc > (double)tau_e + B2;
@@ -488,73 +492,101 @@ __global__ void __launch_bounds__(S2_THREADS) select_v3_kernel(IndexView ix, Ste
 
 
 // ===========================================================================
-// attend_v3 (v4 inner loop)
-//   QK: lane = (token j, head h) computes the full d-dim dot of its pair from
-//       the stage (K rows padded to 16B*odd stride: conflict-free broadcast
-//       reads) against q[h] in smem, with packed FFMA2.
-//   softmax: per head over the group (xor shuffles among same-head lanes).
-//   PV: lane = d/32 contiguous dims; p[j][h] read back from smem as float4
-//       / 2xfloat4 broadcasts; packed FFMA2.
-//   Rows past the end of a zone are bulk-copied from a zero row, so the
-//   hot loop carries no per-row predicates.
+// attend_v3 (v5 inner loop): half-warp rows.
+//   A group is RG rows; lanes 0-15 take the even rows, lanes 16-31 the odd
+//   rows, each lane owning DPL = d/16 contiguous dims of its rows (one 16-byte
+//   smem read per row for bf16 d=128).  QK partials (RG/2 rows x HS heads = 16
+//   per lane) are reduced over the 16 lanes of the half with a 15-shuffle
+//   transposed reduction; lane (half, sub) ends with the logit of token
+//   j = half + 2*(sub / HS), head sub % HS.  P.V accumulates per half and the
+//   halves are folded once per warp.  Packed FFMA2 throughout.  Rows past the
+//   end of a zone are bulk-copied from a zero row: no per-row predicates.
 // ===========================================================================
 __device__ __align__(16) unsigned char g_zero_row[1024];
 
-template <typename T, int DL, int HS, bool FULL>
+template <typename T, int DPL, int HS, bool FULL>
 struct AttV3Cfg {
-  static constexpr int RG = 32 / HS;                        // rows per group
+  static constexpr int RG = 32 / HS;                        // rows per group (8 or 4)
   static constexpr int NST = 3;                             // stages per warp
-  static constexpr int D = 32 * DL;
+  static constexpr int D = 16 * DPL;
   static constexpr int ROWT = D * (int)sizeof(T);           // K or V row bytes
-  static constexpr int KST = ROWT + 16;                     // padded K row stride
   static constexpr int ROWV = D * 4;                        // value-sum row bytes
-  static constexpr int SBT = RG * KST + RG * ROWT;          // token stage bytes
+  static constexpr int SBT = 2 * RG * ROWT;
   static constexpr int SB = ((SBT > RG * ROWV ? SBT : RG * ROWV) + 127) / 128 * 128;
   static constexpr int WARPS = 8;
-  static constexpr int PB = RG * HS * 4;                    // p buffer bytes per warp
   static constexpr size_t SMEM = (size_t)WARPS * NST * SB + (size_t)WARPS * NST * 8 + 64 +
-                                 (size_t)WARPS * NST * 32 * 12 + (size_t)WARPS * PB + (size_t)HS * D * 4;
+                                 (size_t)WARPS * NST * 32 * 12 + (size_t)WARPS * 32 * 4;
 };
 
-template <typename T> struct Cvt8;
-template <> struct Cvt8<__nv_bfloat16> {  // 16 bytes = 8 elements
-  static constexpr int N = 8;
-  static __device__ __forceinline__ void run(const uint4& r, float2 (&o)[4]) {
+// DPL elements of a row at `p` -> DPL/2 float2
+template <typename T, int DPL> struct RowF2;
+template <> struct RowF2<__nv_bfloat16, 8> {
+  static __device__ __forceinline__ void ld(const void* p, float2 (&o)[4]) {
+    const uint4 r = *reinterpret_cast<const uint4*>(p);
     const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r);
 #pragma unroll
     for (int i = 0; i < 4; i++) o[i] = __bfloat1622float2(h[i]);
   }
 };
-template <> struct Cvt8<float> {  // 16 bytes = 4 elements
-  static constexpr int N = 4;
-  static __device__ __forceinline__ void run(const uint4& r, float2 (&o)[4]) {
-    o[0] = make_float2(__uint_as_float(r.x), __uint_as_float(r.y));
-    o[1] = make_float2(__uint_as_float(r.z), __uint_as_float(r.w));
+template <> struct RowF2<__nv_bfloat16, 4> {
+  static __device__ __forceinline__ void ld(const void* p, float2 (&o)[2]) {
+    const uint2 r = *reinterpret_cast<const uint2*>(p);
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r);
+    o[0] = __bfloat1622float2(h[0]);
+    o[1] = __bfloat1622float2(h[1]);
+  }
+};
+template <> struct RowF2<float, 8> {
+  static __device__ __forceinline__ void ld(const void* p, float2 (&o)[4]) {
+    const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
+    o[0] = make_float2(a.x, a.y); o[1] = make_float2(a.z, a.w); o[2] = make_float2(b.x, b.y); o[3] = make_float2(b.z, b.w);
+  }
+};
+template <> struct RowF2<float, 4> {
+  static __device__ __forceinline__ void ld(const void* p, float2 (&o)[2]) {
+    const float4 a = *reinterpret_cast<const float4*>(p);
+    o[0] = make_float2(a.x, a.y); o[1] = make_float2(a.z, a.w);
   }
 };
 
-template <typename T, int DL, int HS, bool FULL>
+// 16 values summed over the 16 lanes of each half-warp; returns the total of
+// index (lane & 15)
+__device__ __forceinline__ float transpose_reduce16(float (&v)[16]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int off = 8; off >= 1; off >>= 1) {
+    const bool up = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < off; i++) {
+      const float send = up ? v[i] : v[i + off];
+      const float keep = up ? v[i + off] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  return v[0];
+}
+
+template <typename T, int DPL, int HS, bool FULL>
 __global__ void __launch_bounds__(256, 2) attend_v3_kernel(IndexView ix, SteadyView st, StepView sv, AttnParams p,
                                                             const int32_t* __restrict__ n_store) {
-  using CF = AttV3Cfg<T, DL, HS, FULL>;
-  constexpr int RG = CF::RG, NST = CF::NST, ROWT = CF::ROWT, KST = CF::KST, ROWV = CF::ROWV, SB = CF::SB;
-  constexpr int D = CF::D;
+  using CF = AttV3Cfg<T, DPL, HS, FULL>;
+  constexpr int RG = CF::RG, NST = CF::NST, ROWT = CF::ROWT, ROWV = CF::ROWV, SB = CF::SB;
+  constexpr int D = CF::D, RH = RG / 2, DP2 = DPL / 2;
   const int s_idx = blockIdx.x, u = blockIdx.y, S = gridDim.x;
   const int G = p.G;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int half = lane >> 4, sub = lane & 15;
   extern __shared__ __align__(128) unsigned char at3[];
   unsigned char* ring = at3 + (size_t)warp * NST * SB;
-  unsigned char* tail_base = at3 + (size_t)CF::WARPS * NST * SB;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(tail_base) + warp * NST;
-  int* wkind = reinterpret_cast<int*>(tail_base + (size_t)CF::WARPS * NST * 8);
-  unsigned char* meta = tail_base + (size_t)CF::WARPS * NST * 8 + 64 + (size_t)warp * NST * 32 * 12;
+  unsigned char* tb = at3 + (size_t)CF::WARPS * NST * SB;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(tb) + warp * NST;
+  int* wkind = reinterpret_cast<int*>(tb + (size_t)CF::WARPS * NST * 8);
+  unsigned char* meta = tb + (size_t)CF::WARPS * NST * 8 + 64 + (size_t)warp * NST * 32 * 12;
   int* smask = reinterpret_cast<int*>(meta);
   float* sx = reinterpret_cast<float*>(meta + NST * 32 * 4);
   float* sw = reinterpret_cast<float*>(meta + NST * 32 * 8);
-  float* pbuf = reinterpret_cast<float*>(tail_base + (size_t)CF::WARPS * NST * 8 + 64 +
-                                         (size_t)CF::WARPS * NST * 32 * 12) + warp * RG * HS;
-  float* qs = reinterpret_cast<float*>(tail_base + (size_t)CF::WARPS * NST * 8 + 64 +
-                                       (size_t)CF::WARPS * NST * 32 * 12 + (size_t)CF::WARPS * CF::PB);
+  float* pbuf = reinterpret_cast<float*>(tb + (size_t)CF::WARPS * NST * 8 + 64 + (size_t)CF::WARPS * NST * 32 * 12) +
+                warp * 32;
 
   const int n_st = st.n[u];
   const int n_rt = FULL ? n_store[u] : sv.cnt[u * 4 + 1];
@@ -574,17 +606,23 @@ __global__ void __launch_bounds__(256, 2) attend_v3_kernel(IndexView ix, SteadyV
   const int gb = nw > 0 ? (int)((long long)li * gk / nw) : 0;
   const int ge = nw > 0 ? (int)((long long)(li + 1) * gk / nw) : 0;
 
-  const float isd = p.inv_sqrt_d;
-  for (int i = threadIdx.x; i < HS * D; i += blockDim.x) {
-    const int h = i / D;
-    qs[i] = h < G ? sv.q[((size_t)u * G + h) * D + (i % D)] * isd : 0.f;
-  }
   if (lane == 0) {
     for (int i = 0; i < NST; i++) mbar_init(bars + i, 1);
     fence_mbar_init();
     wkind[warp] = (ge > gb) ? kind : -1;
   }
-  __syncthreads();
+  __syncwarp();
+
+  const float isd = p.inv_sqrt_d;
+  // q slice of this lane's dims, pre-scaled: qv[h][k] covers dims sub*DPL + 2k, +1
+  float2 qv[HS][DP2];
+#pragma unroll
+  for (int h = 0; h < HS; h++)
+#pragma unroll
+    for (int k = 0; k < DP2; k++) {
+      const float* qp = sv.q + ((size_t)u * G + (h < G ? h : 0)) * D + sub * DPL + 2 * k;
+      qv[h][k] = h < G ? make_float2(qp[0] * isd, qp[1] * isd) : make_float2(0.f, 0.f);
+    }
 
   const T* stk = (const T*)st.k + (size_t)u * st.t_cap * D;
   const T* stv = (const T*)st.v + (size_t)u * st.t_cap * D;
@@ -593,28 +631,29 @@ __global__ void __launch_bounds__(256, 2) attend_v3_kernel(IndexView ix, SteadyV
   const int32_t* trow = FULL ? nullptr : sv.rtok_row + (size_t)u * sv.rt_cap;
   const uint8_t* tmk = FULL ? nullptr : sv.rtok_mask + (size_t)u * sv.rt_cap;
   const int32_t* eu = FULL ? nullptr : sv.eu_ids + (size_t)u * sv.eu_cap;
-  const float* eux = FULL ? nullptr : sv.eu_x + (size_t)u * sv.eu_cap * G;
-  const float* eusz = FULL ? nullptr : sv.eu_sz + (size_t)u * sv.eu_cap;
+  const uint8_t* emk = FULL ? nullptr : sv.eu_mask + (size_t)u * sv.eu_cap;
+  const float* scr = FULL ? nullptr : sv.scores + (size_t)u * G * ix.m_cap;
+  const int32_t* csz = ix.cl_size + (size_t)u * ix.m_cap;
   const float* vsb = ix.VS32 + (size_t)u * ix.m_cap * D;
   const int allmask = (1 << G) - 1;
-  const int j_own = lane / HS, h_own = lane % HS;
+  // (token, head) whose logit this lane holds after the reduction
+  const int j_own = half + 2 * (sub / HS), h_own = sub % HS;
 
   SoftState<HS> ss;
 #pragma unroll
   for (int h = 0; h < HS; h++) { ss.M[h] = -INFINITY; ss.D[h] = 0.f; }
-  float2 acc[HS][DL / 2];
+  float2 acc[HS][DP2];
 #pragma unroll
   for (int h = 0; h < HS; h++)
 #pragma unroll
-    for (int k = 0; k < DL / 2; k++) acc[h][k] = make_float2(0.f, 0.f);
+    for (int k = 0; k < DP2; k++) acc[h][k] = make_float2(0.f, 0.f);
 
   struct Meta { const void* k; const void* v; int mk; float x, w; };
   auto load_meta = [&](int g) {
     Meta mt{g_zero_row, g_zero_row, 0, -INFINITY, 0.f};
     if (g >= ge) return mt;
     const int item0 = g * RG;
-    const int j = lane % RG;
-    const int it = item0 + j;
+    const int it = item0 + (lane % RG);
     if (it < n_kind) {
       if (kind == 0) { mt.k = stk + (size_t)it * D; mt.v = stv + (size_t)it * D; }
       else if (kind == 1) {
@@ -629,8 +668,10 @@ __global__ void __launch_bounds__(256, 2) attend_v3_kernel(IndexView ix, SteadyV
       if (kind == 0 || FULL) mt.mk = allmask;
       else if (kind == 1) mt.mk = __ldcg(tmk + io);
       else {
-        mt.x = h_own < G ? __ldcg(eux + (size_t)io * G + h_own) * isd : -INFINITY;
-        mt.w = __ldcg(eusz + io);
+        const int c = __ldcg(eu + io);
+        mt.mk = __ldcg(emk + io);
+        mt.x = ((mt.mk >> h_own) & 1) ? __ldcg(scr + (size_t)h_own * ix.m_cap + c) * isd : -INFINITY;
+        mt.w = (float)__ldcg(csz + c);
       }
     }
     return mt;
@@ -641,8 +682,8 @@ __global__ void __launch_bounds__(256, 2) attend_v3_kernel(IndexView ix, SteadyV
     __syncwarp();
     if (lane < RG) {
       if (kind < 2) {
-        bulk_g2s(stage + lane * KST, mt.k, ROWT, bars + sti);
-        bulk_g2s(stage + RG * KST + lane * ROWT, mt.v, ROWT, bars + sti);
+        bulk_g2s(stage + lane * ROWT, mt.k, ROWT, bars + sti);
+        bulk_g2s(stage + RG * ROWT + lane * ROWT, mt.v, ROWT, bars + sti);
       } else {
         bulk_g2s(stage + lane * ROWV, mt.k, ROWV, bars + sti);
       }
@@ -657,57 +698,46 @@ __global__ void __launch_bounds__(256, 2) attend_v3_kernel(IndexView ix, SteadyV
     float alpha[HS];
     float pw;
     if (kind < 2) {
-      // full dot of (token j_own, head h_own)
-      const unsigned char* kr = stage + j_own * KST;
-      const float* qh = qs + h_own * D;
-      float2 a2 = make_float2(0.f, 0.f);
-      constexpr int EPC = Cvt8<T>::N;  // elements per 16-byte chunk
-#pragma unroll 4
-      for (int t = 0; t < D; t += EPC) {
-        const uint4 raw = *reinterpret_cast<const uint4*>(kr + t * (int)sizeof(T));
-        float2 kf[4];
-        Cvt8<T>::run(raw, kf);
+      float v[16];
 #pragma unroll
-        for (int i = 0; i < EPC / 2; i++) a2 = __ffma2_rn(kf[i], *reinterpret_cast<const float2*>(qh + t + 2 * i), a2);
+      for (int jj = 0; jj < RH; jj++) {
+        const int j = half + 2 * jj;
+        float2 kf[DP2];
+        RowF2<T, DPL>::ld(stage + j * ROWT + sub * DPL * (int)sizeof(T), kf);
+#pragma unroll
+        for (int h = 0; h < HS; h++) {
+          float2 a2 = __fmul2_rn(kf[0], qv[h][0]);
+#pragma unroll
+          for (int k = 1; k < DP2; k++) a2 = __ffma2_rn(kf[k], qv[h][k], a2);
+          v[jj * HS + h] = a2.x + a2.y;
+        }
       }
-      float x = a2.x + a2.y;
+      float x = transpose_reduce16(v);
       if (!((smask[sti * 32 + lane] >> h_own) & 1)) x = -INFINITY;
       pw = softmax_group<HS>(x, 1.f, ss, alpha);
     } else {
       pw = softmax_group<HS>(sx[sti * 32 + lane], sw[sti * 32 + lane], ss, alpha);
     }
-    pbuf[lane] = pw;  // index j*HS + h == lane
+    pbuf[j_own * HS + h_own] = pw;
     __syncwarp();
 #pragma unroll
     for (int h = 0; h < HS; h++) {
       const float2 a = make_float2(alpha[h], alpha[h]);
 #pragma unroll
-      for (int k = 0; k < DL / 2; k++) acc[h][k] = __fmul2_rn(acc[h][k], a);
+      for (int k = 0; k < DP2; k++) acc[h][k] = __fmul2_rn(acc[h][k], a);
     }
 #pragma unroll
-    for (int j = 0; j < RG; j++) {
-      float2 vf[DL / 2];
-      if (kind < 2) {
-        const T* vr = reinterpret_cast<const T*>(stage + RG * KST + j * ROWT) + lane * DL;
-        if constexpr (sizeof(T) == 2) {
-          const __nv_bfloat162* v2 = reinterpret_cast<const __nv_bfloat162*>(vr);
-#pragma unroll
-          for (int k = 0; k < DL / 2; k++) vf[k] = __bfloat1622float2(v2[k]);
-        } else {
-#pragma unroll
-          for (int k = 0; k < DL / 2; k++) vf[k] = *reinterpret_cast<const float2*>(reinterpret_cast<const float*>(vr) + 2 * k);
-        }
-      } else {
-        const float* vr = reinterpret_cast<const float*>(stage + j * ROWV) + lane * DL;
-#pragma unroll
-        for (int k = 0; k < DL / 2; k++) vf[k] = *reinterpret_cast<const float2*>(vr + 2 * k);
-      }
+    for (int jj = 0; jj < RH; jj++) {
+      const int j = half + 2 * jj;
+      float2 vf[DP2];
+      if (kind < 2) RowF2<T, DPL>::ld(stage + RG * ROWT + j * ROWT + sub * DPL * (int)sizeof(T), vf);
+      else RowF2<float, DPL>::ld(stage + j * ROWV + sub * DPL * 4, vf);
 #pragma unroll
       for (int h = 0; h < HS; h++) {
         const float pj = pbuf[j * HS + h];
         const float2 p2 = make_float2(pj, pj);
 #pragma unroll
-        for (int k = 0; k < DL / 2; k++) acc[h][k] = __ffma2_rn(p2, vf[k], acc[h][k]);
+        for (int k = 0; k < DP2; k++) acc[h][k] = __ffma2_rn(p2, vf[k], acc[h][k]);
       }
     }
   };
@@ -736,15 +766,25 @@ __global__ void __launch_bounds__(256, 2) attend_v3_kernel(IndexView ix, SteadyV
       __syncwarp();
     }
   }
+  // fold the two halves (same heads, same dims, disjoint rows)
+#pragma unroll
+  for (int h = 0; h < HS; h++)
+#pragma unroll
+    for (int k = 0; k < DP2; k++) {
+      acc[h][k].x += __shfl_xor_sync(0xffffffffu, acc[h][k].x, 16);
+      acc[h][k].y += __shfl_xor_sync(0xffffffffu, acc[h][k].y, 16);
+    }
   // ---- per-warp partial into the warp's own ring, then CTA combine per kind
   float* slot = reinterpret_cast<float*>(ring);  // [HS][2 + D]
+  if (half == 0) {
 #pragma unroll
-  for (int h = 0; h < HS; h++) {
-    if (lane == 0) { slot[h * (2 + D)] = ss.M[h]; slot[h * (2 + D) + 1] = ss.D[h]; }
+    for (int h = 0; h < HS; h++) {
+      if (sub == 0) { slot[h * (2 + D)] = ss.M[h]; slot[h * (2 + D) + 1] = ss.D[h]; }
 #pragma unroll
-    for (int k = 0; k < DL / 2; k++) {
-      slot[h * (2 + D) + 2 + lane * DL + 2 * k] = acc[h][k].x;
-      slot[h * (2 + D) + 2 + lane * DL + 2 * k + 1] = acc[h][k].y;
+      for (int k = 0; k < DP2; k++) {
+        slot[h * (2 + D) + 2 + sub * DPL + 2 * k] = acc[h][k].x;
+        slot[h * (2 + D) + 2 + sub * DPL + 2 * k + 1] = acc[h][k].y;
+      }
     }
   }
   __syncthreads();
@@ -780,14 +820,14 @@ size_t attend_v3_smem() { return AttV3Cfg<T, DL, HS, FULL>::SMEM; }
                                                             const int32_t*);                               \
   template size_t attend_v3_smem<T, DL, HS, false>();                                                      \
   template size_t attend_v3_smem<T, DL, HS, true>();
+WK_INST_ATT3(__nv_bfloat16, 8, 4)
+WK_INST_ATT3(__nv_bfloat16, 8, 8)
 WK_INST_ATT3(__nv_bfloat16, 4, 4)
 WK_INST_ATT3(__nv_bfloat16, 4, 8)
-WK_INST_ATT3(__nv_bfloat16, 2, 4)
-WK_INST_ATT3(__nv_bfloat16, 2, 8)
+WK_INST_ATT3(float, 8, 4)
+WK_INST_ATT3(float, 8, 8)
 WK_INST_ATT3(float, 4, 4)
 WK_INST_ATT3(float, 4, 8)
-WK_INST_ATT3(float, 2, 4)
-WK_INST_ATT3(float, 2, 8)
 
 // ===========================================================================
 // score_v3: grid = (nblk, U), block = 128 (4 warps); each warp streams a
