@@ -29,6 +29,10 @@ size_t select_smem_bytes();
 // decode_v2.cu
 template <int HS>
 __global__ void score_v2_kernel(IndexView, StepView, int, int, int);
+// select_v4.cu
+template <int PT>
+__global__ void select_v4_kernel(IndexView, StepView, SelParams);
+size_t select_v4_smem();
 // decode_v3.cu
 __global__ void select_v3_kernel(IndexView, StepView, SelParams, int, int);
 size_t sel_smem_bytes(int m_max, int r_max);
@@ -77,6 +81,8 @@ static int configure_smem() {
   if (cudaFuncSetAttribute(attend_kernel<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, at) != cudaSuccess) return WK_ECUDA;
   if (cudaFuncSetAttribute(attend_kernel<__nv_bfloat16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, at) != cudaSuccess) return WK_ECUDA;
   if (cudaFuncSetAttribute(select_v3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess) return WK_ECUDA;
+  if (cudaFuncSetAttribute(select_v4_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)select_v4_smem()) != cudaSuccess) return WK_ECUDA;
+  if (cudaFuncSetAttribute(select_v4_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)select_v4_smem()) != cudaSuccess) return WK_ECUDA;
   const int rs = (int)recall_smem_bytes();
   if (cudaFuncSetAttribute(recall_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, rs) != cudaSuccess) return WK_ECUDA;
   if (cudaFuncSetAttribute(recall_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, rs) != cudaSuccess) return WK_ECUDA;
@@ -219,7 +225,12 @@ int wk_score_topk(const wk_index_view* ix, const wk_step_view* sv, const wk_zone
   p.need_tail = zp->tail_denominator_only;
   p.need_allc = zp->denominator_eq2;
   if (v2) {
-    select_v3_kernel<<<U * zp->G, 256, sel_smem_bytes(m_max, sv->r_cap), s>>>(*ix, *sv, p, m_max, sv->r_cap);
+    if (m_max <= 8192 && (zp->d % 32) == 0)
+      select_v4_kernel<16><<<U * zp->G, 512, select_v4_smem(), s>>>(*ix, *sv, p);
+    else if (m_max <= 16384 && (zp->d % 32) == 0)
+      select_v4_kernel<32><<<U * zp->G, 512, select_v4_smem(), s>>>(*ix, *sv, p);
+    else
+      select_v3_kernel<<<U * zp->G, 256, sel_smem_bytes(m_max, sv->r_cap), s>>>(*ix, *sv, p, m_max, sv->r_cap);
     WK_CHECK_LAUNCH();
     return 0;
   }

@@ -26,6 +26,14 @@ namespace wk {
 // ---------------------------------------------------------------------------
 // select_v3: exact zones (index.py:61-93) + unit unions
 // ---------------------------------------------------------------------------
+__device__ long long g_sel_dbg[4096][16];  // per-CTA phase timestamps (globaltimer, ns)
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define SEL_MARK(i) do { if (threadIdx.x == 0 && blockIdx.x < 4096) g_sel_dbg[blockIdx.x][i] = gtimer(); } while (0)
+
 constexpr int S2_THREADS = 256;
 constexpr int S2_BAND = 512;
 constexpr int S2_RL = 4096;     // max r (retrieval clusters per head)
@@ -286,6 +294,7 @@ __global__ void __launch_bounds__(S2_THREADS) select_v3_kernel(IndexView ix, Ste
     sm.ebits = reinterpret_cast<unsigned int*>(q);
   }
   __syncthreads();
+  SEL_MARK(0);
   const int G = p.G, d = p.d;
   const int u = blockIdx.x / G, g = blockIdx.x % G;
   const int m = sv.m[u];
@@ -325,9 +334,11 @@ __global__ void __launch_bounds__(S2_THREADS) select_v3_kernel(IndexView ix, Ste
     const double B = 2.0 * (gam + uu + 1e-13) * (1.0 + 1e-5) * sqrt((double)qn2) * (1.0 + 1e-5) *
                      (double)cmax * (1.0 + 1e-5);
     const double B2 = 2.0 * B;
+    SEL_MARK(1);
     const unsigned* kp = cached ? sm.keys : nullptr;
     const float tau_r = u2f_ord(s2_kth_largest(kp, s, m, r, sm));
     const float tau_e = e > 0 ? u2f_ord(s2_kth_largest(kp, s, m, r + e, sm)) : 0.f;
+    SEL_MARK(2);
     if (threadIdx.x == 0) { sm.n_in_r = 0; sm.n_band_r = 0; sm.n_band_e = 0; sm.n_in_e = 0; sm.n_rl = 0; }
     __syncthreads();
     int my_in_e = 0;
@@ -350,7 +361,9 @@ __global__ void __launch_bounds__(S2_THREADS) select_v3_kernel(IndexView ix, Ste
     my_in_e = __reduce_add_sync(FULLMASK, my_in_e);
     if (lane == 0 && my_in_e) atomicAdd(&sm.n_in_e, my_in_e);
     __syncthreads();
+    SEL_MARK(3);
     const int nin_r = sm.n_rl, nbr = sm.n_band_r, nbe = sm.n_band_e, nin_e = sm.n_in_e;
+    if (threadIdx.x == 0 && blockIdx.x < 4096) { g_sel_dbg[blockIdx.x][12] = nbr; g_sel_dbg[blockIdx.x][13] = nbe; }
     const bool bad = nbr > S2_BAND || nbe > S2_BAND || nin_r > r || nin_r + nbr < r ||
                      (e > 0 && (nin_e > r + e || nin_e + nbe < r + e));
     if (bad) {
@@ -377,6 +390,7 @@ __global__ void __launch_bounds__(S2_THREADS) select_v3_kernel(IndexView ix, Ste
         sm.bsel_e[i] = rank < need_e ? 1 : 0;
       }
       __syncthreads();
+      SEL_MARK(4);
       // bitonic sort of the r retrieval keys
       int npow = 1;
       while (npow < r) npow <<= 1;
@@ -393,6 +407,7 @@ __global__ void __launch_bounds__(S2_THREADS) select_v3_kernel(IndexView ix, Ste
           }
           __syncthreads();
         }
+      SEL_MARK(5);
       // clumps of neighbours closer than 2B: exact scores, exact order
       for (int i = threadIdx.x; i < r; i += blockDim.x) {
         const double si = (double)s2_score(sm.rl[i]);
@@ -423,6 +438,7 @@ __global__ void __launch_bounds__(S2_THREADS) select_v3_kernel(IndexView ix, Ste
         }
       }
       __syncthreads();
+      SEL_MARK(6);
       int32_t* rl_out = sv.rlist + ((size_t)u * G + g) * sv.r_cap;
       for (int i = threadIdx.x; i < r; i += blockDim.x) {
         const int c = s2_id(sm.rl[i]);
@@ -453,6 +469,7 @@ __global__ void __launch_bounds__(S2_THREADS) select_v3_kernel(IndexView ix, Ste
         }
       }
       __syncthreads();
+      SEL_MARK(7);
       if (p.need_tail || p.need_allc) {
         const float isd = p.inv_sqrt_d;
         float mx_t = -INFINITY, mx_a = -INFINITY;
@@ -477,6 +494,7 @@ __global__ void __launch_bounds__(S2_THREADS) select_v3_kernel(IndexView ix, Ste
     }
   }
   if (!ok && threadIdx.x == 0) { tailp[0] = -INFINITY; tailp[1] = 0.f; tailp[2] = -INFINITY; tailp[3] = 0.f; }
+  SEL_MARK(8);
   // ---- the last CTA of the unit builds the unions ----
   __threadfence();
   __syncthreads();
@@ -485,7 +503,9 @@ __global__ void __launch_bounds__(S2_THREADS) select_v3_kernel(IndexView ix, Ste
   if (!sm.last) return;
   __threadfence();
   if (threadIdx.x == 0) sv.sel_done[u] = 0;
+  SEL_MARK(9);
   s2_union(ix, sv, u, m, G, sm);
+  SEL_MARK(10);
 }
 
 
@@ -925,3 +945,7 @@ template size_t score_v3_smem<4, 2>();
 template size_t score_v3_smem<8, 2>();
 
 }  // namespace wk
+
+extern "C" int wk_debug_select_timing(long long* out, int n) {
+  return cudaMemcpyFromSymbol(out, wk::g_sel_dbg, sizeof(long long) * 16 * (size_t)n) == cudaSuccess ? 0 : -2;
+}

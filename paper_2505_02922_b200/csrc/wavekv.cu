@@ -4,6 +4,7 @@
 #include "decode.cu"
 #include "decode_v2.cu"
 #include "decode_v3.cu"
+#include "select_v4.cu"
 #include "cache.cu"
 #include "metrics.cu"
 #include "abi.cu"
