@@ -29,6 +29,8 @@ size_t select_smem_bytes();
 // decode_v2.cu
 template <int HS>
 __global__ void score_v2_kernel(IndexView, StepView, int, int, int);
+// select_v5.cu
+__global__ void select_v5_kernel(IndexView, StepView, SelParams);
 // select_v4.cu
 template <int PT>
 __global__ void select_v4_kernel(IndexView, StepView, SelParams);
@@ -225,10 +227,9 @@ int wk_score_topk(const wk_index_view* ix, const wk_step_view* sv, const wk_zone
   p.need_tail = zp->tail_denominator_only;
   p.need_allc = zp->denominator_eq2;
   if (v2) {
-    if (m_max <= 8192 && (zp->d % 32) == 0)
-      select_v4_kernel<16><<<U * zp->G, 512, select_v4_smem(), s>>>(*ix, *sv, p);
-    else if (m_max <= 16384 && (zp->d % 32) == 0)
-      select_v4_kernel<32><<<U * zp->G, 512, select_v4_smem(), s>>>(*ix, *sv, p);
+    const double r_max = floor(zp->retrieval_fraction * (double)m_max + 0.5) + 1;
+    if (r_max <= 384 && (zp->d % 32) == 0)
+      select_v5_kernel<<<U * zp->G, 256, 0, s>>>(*ix, *sv, p);
     else
       select_v3_kernel<<<U * zp->G, 256, sel_smem_bytes(m_max, sv->r_cap), s>>>(*ix, *sv, p, m_max, sv->r_cap);
     WK_CHECK_LAUNCH();

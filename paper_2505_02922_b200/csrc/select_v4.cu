@@ -15,6 +15,9 @@
 
 namespace wk {
 
+// g_sel_dbg: defined in decode_v3.cu (same translation unit)
+#define S4_MARK(i) do { if (threadIdx.x == 0 && blockIdx.x < 4096) { long long _t; asm volatile("mov.u64 %0, %globaltimer;" : "=l"(_t)); g_sel_dbg[blockIdx.x][i] = _t; } } while (0)
+
 constexpr int S4_THREADS = 512;
 constexpr int S4_NB = 1024;      // histogram buckets
 constexpr int S4_LIST = 1024;    // bucket-collection capacity
@@ -336,6 +339,7 @@ template <int PT>
 __global__ void __launch_bounds__(S4_THREADS) select_v4_kernel(IndexView ix, StepView sv, SelParams p) {
   extern __shared__ __align__(128) unsigned char s4_raw[];
   Sel4Smem& sm = *reinterpret_cast<Sel4Smem*>(s4_raw);
+  S4_MARK(0);
   const int G = p.G, d = p.d;
   const int u = blockIdx.x / G, g = blockIdx.x % G;
   const int m = sv.m[u];
@@ -388,10 +392,12 @@ __global__ void __launch_bounds__(S4_THREADS) select_v4_kernel(IndexView ix, Ste
     const double B = 2.0 * (gam + uu + 1e-13) * (1.0 + 1e-5) * sqrt((double)qn2) * (1.0 + 1e-5) *
                      (double)cmax * (1.0 + 1e-5);
     const double B2 = 2.0 * B;
+    S4_MARK(1);
     float tau_r = 0.f, tau_e = 0.f;
     if (!s4_two_thresholds<PT>(sc, m, r, e > 0 ? r + e : 0, smin, smax, sm, tau_r, tau_e)) {
       set_status(sv.status, kErrBandOverflow);
     } else {
+      S4_MARK(2);
       // ---- classification (registers) ----
       if (t == 0) { sm.n_rl = 0; sm.n_band_r = 0; sm.n_band_e = 0; sm.n_in_e = 0; sm.n_el = 0; }
       __syncthreads();
@@ -417,7 +423,9 @@ __global__ void __launch_bounds__(S4_THREADS) select_v4_kernel(IndexView ix, Ste
       my_in_e = __reduce_add_sync(0xffffffffu, my_in_e);
       if (lane == 0 && my_in_e) atomicAdd(&sm.n_in_e, my_in_e);
       __syncthreads();
+      S4_MARK(3);
       const int nin_r = sm.n_rl, nbr = sm.n_band_r, nbe = sm.n_band_e, nin_e = sm.n_in_e;
+      if (t == 0) { g_sel_dbg[blockIdx.x][12] = nbr; g_sel_dbg[blockIdx.x][13] = nbe; g_sel_dbg[blockIdx.x][14] = sm.n1; g_sel_dbg[blockIdx.x][15] = sm.n2; }
       const bool bad = r > S4_RL || nbr > S4_BAND || nbe > S4_BAND || nin_r > r || nin_r + nbr < r ||
                        (e > 0 && (nin_e > r + e || nin_e + nbe < r + e));
       if (bad) {
@@ -445,12 +453,14 @@ __global__ void __launch_bounds__(S4_THREADS) select_v4_kernel(IndexView ix, Ste
           sm.bsel_e[i] = rank < need_e ? 1 : 0;
         }
         __syncthreads();
+        S4_MARK(4);
         // ---- order the retrieval list: warp 0 sorts, every warp re-scores clumps
         if (r <= 256) { if (warp == 0) s4_warp_sort(sm.rl, r); }
         else s4_block_sort(sm.rl, r);
         __syncthreads();
         for (int i = t; i < r; i += T) sm.rex[i] = 0.0;
         __syncthreads();
+        S4_MARK(5);
         // clump members: exact scores (one warp per member)
         for (int i = warp; i < r; i += nwarps) {
           const double si = (double)s4_score(sm.rl[i]);
@@ -485,6 +495,7 @@ __global__ void __launch_bounds__(S4_THREADS) select_v4_kernel(IndexView ix, Ste
           }
         }
         __syncthreads();
+        S4_MARK(6);
         // ---- outputs ----
         int32_t* rl_out = sv.rlist + ((size_t)u * G + g) * sv.r_cap;
         for (int i = t; i < r; i += T) {
@@ -549,6 +560,7 @@ __global__ void __launch_bounds__(S4_THREADS) select_v4_kernel(IndexView ix, Ste
       }
     }
   }
+  S4_MARK(7);
   if (!ok && t == 0) { tailp[0] = -INFINITY; tailp[1] = 0.f; tailp[2] = -INFINITY; tailp[3] = 0.f; }
   // ---- the last CTA of the unit builds the unions ----
   __threadfence();
@@ -558,7 +570,9 @@ __global__ void __launch_bounds__(S4_THREADS) select_v4_kernel(IndexView ix, Ste
   if (!sm.last) return;
   __threadfence();
   if (t == 0) sv.sel_done[u] = 0;
+  S4_MARK(9);
   s4_union<PT>(ix, sv, u, m, sm);
+  S4_MARK(10);
 }
 
 size_t select_v4_smem() { return sizeof(Sel4Smem); }

@@ -5,6 +5,7 @@
 #include "decode_v2.cu"
 #include "decode_v3.cu"
 #include "select_v4.cu"
+#include "select_v5.cu"
 #include "cache.cu"
 #include "metrics.cu"
 #include "abi.cu"

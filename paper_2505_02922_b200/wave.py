@@ -98,7 +98,7 @@ class WaveLayer:
         k_upd = math.ceil(ic.update_segment / ic.centroid_ratio)
         m_pref = sum(math.ceil(min(ic.segment_size, n_idx - s) / ic.centroid_ratio)
                      for s in range(0, n_idx, ic.segment_size))
-        self.m_cap = max(1, m_pref + n_upd * k_upd)
+        self.m_cap = max(4, -(-(m_pref + n_upd * k_upd) // 4) * 4)  # multiple of 4 (float4 scans)
         self.s_cap = max(1, n_idx + n_upd * ic.update_segment)
         self.t_cap = ic.sink_tokens + ic.update_segment + ic.local_window + max(0, ic.local_window) + 8
         self.t_cap = max(self.t_cap, min(max_prefill, ic.sink_tokens + ic.local_window) + 8)

@@ -12,13 +12,15 @@ kv = torch.randn((4, 2, U, D), device=dev).bfloat16().float()
 for i in range(3):
     lay.launch_step(q[i], kv[i, 0], kv[i, 1])
 torch.cuda.synchronize()
+L0 = _lib.lib(); z = np.zeros((4096,16), np.int64); L0.wk_debug_select_timing(z.ctypes.data_as(ctypes.c_void_p), 0)
+lay.launch_step(q[3], kv[3, 0], kv[3, 1]); torch.cuda.synchronize()
 L = _lib.lib()
 out = np.zeros((4096, 16), np.int64)
 L.wk_debug_select_timing(out.ctypes.data_as(ctypes.c_void_p), 4096)
 o = out[:U * G].astype(np.float64)
 t0 = o[:, 0].min()
 print("phase end times relative to first CTA start (us): median / max over CTAs")
-names = ['start','keys+norms','radix x2','classify','band exact','sort','clumps','mark R+E','(tail)','last-CTA','union']
+names = ['start','passA','passB','passC+tau','passD','exact','order','marks','-','last-CTA','union']
 for i in range(11):
     col = o[:, i]
     v = col[col > 0]
@@ -26,3 +28,4 @@ for i in range(11):
 d = o[:, 1:9] - o[:, 0:8]
 print("per-phase durations median (us):", np.round(np.median(d, axis=0) / 1e3, 1))
 print("band sizes r/e: median", np.median(o[:, 12]), np.median(o[:, 13]), "max", o[:, 12].max(), o[:, 13].max())
+print("bucket lists n1/n2 median", np.median(o[:,14]), np.median(o[:,15]), "max", o[:,14].max(), o[:,15].max())
