@@ -226,10 +226,11 @@ int wk_score_topk(const wk_index_view* ix, const wk_step_view* sv, const wk_zone
   p.inv_sqrt_d = (float)(1.0 / sqrt((double)zp->d));
   p.need_tail = zp->tail_denominator_only;
   p.need_allc = zp->denominator_eq2;
+  p.score_fp64 = v2 ? 1 : 0;
   if (v2) {
     const double r_max = floor(zp->retrieval_fraction * (double)m_max + 0.5) + 1;
-    if (r_max <= 384 && (zp->d % 32) == 0)
-      select_v5_kernel<<<U * zp->G, 256, 0, s>>>(*ix, *sv, p);
+    if (r_max <= 384 && (zp->d % 32) == 0 && m_max <= 16384)
+      select_v5_kernel<<<U * zp->G, 256, (size_t)((m_max + 7) & ~7) * 2, s>>>(*ix, *sv, p);
     else
       select_v3_kernel<<<U * zp->G, 256, sel_smem_bytes(m_max, sv->r_cap), s>>>(*ix, *sv, p, m_max, sv->r_cap);
     WK_CHECK_LAUNCH();

@@ -236,6 +236,17 @@ WK_DEVINL float einsum_row(const float* x, const float* y, int d) {
   return __fadd_rn(__fadd_rn(acc[0], acc[1]), __fadd_rn(acc[2], acc[3]));
 }
 
+// Rigorous bound on |s' - s| for every centroid row: s' = the scoring kernel's
+// score, s = the reference's fp64 dgemv.  fp64-accumulated scores (score_v3):
+// C32 rounding + fp32 store = 2^-23 |q||C|; fp32-accumulated scores (v1):
+// additionally gamma_d = d 2^-24 / (1 - d 2^-24).  1.25x margin covers the fp32
+// evaluation of |q| and max|C|.
+WK_DEVINL double score_error_bound(double qnorm2, double cmax, int d, bool fp64_scores) {
+  const double uu = 5.9604644775390625e-08;  // 2^-24
+  const double gam = fp64_scores ? 0.0 : (double)d * uu / (1.0 - (double)d * uu);
+  return 1.25 * (gam + 2.0 * uu + 1e-13) * sqrt(qnorm2) * cmax;
+}
+
 WK_DEVINL float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -233,8 +233,7 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(IndexView ix, StepV
   float cmax = block_reduce(cm, true, sm);
   const double uu = 5.9604644775390625e-08;  // 2^-24
   const double gam = (double)d * uu / (1.0 - (double)d * uu);
-  const double B = 2.0 * (gam + uu + 1e-13) * (1.0 + 1e-5) * sqrt((double)qn2) * (1.0 + 1e-5) *
-                   (double)cmax * (1.0 + 1e-5);
+  const double B = score_error_bound((double)qn2, (double)cmax, d, p.score_fp64 != 0);
   const double B2 = 2.0 * B;
   // ---- thresholds -------------------------------------------------------------
   const float tau_r = u2f_ord(radix_kth_largest(s, m, r, sm));

@@ -14,6 +14,7 @@ struct SelParams {
   double retrieval_fraction, estimation_fraction;
   float inv_sqrt_d;
   int need_tail, need_allc;
+  int score_fp64;  // scores came from the fp64-accumulating kernel (score_v3)
 };
 
 struct AttnParams {

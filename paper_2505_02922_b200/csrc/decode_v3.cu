@@ -331,8 +331,7 @@ __global__ void __launch_bounds__(S2_THREADS) select_v3_kernel(IndexView ix, Ste
     const float cmax = s2_block_reduce(cm, true, sm);
     const double uu = 5.9604644775390625e-08;
     const double gam = (double)d * uu / (1.0 - (double)d * uu);
-    const double B = 2.0 * (gam + uu + 1e-13) * (1.0 + 1e-5) * sqrt((double)qn2) * (1.0 + 1e-5) *
-                     (double)cmax * (1.0 + 1e-5);
+    const double B = score_error_bound((double)qn2, (double)cmax, d, p.score_fp64 != 0);
     const double B2 = 2.0 * B;
     SEL_MARK(1);
     const unsigned* kp = cached ? sm.keys : nullptr;
@@ -853,6 +852,22 @@ WK_INST_ATT3(float, 4, 8)
 // score_v3: grid = (nblk, U), block = 128 (4 warps); each warp streams a
 // contiguous row range through a 4-stage bulk-copy ring.
 // ===========================================================================
+// fp64 twin of transpose_reduce32
+__device__ __forceinline__ double transpose_reduce32d(double (&v)[32]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    const bool up = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < off; i++) {
+      const double send = up ? v[i] : v[i + off];
+      const double keep = up ? v[i + off] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  return v[0];
+}
+
 template <int HS, int DL>
 struct ScoreV3Cfg {
   static constexpr int RG = 32 / HS;
@@ -913,20 +928,24 @@ __global__ void __launch_bounds__(128) score_v3_kernel(IndexView ix, StepView sv
     const unsigned char* stage = ring + sti * SB;
     const int row0 = wr0 + gi * RG;
     const int nv = min(RG, wr1 - row0);
-    float v[32];
+    // fp64 accumulation: fp32 x fp32 products are exact in fp64, so the only
+    // error left vs the reference's fp64 dgemv is the rounding of C64 to C32
+    // and of the final store (2^-23 |q||C|): the exact-selection band shrinks
+    // ~100x compared with an fp32 dot.
+    double v[32];
 #pragma unroll
     for (int j = 0; j < RG; j++) {
       float c[DL];
       RowLoad<float, DL>::cvt(*reinterpret_cast<const typename RowLoad<float, DL>::R*>(stage + j * ROW + lane * DL * 4), c);
 #pragma unroll
       for (int h = 0; h < HS; h++) {
-        float a = 0.f;
+        double a = (double)c[0] * (double)qv[h][0];
 #pragma unroll
-        for (int k = 0; k < DL; k++) a = fmaf(c[k], qv[h][k], a);
-        v[j * HS + h] = j < nv ? a : 0.f;
+        for (int k = 1; k < DL; k++) a = fma((double)c[k], (double)qv[h][k], a);
+        v[j * HS + h] = j < nv ? a : 0.0;
       }
     }
-    const float tot = transpose_reduce32(v);
+    const float tot = (float)transpose_reduce32d(v);
     const int jr = lane / HS, h = lane % HS;
     if (jr < nv && h < G) out[(size_t)h * ix.m_cap + row0 + jr] = tot;
     __syncwarp();

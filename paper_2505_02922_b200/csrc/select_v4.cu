@@ -389,8 +389,7 @@ __global__ void __launch_bounds__(S4_THREADS) select_v4_kernel(IndexView ix, Ste
     const float smax = s4_reduce(mx, true, sm);
     const double uu = 5.9604644775390625e-08;
     const double gam = (double)d * uu / (1.0 - (double)d * uu);
-    const double B = 2.0 * (gam + uu + 1e-13) * (1.0 + 1e-5) * sqrt((double)qn2) * (1.0 + 1e-5) *
-                     (double)cmax * (1.0 + 1e-5);
+    const double B = score_error_bound((double)qn2, (double)cmax, d, p.score_fp64 != 0);
     const double B2 = 2.0 * B;
     S4_MARK(1);
     float tau_r = 0.f, tau_e = 0.f;

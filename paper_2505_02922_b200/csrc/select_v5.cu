@@ -220,6 +220,8 @@ __device__ void s5_union(const IndexView& ix, const StepView& sv, int u, int m, 
 
 __global__ void __launch_bounds__(S5_T, 4) select_v5_kernel(IndexView ix, StepView sv, SelParams p) {
   __shared__ Sel5Smem sm;
+  extern __shared__ unsigned short bid16[];  // [m] bucket id of every cluster score
+  __shared__ unsigned int rbits[512];         // retrieval set of this head (m <= 16384)
   S5_MARK(0);
   const int G = p.G, d = p.d;
   const int u = blockIdx.x / G, g = blockIdx.x % G;
@@ -242,6 +244,11 @@ __global__ void __launch_bounds__(S5_T, 4) select_v5_kernel(IndexView ix, StepVi
   uint32_t* zm = sv.zmask + (size_t)u * ix.m_cap;
   const double* C64 = ix.C64 + (size_t)u * ix.m_cap * d;
   bool ok = m > 0 && r <= sv.r_cap;
+  float bk_mn = 0.f, bk_scale = 0.f;  // bucket map: floor((v - mn) * scale), clamped
+  auto bucket = [&](float v) {
+    int b = (int)((v - bk_mn) * bk_scale);
+    return b < 0 ? 0 : (b >= S5_NB ? S5_NB - 1 : b);
+  };
   if (m > 0 && !ok) set_status(sv.status, kErrBandOverflow);
   if (ok) {
     // ---- pass A: min / max of scores, max centroid norm (float4 loads) ----
@@ -266,23 +273,26 @@ __global__ void __launch_bounds__(S5_T, 4) select_v5_kernel(IndexView ix, StepVi
     mx = s5_reduce(mx, true, sm);
     const double uu = 5.9604644775390625e-08;
     const double gam = (double)d * uu / (1.0 - (double)d * uu);
-    const double B = 2.0 * (gam + uu + 1e-13) * (1.0 + 1e-5) * sqrt((double)qn2) * (1.0 + 1e-5) *
-                     (double)cmax * (1.0 + 1e-5);
+    const double B = score_error_bound((double)qn2, (double)cmax, d, p.score_fp64 != 0);
     const double B2 = 2.0 * B;
     const float span = mx - mn;
-    const float scale = span > 0.f ? (float)S5_NB / span : 0.f;
-    auto bucket = [&](float v) {
-      int b = (int)((v - mn) * scale);
-      return b < 0 ? 0 : (b >= S5_NB ? S5_NB - 1 : b);
-    };
+    bk_mn = mn;
+    bk_scale = span > 0.f ? (float)S5_NB / span : 0.f;
     S5_MARK(1);
-    // ---- pass B: histogram ----
+    // ---- pass B: bucket id of every score (one batched read), histogram ----
     for (int i = t; i < m4; i += T) {
       const float4 v = __ldcg(reinterpret_cast<const float4*>(s) + i);
-      atomicAdd(&sm.hist[bucket(v.x)], 1); atomicAdd(&sm.hist[bucket(v.y)], 1);
-      atomicAdd(&sm.hist[bucket(v.z)], 1); atomicAdd(&sm.hist[bucket(v.w)], 1);
+      const int k0 = bucket(v.x), k1 = bucket(v.y), k2 = bucket(v.z), k3 = bucket(v.w);
+      bid16[4 * i] = (unsigned short)k0; bid16[4 * i + 1] = (unsigned short)k1;
+      bid16[4 * i + 2] = (unsigned short)k2; bid16[4 * i + 3] = (unsigned short)k3;
+      atomicAdd(&sm.hist[k0], 1); atomicAdd(&sm.hist[k1], 1); atomicAdd(&sm.hist[k2], 1); atomicAdd(&sm.hist[k3], 1);
     }
-    for (int i = 4 * m4 + t; i < m; i += T) atomicAdd(&sm.hist[bucket(s[i])], 1);
+    for (int i = 4 * m4 + t; i < m; i += T) {
+      const int k = bucket(s[i]);
+      bid16[i] = (unsigned short)k;
+      atomicAdd(&sm.hist[k], 1);
+    }
+    for (int w = t; w < (m + 31) / 32; w += T) rbits[w] = 0u;
     __syncthreads();
     // buckets holding rank K1 = r and K2 = r + e (descending): thread t owns
     // buckets 511-2t and 510-2t
@@ -321,10 +331,11 @@ __global__ void __launch_bounds__(S5_T, 4) select_v5_kernel(IndexView ix, StepVi
       const int b1 = sm.b1, b2 = e > 0 ? sm.b2 : -1;
       for (int base = 0; base < m; base += T) {
         const int c = base + t;
-        const float v = c < m ? __ldcg(s + c) : 0.f;
-        const int bk = c < m ? bucket(v) : -1;
-        s5_append(bk == b1, s5_key(v, c), sm.l1, &sm.n1, S5_LIST, &sm.ovf);
-        s5_append(bk == b2, s5_key(v, c), sm.l2, &sm.n2, S5_LIST, &sm.ovf);
+        const int bk = c < m ? (int)bid16[c] : -1;
+        const bool f1 = bk == b1, f2 = bk == b2;
+        const float v = (f1 || f2) ? __ldcg(s + c) : 0.f;
+        s5_append(f1, s5_key(v, c), sm.l1, &sm.n1, S5_LIST, &sm.ovf);
+        s5_append(f2, s5_key(v, c), sm.l2, &sm.n2, S5_LIST, &sm.ovf);
       }
     }
     __syncthreads();
@@ -360,25 +371,33 @@ __global__ void __launch_bounds__(S5_T, 4) select_v5_kernel(IndexView ix, StepVi
     const float cmax = s5_reduce(cm, true, sm);
     const double uu = 5.9604644775390625e-08;
     const double gam = (double)d * uu / (1.0 - (double)d * uu);
-    const double B = 2.0 * (gam + uu + 1e-13) * (1.0 + 1e-5) * sqrt((double)qn2) * (1.0 + 1e-5) *
-                     (double)cmax * (1.0 + 1e-5);
+    const double B = score_error_bound((double)qn2, (double)cmax, d, p.score_fp64 != 0);
     const double B2 = 2.0 * B;
     const double hr = (double)tau_r + B2, lr = (double)tau_r - B2, he = (double)tau_e + B2, le = (double)tau_e - B2;
     S5_MARK(3);
-    // ---- pass D: candidates (certain-in + band around tau_r), band around tau_e
+    // ---- pass D: candidates (certain-in + band around tau_r), band around
+    //      tau_e.  bucket() is monotone, so bucket(s) > bucket(hi) => s > hi and
+    //      bucket(s) < bucket(lo) => s < lo; only ids in [bucket(lo),
+    //      bucket(hi)] need their score.
+    const int khr = bucket(__double2float_ru(hr)), klr = bucket(__double2float_rd(lr));
+    const int khe = bucket(__double2float_ru(he)), kle = bucket(__double2float_rd(le));
     int my_in_e = 0;
     for (int base = 0; base < m; base += T) {
       const int c = base + t;
       const bool act = c < m;
-      const float v = act ? __ldcg(s + c) : -INFINITY;
+      const int k = act ? (int)bid16[c] : -1;
+      const bool need_v = act && ((k >= klr && k <= khr) || (e > 0 && k >= kle && k <= khe));
+      const bool cand_r = act && k >= klr;  // certain-in or band (subject to exact compare)
+      float v = 0.f;
+      if (need_v || cand_r) v = __ldcg(s + c);
       const double dv = (double)v;
-      const bool in_r = act && dv > hr;
-      const bool bd_r = act && !in_r && dv >= lr;
+      const bool in_r = act && (k > khr || (k >= klr && dv > hr));
+      const bool bd_r = act && !in_r && k >= klr && dv >= lr;
       s5_append(in_r || bd_r, s5_key(v, c), sm.cand, &sm.ncand, S5_CAND, &sm.ovf);
       if (bd_r) atomicAdd(&sm.nband_r, 1);
       if (e > 0) {
-        const bool in_e = act && dv > he;
-        const bool bd_e = act && !in_e && dv >= le;
+        const bool in_e = act && (k > khe || (k >= kle && dv > he));
+        const bool bd_e = act && !in_e && k >= kle && k <= khe && dv >= le;
         my_in_e += in_e ? 1 : 0;
         const unsigned mk = __ballot_sync(0xffffffffu, bd_e);
         if (mk) {
@@ -486,16 +505,18 @@ __global__ void __launch_bounds__(S5_T, 4) select_v5_kernel(IndexView ix, StepVi
         const int c = s5_id(sm.cs[i]);
         rl_out[i] = c;
         atomicOr(zm + c, 1u << g);
+        atomicOr(rbits + (c >> 5), 1u << (c & 31));
       }
-      __threadfence_block();
       __syncthreads();
       int32_t* el_out = sv.elist ? sv.elist + ((size_t)u * G + g) * sv.e_cap : nullptr;
       if (e > 0) {
-        // E = top(r+e) minus R: R membership read back from the zone bits
+        // E = top(r+e) minus R (certain part from bucket ids; the band part below)
         for (int base = 0; base < m; base += T) {
           const int c = base + t;
-          const bool in_e = c < m && (double)__ldcg(s + c) > he;
-          const bool f = in_e && !(__ldcg(zm + c) & (1u << g));
+          const int k = c < m ? (int)bid16[c] : -1;
+          bool in_e = c < m && k > khe;
+          if (c < m && !in_e && k >= kle && k <= khe) in_e = (double)__ldcg(s + c) > he;
+          const bool f = in_e && !((rbits[c >> 5] >> (c & 31)) & 1u);
           if (f) atomicOr(zm + c, 1u << (8 + g));
           if (el_out) {
             const unsigned mk = __ballot_sync(0xffffffffu, f);
@@ -509,7 +530,7 @@ __global__ void __launch_bounds__(S5_T, 4) select_v5_kernel(IndexView ix, StepVi
         }
         for (int i = t; i < nbe; i += T) {
           const int c = sm.be_id[i];
-          if (sm.be_sel[i] && !(__ldcg(zm + c) & (1u << g))) {
+          if (sm.be_sel[i] && !((rbits[c >> 5] >> (c & 31)) & 1u)) {
             atomicOr(zm + c, 1u << (8 + g));
             if (el_out) el_out[atomicAdd(&sm.n_el, 1)] = c;
           }
