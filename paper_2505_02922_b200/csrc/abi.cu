@@ -83,6 +83,7 @@ static int configure_smem() {
   if (cudaFuncSetAttribute(attend_kernel<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, at) != cudaSuccess) return WK_ECUDA;
   if (cudaFuncSetAttribute(attend_kernel<__nv_bfloat16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, at) != cudaSuccess) return WK_ECUDA;
   if (cudaFuncSetAttribute(select_v3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess) return WK_ECUDA;
+  if (cudaFuncSetAttribute(select_v5_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024) != cudaSuccess) return WK_ECUDA;
   if (cudaFuncSetAttribute(select_v4_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)select_v4_smem()) != cudaSuccess) return WK_ECUDA;
   if (cudaFuncSetAttribute(select_v4_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)select_v4_smem()) != cudaSuccess) return WK_ECUDA;
   const int rs = (int)recall_smem_bytes();
