@@ -41,6 +41,9 @@ typedef struct wk_index_view {
   float* VS32;        /* [U, m_cap, d] fp32 value sums                         */
   double* VS64;       /* [U, m_cap, d] fp64 value sums (optional, may be NULL) */
   int64_t s_cap, m_cap;
+  float* Cmax;        /* [U] max_c ||C32_c|| (score error bound), set at build */
+  void* C16;          /* [U, m_cap, d] fp16 centroids / Cscale (scoring scan)   */
+  float* Cscale;      /* [U, m_cap] power-of-two row scale of C16               */
 } wk_index_view;
 
 /* One clustering segment: a contiguous token range of one unit
@@ -107,6 +110,11 @@ typedef struct wk_step_view {
   int32_t rt_cap, pad_;
   float* eu_x;        /* [U, eu_cap, G] estimation-row scores (-inf: head not in zone) */
   float* eu_sz;       /* [U, eu_cap] estimation-row cluster sizes                */
+  uint32_t* rbits;    /* [U, G, w_cap] retrieval set of each head (bitmap)      */
+  uint32_t* ebits;    /* [U, G, w_cap] estimation set of each head (bitmap)     */
+  int32_t* pieces;    /* [U, pc_cap, 2] retrieval runs: (store row, n | mask<<8) */
+  int32_t* woff;      /* [U + 1] attention chunk prefix (scratch)               */
+  int32_t w_cap, pc_cap;
 } wk_step_view;
 
 typedef struct wk_zone_params {
@@ -115,6 +123,9 @@ typedef struct wk_zone_params {
   double estimation_fraction; /* IndexConfig.estimation_fraction (config.py:27) */
   int32_t tail_denominator_only; /* IndexConfig.tail_mode                      */
   int32_t denominator_eq2;       /* EngineConfig.denominator_mode              */
+  int32_t score_mode;            /* 0 fp32 C32 scan, 1 fp64-accumulated C32,
+                                    2 fp16 C16 on tensor cores                 */
+  int32_t pad_;
 } wk_zone_params;
 
 /* Device block cache (the wave buffer), one state machine per cache unit

@@ -23,7 +23,8 @@ _I64 = ctypes.c_int64
 class IndexViewC(ctypes.Structure):
     _fields_ = [("store_k", _P), ("store_v", _P), ("store_tok", _P), ("cl_off", _P),
                 ("cl_size", _P), ("C64", _P), ("C32", _P), ("Cnorm", _P), ("VS32", _P),
-                ("VS64", _P), ("s_cap", _I64), ("m_cap", _I64)]
+                ("VS64", _P), ("s_cap", _I64), ("m_cap", _I64), ("Cmax", _P), ("C16", _P),
+                ("Cscale", _P)]
 
 
 class SegmentC(ctypes.Structure):
@@ -48,7 +49,8 @@ class StepViewC(ctypes.Structure):
                 ("out", _P), ("logden", _P), ("cov", _P), ("status", _P), ("r_cap", _I32),
                 ("e_cap", _I32), ("ru_cap", _I32), ("eu_cap", _I32), ("rtok_row", _P),
                 ("rtok_mask", _P), ("sel_done", _P), ("rt_cap", _I32), ("pad_", _I32),
-                ("eu_x", _P), ("eu_sz", _P)]
+                ("eu_x", _P), ("eu_sz", _P), ("rbits", _P), ("ebits", _P), ("pieces", _P),
+                ("woff", _P), ("w_cap", _I32), ("pc_cap", _I32)]
 
 
 class CacheViewC(ctypes.Structure):
@@ -64,7 +66,8 @@ class CacheViewC(ctypes.Structure):
 class ZoneParamsC(ctypes.Structure):
     _fields_ = [("G", _I32), ("d", _I32), ("blas_threads", _I32),
                 ("retrieval_fraction", ctypes.c_double), ("estimation_fraction", ctypes.c_double),
-                ("tail_denominator_only", _I32), ("denominator_eq2", _I32)]
+                ("tail_denominator_only", _I32), ("denominator_eq2", _I32), ("score_mode", _I32),
+                ("pad_", _I32)]
 
 
 _lib = None

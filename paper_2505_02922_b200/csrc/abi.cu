@@ -49,6 +49,19 @@ size_t score_v3_smem();
 template <typename T, int DL, int HS, bool FULL>
 __global__ void attend_v2_kernel(IndexView, SteadyView, StepView, AttnParams, const int32_t*);
 size_t attend_v2_smem_bytes(int d, int HS);
+// select_v6.cu / attend_v4.cu / score_v4.cu
+template <int CAND, bool SMS>
+__global__ void select_v6_kernel(IndexView, StepView, SelParams);
+size_t select_v6_dyn_smem(int m_max, bool sms, int cand);
+template <typename T, int DPL, int HS, bool FULL>
+__global__ void attend_v4_kernel(IndexView, SteadyView, StepView, AttnParams, const int32_t*, int);
+template <typename T, int DPL, int HS, bool FULL>
+size_t attend_v4_smem();
+template <bool FULL, int DL>
+__global__ void att4_merge_kernel(SteadyView, StepView, AttnParams, const int32_t*, int, int, int);
+__global__ void km_pack16_kernel(const SegDesc*, IndexView, int);
+template <int KS, int NT>
+__global__ void score_v4_kernel(IndexView, StepView, int, int);
 // metrics.cu
 template <typename T>
 __global__ void recall_kernel(IndexView, SteadyView, StepView, const int32_t*, int, int, int, int, float*,
@@ -147,9 +160,86 @@ static int dispatch_attend_v2(const IndexView& ix, const SteadyView& st, const S
   }
 }
 
+// ---- v6 pipeline: score_v4 (tensor cores) | score_v3, select_v6, attend_v4 ----
+static int g_sel_prof = 0;
+extern "C" int wk_debug_select_prof(int on) { g_sel_prof = on; return 0; }
+static bool v6_ok(const wk_index_view* ix, const wk_step_view* sv, int d) {
+  return (d == 64 || d == 128) && sv->rbits && sv->ebits && sv->pieces && sv->woff && sv->sel_done && ix->Cmax;
+}
+
+template <int KS, int NT>
+static int launch_score_v4(const IndexView& ix, const StepView& sv, int G, int U, int m_max, cudaStream_t s) {
+  const int ntile = (m_max + 15) / 16;
+  // ~8 CTAs of 4 warps per SM-wave over all units
+  long long want = ((long long)ntile * U + 148 * 8 - 1) / (148 * 8);
+  int tpc = (int)((want + 3) / 4) * 4;
+  if (tpc < 8) tpc = 8;
+  dim3 g((ntile + tpc - 1) / tpc, U);
+  score_v4_kernel<KS, NT><<<g, 128, 0, s>>>(ix, sv, G, tpc);
+  return cudaGetLastError() == cudaSuccess ? 0 : WK_ECUDA;
+}
+
+static int launch_select_v6(const IndexView& ix, const StepView& sv, const SelParams& p, int U, int m_max,
+                            cudaStream_t s) {
+  const double r_max = floor(p.retrieval_fraction * (double)m_max + 0.5) + 1;
+  const int blocks = U * p.G;
+  static int cfg = 0;
+  if (!cfg) {
+    if (cudaFuncSetAttribute(select_v6_kernel<512, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)select_v6_dyn_smem(16384, true, 512)) != cudaSuccess ||
+        cudaFuncSetAttribute(select_v6_kernel<512, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)select_v6_dyn_smem(262144, false, 512)) != cudaSuccess ||
+        cudaFuncSetAttribute(select_v6_kernel<2048, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)select_v6_dyn_smem(262144, false, 2048)) != cudaSuccess)
+      return WK_ECUDA;
+    cfg = 1;
+  }
+  if (m_max > 262144) return WK_ECONFIG;
+  if (m_max <= 16384 && r_max <= 480)
+    select_v6_kernel<512, true><<<blocks, 256, select_v6_dyn_smem(m_max, true, 512), s>>>(ix, sv, p);
+  else if (r_max <= 480)
+    select_v6_kernel<512, false><<<blocks, 256, select_v6_dyn_smem(m_max, false, 512), s>>>(ix, sv, p);
+  else if (r_max <= 1900)
+    select_v6_kernel<2048, false><<<blocks, 256, select_v6_dyn_smem(m_max, false, 2048), s>>>(ix, sv, p);
+  else
+    return WK_ECONFIG;
+  return cudaGetLastError() == cudaSuccess ? 0 : WK_ECUDA;
+}
+
+template <typename T, int DPL, int HS, bool FULL>
+static int launch_attend_v4(const IndexView& ix, const SteadyView& st, const StepView& sv, const AttnParams& p,
+                            const int32_t* n_store, int U, int P, cudaStream_t s) {
+  if (U > 1024) return WK_ECONFIG;
+  const size_t sm = attend_v4_smem<T, DPL, HS, FULL>();
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(attend_v4_kernel<T, DPL, HS, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sm) != cudaSuccess)
+      return WK_ECUDA;
+    configured = true;
+  }
+  attend_v4_kernel<T, DPL, HS, FULL><<<P, 256, sm, s>>>(ix, st, sv, p, n_store, U);
+  if (cudaGetLastError() != cudaSuccess) return WK_ECUDA;
+  const int RG = 32 / HS;
+  att4_merge_kernel<FULL, DPL / 2><<<(U * p.G + 3) / 4, 128, 0, s>>>(st, sv, p, n_store, U, P * 8, RG);
+  return cudaGetLastError() == cudaSuccess ? 0 : WK_ECUDA;
+}
+
+template <typename T, bool FULL>
+static int dispatch_attend_v4(const IndexView& ix, const SteadyView& st, const StepView& sv, const AttnParams& p,
+                              const int32_t* n_store, int U, int P, cudaStream_t s) {
+  const int hs = head_slots(p.G);
+  if (p.d == 128) {
+    return hs == 4 ? launch_attend_v4<T, 8, 4, FULL>(ix, st, sv, p, n_store, U, P, s)
+                   : launch_attend_v4<T, 8, 8, FULL>(ix, st, sv, p, n_store, U, P, s);
+  }
+  return hs == 4 ? launch_attend_v4<T, 4, 4, FULL>(ix, st, sv, p, n_store, U, P, s)
+                 : launch_attend_v4<T, 4, 8, FULL>(ix, st, sv, p, n_store, U, P, s);
+}
+
 extern "C" {
 
-int wk_version(void) { return 2; }
+int wk_version(void) { return 3; }
 
 int wk_kmeans_segments(const wk_index_view* ix, const wk_segment* segs, int n_segs,
                        const wk_build_scratch* scr, int d, int store_bf16, int kmeans_iters,
@@ -185,6 +275,10 @@ int wk_kmeans_segments(const wk_index_view* ix, const wk_segment* segs, int n_se
   else
     km_finalize_kernel<float><<<n_segs, 256, usmem, s>>>(sd, scr->A, scr->perm, *ix, d, scr->status);
   WK_CHECK_LAUNCH();
+  if (ix->C16 && ix->Cscale && ix->Cmax && (d % 16) == 0 && d <= 128 && (ix->m_cap % 16) == 0) {
+    km_pack16_kernel<<<n_segs, 256, 0, s>>>(sd, *ix, d);
+    WK_CHECK_LAUNCH();
+  }
   return 0;
 }
 
@@ -204,6 +298,38 @@ int wk_score_topk(const wk_index_view* ix, const wk_step_view* sv, const wk_zone
     return WK_ECONFIG;
   if (configure_smem()) return WK_ECUDA;
   cudaStream_t s = (cudaStream_t)stream;
+  if (v6_ok(ix, sv, zp->d)) {
+    const bool tc = zp->score_mode == 2 && ix->C16 && ix->Cscale;
+    int rc = 0;
+    if (m_max > 0) {
+      const int nt = zp->G <= 4 ? 1 : 2;
+      if (tc) {
+        if (zp->d == 128) rc = nt == 1 ? launch_score_v4<8, 1>(*ix, *sv, zp->G, U, m_max, s)
+                                       : launch_score_v4<8, 2>(*ix, *sv, zp->G, U, m_max, s);
+        else rc = nt == 1 ? launch_score_v4<4, 1>(*ix, *sv, zp->G, U, m_max, s)
+                          : launch_score_v4<4, 2>(*ix, *sv, zp->G, U, m_max, s);
+      } else {
+        const int hs = head_slots(zp->G);
+        if (zp->d == 128) rc = hs == 4 ? launch_score_v3<4, 4>(*ix, *sv, zp->G, U, m_max, s)
+                                       : launch_score_v3<8, 4>(*ix, *sv, zp->G, U, m_max, s);
+        else rc = hs == 4 ? launch_score_v3<4, 2>(*ix, *sv, zp->G, U, m_max, s)
+                          : launch_score_v3<8, 2>(*ix, *sv, zp->G, U, m_max, s);
+      }
+      if (rc) return rc;
+    }
+    SelParams p;
+    p.G = zp->G; p.d = zp->d; p.blas_threads = zp->blas_threads;
+    p.retrieval_fraction = zp->retrieval_fraction;
+    p.estimation_fraction = zp->estimation_fraction;
+    p.inv_sqrt_d = (float)(1.0 / sqrt((double)zp->d));
+    p.need_tail = zp->tail_denominator_only;
+    p.need_allc = zp->denominator_eq2;
+    p.score_fp64 = 1;
+    p.score_mode = tc ? 2 : 1;
+    p.piece_rows = 32 / head_slots(zp->G);
+    p.prof = g_sel_prof;
+    return launch_select_v6(*ix, *sv, p, U, m_max, s);
+  }
   const bool v2 = v2_ok(zp->d) && sv->rtok_row && sv->sel_done;
   if (m_max > 0) {
     if (v2) {
@@ -256,6 +382,9 @@ int wk_tripartite_attn(const wk_index_view* ix, const wk_steady_view* st, const 
   p.tail_denominator_only = zp->tail_denominator_only;
   p.denominator_eq2 = zp->denominator_eq2;
   dim3 grid(S, U);
+  if (v6_ok(ix, sv, zp->d))
+    return store_bf16 ? dispatch_attend_v4<__nv_bfloat16, false>(*ix, *st, *sv, p, nullptr, U, S, s)
+                      : dispatch_attend_v4<float, false>(*ix, *st, *sv, p, nullptr, U, S, s);
   if (v2_ok(zp->d) && sv->rtok_row && sv->sel_done) {
     const int rc = store_bf16 ? dispatch_attend_v2<__nv_bfloat16, false>(*ix, *st, *sv, p, nullptr, U, S, s)
                               : dispatch_attend_v2<float, false>(*ix, *st, *sv, p, nullptr, U, S, s);
@@ -284,6 +413,9 @@ int wk_full_attn(const wk_index_view* ix, const wk_steady_view* st, const wk_ste
   p.tail_denominator_only = 0;
   p.denominator_eq2 = 0;
   dim3 grid(S, U);
+  if (v6_ok(ix, sv, d))
+    return store_bf16 ? dispatch_attend_v4<__nv_bfloat16, true>(*ix, *st, v, p, n_store, U, S, s)
+                      : dispatch_attend_v4<float, true>(*ix, *st, v, p, n_store, U, S, s);
   if (v2_ok(d)) {
     const int rc = store_bf16 ? dispatch_attend_v2<__nv_bfloat16, true>(*ix, *st, v, p, n_store, U, S, s)
                               : dispatch_attend_v2<float, true>(*ix, *st, v, p, n_store, U, S, s);

@@ -1,0 +1,579 @@
+// attend_v4.cu -- fused tripartite decode attention (attention.py:67-148,
+// engine.py:150-172), persistent flat schedule.
+//
+// Work is a flat list of CHUNKS over all units: per unit u, first the steady
+// zone (sinks + decode buffer, engine.py:87-96) in runs of RG contiguous rows,
+// then the retrieval pieces built by select_v6 (runs of <= RG contiguous store
+// rows of one cluster; the store is cluster-contiguous, store.py:51-54), then
+// the estimation rows (fp32 value sums of the union estimation clusters) RG at
+// a time.  A persistent grid of P CTAs x 8 warps splits the list evenly; each
+// warp streams its contiguous chunk range through a private ring of NST
+// shared-memory stages filled by 1-D bulk copies (cp.async.bulk / TMA): a
+// chunk is 2 copies (K run, V run) plus zero-row tail copies, so the HBM reads
+// are whole contiguous runs.  The warp flushes an online-softmax partial
+// (max, denominator, numerator[d] per head) to global memory whenever the
+// (unit, kind) of its chunks changes; att4_merge_kernel folds the partials of
+// each (unit, head) with the log-sum-exp merge (attention.py:115-148) and the
+// eq2 / tail modes of _final_output (engine.py:150-172).
+//
+// Inner loop (per chunk of RG = 32/HS rows): lanes 0-15 take even rows, lanes
+// 16-31 odd rows, each lane owns DPL = d/16 contiguous dims; q.k partials of
+// RG/2 rows x HS heads are reduced over the 16 lanes of a half with a
+// transposed shuffle reduction; packed FFMA2 for q.k and p.v.
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+#include "decode_internal.h"
+
+namespace wk {
+
+__device__ __align__(128) unsigned char g_zero4[8192];
+
+template <int HS>
+struct SoftState4 {
+  float M[HS], D[HS];
+};
+
+// online-softmax update for one chunk; x = the lane's logit for (row j_own,
+// head h_own), wz = its denominator weight (1 for tokens, the cluster size for
+// estimation rows).  Returns the lane's numerator weight; fills alpha[].
+template <int HS>
+WK_DEVINL float att4_softmax(float x, float wz, SoftState4<HS>& st, float (&alpha)[HS]) {
+  float mx = x;
+#pragma unroll
+  for (int off = HS; off < 32; off <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+  const int h_own = (threadIdx.x & 31) % HS;
+  float mo_own = st.M[0];
+#pragma unroll
+  for (int h = 1; h < HS; h++)
+    if (h == h_own) mo_own = st.M[h];
+  const float mnew_own = fmaxf(mo_own, mx);
+  const float pw = (x == -INFINITY) ? 0.f : __expf(x - mnew_own);
+  float ps = pw * wz;
+#pragma unroll
+  for (int off = HS; off < 32; off <<= 1) ps += __shfl_xor_sync(0xffffffffu, ps, off);
+#pragma unroll
+  for (int h = 0; h < HS; h++) {
+    const float mn = __shfl_sync(0xffffffffu, mnew_own, h);
+    const float sd = __shfl_sync(0xffffffffu, ps, h);
+    const float mo = st.M[h];
+    float a = (mo == -INFINITY) ? 0.f : __expf(mo - mn);
+    if (mn == -INFINITY) a = 1.f;
+    alpha[h] = a;
+    st.D[h] = st.D[h] * a + sd;
+    st.M[h] = mn;
+  }
+  return pw;
+}
+
+template <typename T, int DPL> struct Row4;
+template <> struct Row4<__nv_bfloat16, 8> {
+  static WK_DEVINL void ld(const unsigned char* p, float2 (&o)[4]) {
+    const uint4 r = *reinterpret_cast<const uint4*>(p);
+    o[0] = make_float2(__uint_as_float(r.x << 16), __uint_as_float(r.x & 0xffff0000u));
+    o[1] = make_float2(__uint_as_float(r.y << 16), __uint_as_float(r.y & 0xffff0000u));
+    o[2] = make_float2(__uint_as_float(r.z << 16), __uint_as_float(r.z & 0xffff0000u));
+    o[3] = make_float2(__uint_as_float(r.w << 16), __uint_as_float(r.w & 0xffff0000u));
+  }
+};
+template <> struct Row4<__nv_bfloat16, 4> {
+  static WK_DEVINL void ld(const unsigned char* p, float2 (&o)[2]) {
+    const uint2 r = *reinterpret_cast<const uint2*>(p);
+    o[0] = make_float2(__uint_as_float(r.x << 16), __uint_as_float(r.x & 0xffff0000u));
+    o[1] = make_float2(__uint_as_float(r.y << 16), __uint_as_float(r.y & 0xffff0000u));
+  }
+};
+template <> struct Row4<float, 8> {
+  static WK_DEVINL void ld(const unsigned char* p, float2 (&o)[4]) {
+    const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
+    o[0] = make_float2(a.x, a.y); o[1] = make_float2(a.z, a.w); o[2] = make_float2(b.x, b.y); o[3] = make_float2(b.z, b.w);
+  }
+};
+template <> struct Row4<float, 4> {
+  static WK_DEVINL void ld(const unsigned char* p, float2 (&o)[2]) {
+    const float4 a = *reinterpret_cast<const float4*>(p);
+    o[0] = make_float2(a.x, a.y); o[1] = make_float2(a.z, a.w);
+  }
+};
+
+// 16 values summed over the 16 lanes of each half-warp; lane keeps index lane&15
+WK_DEVINL float att4_treduce16(float (&v)[16]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int off = 8; off >= 1; off >>= 1) {
+    const bool up = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < off; i++) {
+      const float send = up ? v[i] : v[i + off];
+      const float keep = up ? v[i + off] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  return v[0];
+}
+
+template <typename T, int DPL, int HS>
+struct Att4Cfg {
+  static constexpr int RG = 32 / HS;               // rows per chunk
+  static constexpr int NST = 3;                    // ring stages per warp
+  static constexpr int D = 16 * DPL;
+  static constexpr int ROWT = D * (int)sizeof(T);  // K or V row bytes
+  static constexpr int ROWV = D * 4;               // value-sum row bytes
+  static constexpr int SB = ((2 * RG * ROWT > RG * ROWV ? 2 * RG * ROWT : RG * ROWV) + 127) / 128 * 128;
+  static constexpr int WARPS = 8;
+  static constexpr int MAXU = 1024;                // units per launch (smem chunk prefix)
+  // per warp: ring + barriers + per-stage lane meta (mask, x, w) + stage tags
+  static constexpr int META = NST * 32 * 12 + NST * 16;
+  static constexpr size_t SMEM = (size_t)WARPS * NST * SB + (size_t)WARPS * NST * 8 + (size_t)WARPS * META +
+                                 (size_t)(MAXU + 1) * 4 + 64;
+};
+
+// chunk counts of unit u
+template <int RG>
+WK_DEVINL void att4_counts(const SteadyView& st, const StepView& sv, const int32_t* n_store, bool full, int u,
+                           int& c0, int& c1, int& c2) {
+  const int n_st = st.n[u];
+  c0 = (n_st + RG - 1) / RG;
+  if (full) {
+    c1 = (n_store[u] + RG - 1) / RG;
+    c2 = 0;
+  } else {
+    c1 = sv.cnt[u * 4 + 3];
+    c2 = (sv.cnt[u * 4 + 2] + RG - 1) / RG;
+  }
+}
+
+// first warp (of W) whose balanced range [N w / W, N (w+1) / W) holds chunk c
+WK_DEVINL int att4_warp_of(long long c, long long N, long long W) { return (int)(((c + 1) * W + N - 1) / N - 1); }
+
+template <typename T, int DPL, int HS, bool FULL>
+__global__ void __launch_bounds__(256, HS == 8 ? 1 : 2) attend_v4_kernel(IndexView ix, SteadyView st, StepView sv, AttnParams p,
+                                                            const int32_t* __restrict__ n_store, int U) {
+  using CF = Att4Cfg<T, DPL, HS>;
+  constexpr int RG = CF::RG, NST = CF::NST, ROWT = CF::ROWT, ROWV = CF::ROWV, SB = CF::SB;
+  constexpr int D = CF::D, RH = RG / 2, DP2 = DPL / 2;
+  const int G = p.G;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int half = lane >> 4, sub = lane & 15;
+  extern __shared__ __align__(128) unsigned char a4s[];
+  unsigned char* ring = a4s + (size_t)warp * NST * SB;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(a4s + (size_t)CF::WARPS * NST * SB) + warp * NST;
+  unsigned char* meta = a4s + (size_t)CF::WARPS * NST * SB + (size_t)CF::WARPS * NST * 8 + (size_t)warp * CF::META;
+  int* smask = reinterpret_cast<int*>(meta);
+  float* sx = reinterpret_cast<float*>(meta + NST * 32 * 4);
+  float* sw = reinterpret_cast<float*>(meta + NST * 32 * 8);
+  int4* stag = reinterpret_cast<int4*>(meta + NST * 32 * 12);  // (unit, kind)
+  int* woff = reinterpret_cast<int*>(a4s + (size_t)CF::WARPS * NST * SB + (size_t)CF::WARPS * NST * 8 +
+                                     (size_t)CF::WARPS * CF::META);
+
+  // ---- chunk prefix over units (every CTA; U <= MAXU) ----
+  {
+    int carry = 0;
+    for (int base = 0; base < U; base += blockDim.x) {
+      const int u = base + threadIdx.x;
+      int c = 0;
+      if (u < U) {
+        int c0, c1, c2;
+        att4_counts<RG>(st, sv, n_store, FULL, u, c0, c1, c2);
+        c = c0 + c1 + c2;
+      }
+      int x = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      int* ws = woff + CF::MAXU + 1;  // 8 ints of scratch past woff (within the +64 pad)
+      if (lane == 31) ws[warp] = x;
+      __syncthreads();
+      int wbase = 0;
+      for (int w = 0; w < warp; w++) wbase += ws[w];
+      int tot = 0;
+      for (int w = 0; w < CF::WARPS; w++) tot += ws[w];
+      if (u < U) woff[u] = carry + wbase + x - c;
+      carry += tot;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) woff[U] = carry;
+    __syncthreads();
+  }
+  const long long Ntot = woff[U];
+  const long long Wtot = (long long)gridDim.x * CF::WARPS;
+  const int wg = blockIdx.x * CF::WARPS + warp;
+  if (blockIdx.x == 0 && sv.woff)
+    for (int i = threadIdx.x; i <= U; i += blockDim.x) sv.woff[i] = woff[i];
+  const long long ca = Ntot * wg / Wtot, cb = Ntot * (wg + 1) / Wtot;
+
+  if (lane == 0) {
+    for (int i = 0; i < NST; i++) mbar_init(bars + i, 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+
+  const float isd = p.inv_sqrt_d;
+  const int allmask = (1 << G) - 1;
+  const int j_own = half + 2 * (sub / HS), h_own = sub % HS;
+
+  // ---- issue cursor: (unit, kind, local chunk) of chunk ci ----
+  int iu = 0;
+  {
+    // binary search: last u with woff[u] <= ca
+    int lo = 0, hi = U - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (woff[mid] <= ca) lo = mid; else hi = mid - 1;
+    }
+    iu = lo;
+  }
+  int ic0 = 0, ic1 = 0, ic2 = 0;
+  if (ca < cb) att4_counts<RG>(st, sv, n_store, FULL, iu, ic0, ic1, ic2);
+
+  auto issue = [&](int sti, long long ci) {
+    while (ci >= woff[iu + 1]) {
+      iu++;
+      att4_counts<RG>(st, sv, n_store, FULL, iu, ic0, ic1, ic2);
+    }
+    int lc = (int)(ci - woff[iu]);
+    int kind;
+    if (lc < ic0) kind = 0;
+    else if (lc < ic0 + ic1) { kind = 1; lc -= ic0; }
+    else { kind = 2; lc -= ic0 + ic1; }
+    const int u = iu;
+    unsigned char* stage = ring + sti * SB;
+    int n = 0, mk = 0;
+    float x = -INFINITY, w = 0.f;
+    if (kind < 2) {
+      const unsigned char* srck;
+      const unsigned char* srcv;
+      if (kind == 0) {
+        const int r0 = lc * RG;
+        n = min(RG, st.n[u] - r0);
+        mk = allmask;
+        srck = (const unsigned char*)st.k + ((size_t)u * st.t_cap + r0) * ROWT;
+        srcv = (const unsigned char*)st.v + ((size_t)u * st.t_cap + r0) * ROWT;
+      } else if (FULL) {
+        const int r0 = lc * RG;
+        n = min(RG, n_store[u] - r0);
+        mk = allmask;
+        srck = (const unsigned char*)ix.store_k + ((size_t)u * ix.s_cap + r0) * ROWT;
+        srcv = (const unsigned char*)ix.store_v + ((size_t)u * ix.s_cap + r0) * ROWT;
+      } else {
+        const int2 pc = __ldcg(reinterpret_cast<const int2*>(sv.pieces) + (size_t)u * sv.pc_cap + lc);
+        n = pc.y & 0xff;
+        mk = pc.y >> 8;
+        srck = (const unsigned char*)ix.store_k + ((size_t)u * ix.s_cap + pc.x) * ROWT;
+        srcv = (const unsigned char*)ix.store_v + ((size_t)u * ix.s_cap + pc.x) * ROWT;
+      }
+      if (lane == 0) {
+        mbar_arrive_expect_tx(bars + sti, (uint32_t)(2 * RG * ROWT));
+        bulk_g2s(stage, srck, (uint32_t)(n * ROWT), bars + sti);
+        bulk_g2s(stage + RG * ROWT, srcv, (uint32_t)(n * ROWT), bars + sti);
+        if (n < RG) {
+          bulk_g2s(stage + n * ROWT, g_zero4, (uint32_t)((RG - n) * ROWT), bars + sti);
+          bulk_g2s(stage + RG * ROWT + n * ROWT, g_zero4, (uint32_t)((RG - n) * ROWT), bars + sti);
+        }
+      }
+      mk = j_own < n ? mk : 0;
+      x = 0.f;
+      w = 1.f;
+    } else {
+      const int e0 = lc * RG;
+      const int n_eu = sv.cnt[u * 4 + 2];
+      n = min(RG, n_eu - e0);
+      if (lane == 0) mbar_arrive_expect_tx(bars + sti, (uint32_t)(RG * ROWV));
+      __syncwarp();
+      int c = 0, emk = 0;
+      if (lane < n) {
+        c = __ldcg(sv.eu_ids + (size_t)u * sv.eu_cap + e0 + lane);
+        emk = __ldcg(sv.eu_mask + (size_t)u * sv.eu_cap + e0 + lane);
+        bulk_g2s(stage + lane * ROWV, ix.VS32 + ((size_t)u * ix.m_cap + c) * D, (uint32_t)ROWV, bars + sti);
+      }
+      if (lane == 0 && n < RG) bulk_g2s(stage + n * ROWV, g_zero4, (uint32_t)((RG - n) * ROWV), bars + sti);
+      // lane (row j_own, head h_own): logit sigma * q.C of its row (the ranking
+      // score, attention.py:98-100) and the cluster size as denominator weight
+      const int cj = __shfl_sync(0xffffffffu, c, j_own), mj = __shfl_sync(0xffffffffu, emk, j_own);
+      if (j_own < n) {
+        w = (float)__ldg(ix.cl_size + (size_t)u * ix.m_cap + cj);
+        if (h_own < G && ((mj >> h_own) & 1))
+          x = __ldcg(sv.scores + ((size_t)u * G + h_own) * ix.m_cap + cj) * isd;
+      }
+      mk = x == -INFINITY ? 0 : allmask;
+    }
+    smask[sti * 32 + lane] = mk;
+    sx[sti * 32 + lane] = x;
+    sw[sti * 32 + lane] = w;
+    if (lane == 0) stag[sti] = make_int4(u, kind, 0, 0);
+  };
+
+  // ---- q of the current unit (pre-scaled), softmax state, accumulators ----
+  float2 qv[HS][DP2];
+  int qu = -1;
+  auto load_q = [&](int u) {
+#pragma unroll
+    for (int h = 0; h < HS; h++)
+#pragma unroll
+      for (int k = 0; k < DP2; k++) {
+        const float* qp = sv.q + ((size_t)u * G + (h < G ? h : 0)) * D + sub * DPL + 2 * k;
+        qv[h][k] = h < G ? make_float2(__ldg(qp) * isd, __ldg(qp + 1) * isd) : make_float2(0.f, 0.f);
+      }
+    qu = u;
+  };
+  SoftState4<HS> ss;
+  float2 acc[HS][DP2];
+  auto reset = [&]() {
+#pragma unroll
+    for (int h = 0; h < HS; h++) {
+      ss.M[h] = -INFINITY;
+      ss.D[h] = 0.f;
+#pragma unroll
+      for (int k = 0; k < DP2; k++) acc[h][k] = make_float2(0.f, 0.f);
+    }
+  };
+  reset();
+  int cu = -1, ck = -1;  // (unit, kind) of the open partial
+  auto flush = [&]() {
+    if (cu < 0) return;
+#pragma unroll
+    for (int h = 0; h < HS; h++)
+#pragma unroll
+      for (int k = 0; k < DP2; k++) {
+        acc[h][k].x += __shfl_xor_sync(0xffffffffu, acc[h][k].x, 16);
+        acc[h][k].y += __shfl_xor_sync(0xffffffffu, acc[h][k].y, 16);
+      }
+    const size_t slot = (size_t)(wg + cu);
+    if (half == 0) {
+#pragma unroll
+      for (int h = 0; h < HS; h++) {
+        if (h < G) {
+          float* dst = sv.part + ((slot * 3 + ck) * G + h) * (size_t)(4 + D);  // (M, D, -, -, num[D])
+          if (sub == 0) { dst[0] = ss.M[h]; dst[1] = ss.D[h]; }
+#pragma unroll
+          for (int k = 0; k < DP2; k++) *reinterpret_cast<float2*>(dst + 4 + sub * DPL + 2 * k) = acc[h][k];
+        }
+      }
+    }
+    reset();
+  };
+
+  auto compute = [&](int sti, int kind) {
+    const unsigned char* stage = ring + sti * SB;
+    float alpha[HS];
+    float pw;
+    if (kind < 2) {
+      float v[16];
+#pragma unroll
+      for (int jj = 0; jj < RH; jj++) {
+        const int j = half + 2 * jj;
+        float2 kf[DP2];
+        Row4<T, DPL>::ld(stage + j * ROWT + sub * DPL * (int)sizeof(T), kf);
+#pragma unroll
+        for (int h = 0; h < HS; h++) {
+          float2 a2 = __fmul2_rn(kf[0], qv[h][0]);
+#pragma unroll
+          for (int k = 1; k < DP2; k++) a2 = __ffma2_rn(kf[k], qv[h][k], a2);
+          v[jj * HS + h] = a2.x + a2.y;
+        }
+      }
+#pragma unroll
+      for (int i = RH * HS; i < 16; i++) v[i] = 0.f;
+      float xl = att4_treduce16(v);
+      if (!((smask[sti * 32 + lane] >> h_own) & 1)) xl = -INFINITY;
+      pw = att4_softmax<HS>(xl, 1.f, ss, alpha);
+    } else {
+      pw = att4_softmax<HS>(sx[sti * 32 + lane], sw[sti * 32 + lane], ss, alpha);
+    }
+    // broadcast p of (row j, head h) from lane (j&1)*16 + (j>>1)*HS + h
+#pragma unroll
+    for (int h = 0; h < HS; h++) {
+      const float2 a = make_float2(alpha[h], alpha[h]);
+#pragma unroll
+      for (int k = 0; k < DP2; k++) acc[h][k] = __fmul2_rn(acc[h][k], a);
+    }
+#pragma unroll
+    for (int jj = 0; jj < RH; jj++) {
+      const int j = half + 2 * jj;
+      float2 vf[DP2];
+      if (kind < 2) Row4<T, DPL>::ld(stage + RG * ROWT + j * ROWT + sub * DPL * (int)sizeof(T), vf);
+      else Row4<float, DPL>::ld(stage + j * ROWV + sub * DPL * 4, vf);
+#pragma unroll
+      for (int h = 0; h < HS; h++) {
+        const float pj = __shfl_sync(0xffffffffu, pw, (lane & 16) + jj * HS + h);
+        const float2 p2 = make_float2(pj, pj);
+#pragma unroll
+        for (int k = 0; k < DP2; k++) acc[h][k] = __ffma2_rn(p2, vf[k], acc[h][k]);
+      }
+    }
+  };
+
+  const int nch = (int)(cb - ca);
+  if (nch > 0) {
+#pragma unroll
+    for (int i = 0; i < NST - 1; i++)
+      if (i < nch) issue(i, ca + i);
+    for (int k = 0; k < nch; k++) {
+      const int sti = k % NST;
+      if (k + NST - 1 < nch) {
+        fence_proxy_async();
+        __syncwarp();
+        issue((k + NST - 1) % NST, ca + k + NST - 1);
+      }
+      __syncwarp();
+      const int4 tg = stag[sti];
+      if (tg.x != cu || tg.y != ck) {
+        flush();
+        cu = tg.x;
+        ck = tg.y;
+        if (qu != cu) load_q(cu);
+      }
+      mbar_wait(bars + sti, (uint32_t)((k / NST) & 1));
+      compute(sti, ck);
+      __syncwarp();
+    }
+    flush();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// merge: one warp per (unit, head); lane owns d/32 dims
+// ---------------------------------------------------------------------------
+template <bool FULL, int DL>
+__global__ void __launch_bounds__(128) att4_merge_kernel(SteadyView st, StepView sv, AttnParams p,
+                                                          const int32_t* __restrict__ n_store, int U, int Wtot,
+                                                          int RG) {
+  const int G = p.G, d = p.d, D2 = 4 + d;  // partial record: (M, D, -, -, num[d])
+  const int gw = blockIdx.x * 4 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (gw >= U * G) return;
+  const int u = gw / G, g = gw % G;
+  const long long N = sv.woff[U];
+  int c0, c1, c2;
+  {
+    const int n_st = st.n[u];
+    c0 = (n_st + RG - 1) / RG;
+    if (FULL) { c1 = (n_store[u] + RG - 1) / RG; c2 = 0; }
+    else { c1 = sv.cnt[u * 4 + 3]; c2 = (sv.cnt[u * 4 + 2] + RG - 1) / RG; }
+  }
+  const long long ub = sv.woff[u];
+  const long long kb[4] = {ub, ub + c0, ub + c0 + c1, ub + c0 + c1 + c2};
+  double kM[3], kD[3];
+  float num[3][DL];  // DL = d / 32 dims per lane
+#pragma unroll
+  for (int k = 0; k < 3; k++) {
+    kM[k] = -INFINITY;
+    kD[k] = 0.0;
+#pragma unroll
+    for (int i = 0; i < DL; i++) num[k][i] = 0.f;
+    if (kb[k + 1] <= kb[k]) continue;
+    const int w0 = att4_warp_of(kb[k], N, Wtot), w1 = att4_warp_of(kb[k + 1] - 1, N, Wtot);
+    // pass 1 (lane-parallel over partials): max
+    float Mx = -INFINITY;
+    for (int w = w0 + lane; w <= w1; w += 32) {
+      const long long a = N * w / Wtot, b = N * (w + 1) / Wtot;
+      if (a >= b) continue;  // empty warp range: no partial written
+      const float* src = sv.part + (((size_t)(w + u) * 3 + k) * G + g) * (size_t)D2;
+      if (__ldcg(src + 1) > 0.f) Mx = fmaxf(Mx, __ldcg(src));
+    }
+    Mx = warp_max(Mx);
+    if (Mx == -INFINITY) continue;
+    // pass 2: per-partial scale (lane-parallel), then independent numerator loads
+    float Dn = 0.f;
+    for (int w32 = w0; w32 <= w1; w32 += 32) {
+      const int w = w32 + lane;
+      float sc = 0.f;
+      if (w <= w1) {
+        const long long a = N * w / Wtot, b = N * (w + 1) / Wtot;
+        if (a < b) {
+          const float* src = sv.part + (((size_t)(w + u) * 3 + k) * G + g) * (size_t)D2;
+          const float dw = __ldcg(src + 1);
+          if (dw > 0.f) { sc = __expf(__ldcg(src) - Mx); Dn += dw * sc; }
+        }
+      }
+      const int nw = min(32, w1 - w32 + 1);
+      // partials of empty-range warps may hold stale bits: scale 0 and select
+#pragma unroll 8
+      for (int i = 0; i < nw; i++) {
+        const float sw = __shfl_sync(0xffffffffu, sc, i);
+        const float* src = sv.part + (((size_t)(w32 + i + u) * 3 + k) * G + g) * (size_t)D2 + 4 + lane * DL;
+        float v[DL];
+        if (DL == 4) {
+          const float4 x = __ldcg(reinterpret_cast<const float4*>(src));
+          v[0] = x.x; v[1] = x.y; v[2 % DL] = x.z; v[3 % DL] = x.w;
+        } else {
+          const float2 x = __ldcg(reinterpret_cast<const float2*>(src));
+          v[0] = x.x; v[1 % DL] = x.y;
+        }
+#pragma unroll
+        for (int j = 0; j < DL; j++) num[k][j] += sw != 0.f ? v[j] * sw : 0.f;
+      }
+    }
+    kM[k] = Mx;
+    kD[k] = warp_sum(Dn);
+  }
+  const float zero4[4] = {-INFINITY, 0.f, -INFINITY, 0.f};
+  const float* tl = (!FULL && sv.tail) ? sv.tail + ((size_t)u * G + g) * 4 : zero4;
+  const bool live0 = kD[0] > 0, live1 = kD[1] > 0, live2 = kD[2] > 0;
+  const bool live3 = p.tail_denominator_only && tl[1] > 0.f;
+  double gmax = -INFINITY;
+  if (live0) gmax = fmax(gmax, kM[0]);
+  if (live1) gmax = fmax(gmax, kM[1]);
+  if (live2) gmax = fmax(gmax, kM[2]);
+  if (live3) gmax = fmax(gmax, (double)tl[0]);
+  if (gmax == -INFINITY) {  // merge requires a non-empty partial (attention.py:117-119)
+    if (lane == 0) set_status(sv.status, kErrEmptyMerge);
+    return;
+  }
+  const double sc0 = live0 ? exp(kM[0] - gmax) : 0.0, sc1 = live1 ? exp(kM[1] - gmax) : 0.0,
+               sc2 = live2 ? exp(kM[2] - gmax) : 0.0, sc3 = live3 ? exp((double)tl[0] - gmax) : 0.0;
+  const double den = kD[0] * sc0 + kD[1] * sc1 + kD[2] * sc2 + (live3 ? (double)tl[1] * sc3 : 0.0);
+  double out_scale, logden, cov;
+  if (!p.denominator_eq2) {
+    out_scale = 1.0 / den;
+    logden = gmax + log(den);
+    cov = den > 0 ? (kD[0] * sc0 + kD[1] * sc1) / den : 0.0;
+  } else {
+    // eq2: denominator = steady exact terms + centroid terms of all clusters
+    const bool la = tl[3] > 0.f;
+    double gd = -INFINITY;
+    if (live0) gd = fmax(gd, kM[0]);
+    if (la) gd = fmax(gd, (double)tl[2]);
+    const double dd = (live0 ? kD[0] * exp(kM[0] - gd) : 0.0) + (la ? (double)tl[3] * exp((double)tl[2] - gd) : 0.0);
+    out_scale = exp(gmax - gd) / dd;
+    logden = gd + log(dd);
+    cov = dd > 0 ? (live0 ? kD[0] * exp(kM[0] - gd) : 0.0) / dd : 0.0;
+  }
+  float* out = sv.out + ((size_t)u * G + g) * d;
+#pragma unroll
+  for (int i = 0; i < DL; i++) {
+    const double v = (double)num[0][i] * sc0 + (double)num[1][i] * sc1 + (double)num[2][i] * sc2;
+    out[lane * DL + i] = (float)(v * out_scale);
+  }
+  if (lane == 0) {
+    sv.logden[(size_t)u * G + g] = (float)logden;
+    sv.cov[(size_t)u * G + g] = (float)cov;
+  }
+}
+
+template <typename T, int DPL, int HS, bool FULL>
+size_t attend_v4_smem() { return Att4Cfg<T, DPL, HS>::SMEM; }
+
+#define WK_INST_ATT4(T, DL, HS)                                                                                   \
+  template __global__ void attend_v4_kernel<T, DL, HS, false>(IndexView, SteadyView, StepView, AttnParams,          \
+                                                             const int32_t*, int);                                 \
+  template __global__ void attend_v4_kernel<T, DL, HS, true>(IndexView, SteadyView, StepView, AttnParams,           \
+                                                            const int32_t*, int);                                  \
+  template size_t attend_v4_smem<T, DL, HS, false>();                                                              \
+  template size_t attend_v4_smem<T, DL, HS, true>();
+WK_INST_ATT4(__nv_bfloat16, 8, 4)
+WK_INST_ATT4(__nv_bfloat16, 8, 8)
+WK_INST_ATT4(__nv_bfloat16, 4, 4)
+WK_INST_ATT4(__nv_bfloat16, 4, 8)
+WK_INST_ATT4(float, 8, 4)
+WK_INST_ATT4(float, 8, 8)
+WK_INST_ATT4(float, 4, 4)
+WK_INST_ATT4(float, 4, 8)
+template __global__ void att4_merge_kernel<false, 4>(SteadyView, StepView, AttnParams, const int32_t*, int, int, int);
+template __global__ void att4_merge_kernel<true, 4>(SteadyView, StepView, AttnParams, const int32_t*, int, int, int);
+template __global__ void att4_merge_kernel<false, 2>(SteadyView, StepView, AttnParams, const int32_t*, int, int, int);
+template __global__ void att4_merge_kernel<true, 2>(SteadyView, StepView, AttnParams, const int32_t*, int, int, int);
+
+}  // namespace wk

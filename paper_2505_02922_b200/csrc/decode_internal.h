@@ -15,6 +15,9 @@ struct SelParams {
   float inv_sqrt_d;
   int need_tail, need_allc;
   int score_fp64;  // scores came from the fp64-accumulating kernel (score_v3)
+  int score_mode;  // wk_zone_params.score_mode of the scores being selected
+  int piece_rows;  // rows per retrieval piece (attend_v4 chunk rows)
+  int prof;        // record phase timestamps (g_sel_dbg)
 };
 
 struct AttnParams {

@@ -1,0 +1,600 @@
+// select_v6.cu -- exact zone planning (index.py:61-93) + per-unit unions.
+//
+// One CTA per (unit, head).  Produces the reference's bits: the ordered
+// retrieval list (top r of the fp64 dgemv score q.C, ties to the lower id,
+// lexsort((arange, -s)) at index.py:75) and the estimation set (the next e,
+// plan_zones index.py:79-93).
+//
+//   1. the head's approximate scores s' (score kernel, |s' - s| <= B) are
+//      staged once in shared memory (SMS) -- every later pass reads smem;
+//   2. 512 linear buckets over [min, max] locate the buckets holding rank r and
+//      rank r+e; rank-by-counting inside them gives the exact r-th / (r+e)-th
+//      largest s' (tau_r, tau_e);
+//   3. rows with s' > tau + 2B are certainly in, s' < tau - 2B certainly out;
+//      the band between and "clumps" (approx-order neighbours closer than 2B)
+//      are re-scored EXACTLY with the reference's dgemv recipe on the fp64
+//      centroid row -- 8 rows per warp, 4 lanes per row (one FMA chain each);
+//   4. R / E membership goes to per-head bitmaps; the last CTA of the unit ORs
+//      the G bitmaps and emits the unit's union: retrieval "pieces" (runs of
+//      <= piece_rows contiguous store rows of one cluster + head mask) and
+//      estimation rows (cluster id, head mask, per-head logits, size) -- the
+//      work lists of attend_v4.
+#include "common.cuh"
+#include "decode_internal.h"
+
+namespace wk {
+
+constexpr int S6_T = 256;
+constexpr int S6_NW = S6_T / 32;
+constexpr int S6_NB = 2048;    // histogram buckets (linear over [min, max])
+constexpr int S6_BAND = 256;   // band rows around tau_{r+e}
+constexpr int S6_SMEM_M = 16384;  // largest m whose scores are staged in smem
+
+template <int CAND>
+struct Sel6Smem {
+  union {
+    int hist[S6_NB];                                               // passes A-B
+    struct { unsigned long long fin[CAND]; double fex[CAND]; } f;  // final order
+  } x;
+  union {
+    unsigned long long cand[CAND];  // candidates (unordered), until sorted
+    double cex[CAND];               // exact scores (band / clump rows), by position
+  } y;
+  unsigned long long cs[CAND];      // candidates ordered (approx desc, id asc)
+  int xpos[CAND];                   // positions needing an exact score
+  int be_id[S6_BAND];
+  double be_ex[S6_BAND];
+  unsigned char be_sel[S6_BAND];
+  float red[3][S6_NW];
+  int wsum[4][S6_NW];
+  int ncand, nband_r, nband_e, n_in_e, nx, ovf, last, b1, b2;
+  int base[4];
+  float fred[3];
+};
+
+// phase timestamps (globaltimer) for tools/seltime6.py when p.prof != 0
+#define S6_MARK(i)                                                                     \
+  do {                                                                                 \
+    if (p.prof && threadIdx.x == 0 && blockIdx.x < 4096) {                             \
+      long long _t;                                                                    \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                           \
+      g_sel_dbg[blockIdx.x][i] = _t;                                                   \
+    }                                                                                  \
+  } while (0)
+
+WK_DEVINL unsigned long long s6_key(float s, int id) {
+  return ((unsigned long long)(~f2u_ord(s)) << 32) | (unsigned int)id;
+}
+WK_DEVINL float s6_score(unsigned long long k) { return u2f_ord(~(unsigned int)(k >> 32)); }
+WK_DEVINL int s6_id(unsigned long long k) { return (int)(k & 0xffffffffu); }
+WK_DEVINL bool s6_better(double a, int ia, double b, int ib) { return a > b || (a == b && ia < ib); }
+
+// warp-aggregated append (all lanes of the warp call it)
+template <typename V>
+WK_DEVINL void s6_append(bool flag, V val, V* list, int* counter, int cap, int* ovf) {
+  const unsigned mk = __ballot_sync(0xffffffffu, flag);
+  if (!mk) return;
+  const int lane = threadIdx.x & 31, leader = __ffs(mk) - 1;
+  int b = 0;
+  if (lane == leader) b = atomicAdd(counter, __popc(mk));
+  b = __shfl_sync(0xffffffffu, b, leader);
+  if (flag) {
+    const int pos = b + __popc(mk & ((1u << lane) - 1u));
+    if (pos < cap) list[pos] = val; else *ovf = 1;
+  }
+}
+
+// block reduction of three floats: (sum, max, max)
+template <int CAND>
+WK_DEVINL void s6_reduce3(float& a, float& b, float& c, Sel6Smem<CAND>& sm) {
+  a = warp_sum(a); b = warp_max(b); c = warp_max(c);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) { sm.red[0][w] = a; sm.red[1][w] = b; sm.red[2][w] = c; }
+  __syncthreads();
+  if (w == 0) {
+    float x = lane < S6_NW ? sm.red[0][lane] : 0.f;
+    float y = lane < S6_NW ? sm.red[1][lane] : -INFINITY;
+    float z = lane < S6_NW ? sm.red[2][lane] : -INFINITY;
+    x = warp_sum(x); y = warp_max(y); z = warp_max(z);
+    if (lane == 0) { sm.fred[0] = x; sm.fred[1] = y; sm.fred[2] = z; }
+  }
+  __syncthreads();
+  a = sm.fred[0]; b = sm.fred[1]; c = sm.fred[2];
+}
+
+// block exclusive scan of four ints; returns totals in tot[]
+template <int CAND>
+WK_DEVINL void s6_scan4(int (&v)[4], int (&tot)[4], Sel6Smem<CAND>& sm) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x[4];
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    x[i] = v[i];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x[i], o);
+      if (lane >= o) x[i] += y;
+    }
+  }
+  if (lane == 31)
+#pragma unroll
+    for (int i = 0; i < 4; i++) sm.wsum[i][w] = x[i];
+  __syncthreads();
+  if (w == 0) {
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      const int val = lane < S6_NW ? sm.wsum[i][lane] : 0;
+      int iv = val;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, iv, o);
+        if (lane >= o) iv += y;
+      }
+      if (lane < S6_NW) sm.wsum[i][lane] = iv - val;
+      if (lane == S6_NW - 1) sm.base[i] = iv;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    const int ex = sm.wsum[i][w] + x[i] - v[i];
+    tot[i] = sm.base[i];
+    v[i] = ex;
+  }
+  __syncthreads();
+}
+
+// exact dgemv-recipe scores (index.py:74 via OpenBLAS dgemv_t, DESIGN.md
+// "Numerics recipes"): item `it` of the warp's 8 rows is served by lanes
+// 4*(it%8) .. +3; lane j accumulates chain j.  Returns the score on every lane
+// of the quad.
+WK_DEVINL double s6_exact_quad(const double* __restrict__ row, const float* __restrict__ q, int d, int cls, bool act) {
+  const int j = threadIdx.x & 3;
+  double acc = 0.0;
+  if (act) {
+    if (cls == 0) {
+#pragma unroll 8
+      for (int t = j; t < d; t += 4) acc = __fma_rn(__ldcg(row + t), (double)__ldg(q + t), acc);
+    } else if (cls == 1) {
+      if (j < 2) {
+#pragma unroll 8
+        for (int t = j; t < d; t += 2) acc = __dadd_rn(acc, __dmul_rn(__ldcg(row + t), (double)__ldg(q + t)));
+      }
+    } else {
+#pragma unroll 8
+      for (int t = j; t < d; t += 4) acc = __dadd_rn(acc, __dmul_rn(__ldcg(row + t), (double)__ldg(q + t)));
+    }
+  }
+  const int base = (threadIdx.x & 31) & ~3;
+  const double a0 = __shfl_sync(0xffffffffu, acc, base), a1 = __shfl_sync(0xffffffffu, acc, base + 1),
+               a2 = __shfl_sync(0xffffffffu, acc, base + 2), a3 = __shfl_sync(0xffffffffu, acc, base + 3);
+  if (cls == 1) return __dadd_rn(0.0, __dadd_rn(a0, a1));
+  return __dadd_rn(0.0, __dadd_rn(__dadd_rn(a0, a2), __dadd_rn(a1, a3)));
+}
+
+// ---------------------------------------------------------------------------
+// union of the unit's G zone bitmaps -> attend_v4 work lists
+// ---------------------------------------------------------------------------
+template <int CAND>
+__device__ void s6_union(const IndexView& ix, const StepView& sv, const SelParams& p, int u, int m,
+                         Sel6Smem<CAND>& sm) {
+  const int G = p.G, T = S6_T, t = threadIdx.x;
+  const int W = (m + 31) >> 5;
+  const int w0 = (int)((long long)W * t / T), w1 = (int)((long long)W * (t + 1) / T);
+  const uint32_t* rb = sv.rbits + (size_t)u * G * sv.w_cap;
+  const uint32_t* eb = sv.ebits + (size_t)u * G * sv.w_cap;
+  const int* csize = ix.cl_size + (size_t)u * ix.m_cap;
+  const int* coff = ix.cl_off + (size_t)u * ix.m_cap;
+  const int PR = p.piece_rows;
+  // pass 1: counts (clusters, tokens, pieces, estimation rows)
+  int v[4] = {0, 0, 0, 0};
+  for (int w = w0; w < w1; w++) {
+    uint32_t ur = 0u, ue = 0u;
+    for (int g = 0; g < G; g++) { ur |= __ldcg(rb + (size_t)g * sv.w_cap + w); ue |= __ldcg(eb + (size_t)g * sv.w_cap + w); }
+    v[0] += __popc(ur);
+    v[3] += __popc(ue);
+    while (ur) {
+      const int c = (w << 5) + __ffs(ur) - 1;
+      ur &= ur - 1;
+      const int s = __ldg(csize + c);
+      v[1] += s;
+      v[2] += (s + PR - 1) / PR;
+    }
+  }
+  int tot[4];
+  s6_scan4(v, tot, sm);
+  const int n_ru = tot[0], n_rt = tot[1], n_pc = tot[2], n_eu = tot[3];
+  const bool fits = n_pc <= sv.pc_cap && n_eu <= sv.eu_cap && n_ru <= sv.ru_cap;
+  if (!fits) set_status(sv.status, kErrUnion);
+  // pass 2: emit
+  int2* pcs = reinterpret_cast<int2*>(sv.pieces) + (size_t)u * sv.pc_cap;
+  int32_t* ru = sv.ru_ids + (size_t)u * sv.ru_cap;
+  uint8_t* rmk = sv.ru_mask + (size_t)u * sv.ru_cap;
+  int32_t* eu = sv.eu_ids + (size_t)u * sv.eu_cap;
+  uint8_t* emk = sv.eu_mask + (size_t)u * sv.eu_cap;
+  int ir = v[0], ipc = v[2], ie = v[3];
+  if (fits) {
+    for (int w = w0; w < w1; w++) {
+      uint32_t rw[8], ew[8];
+      uint32_t ur = 0u, ue = 0u;
+#pragma unroll
+      for (int g = 0; g < 8; g++) {
+        rw[g] = g < G ? __ldcg(rb + (size_t)g * sv.w_cap + w) : 0u;
+        ew[g] = g < G ? __ldcg(eb + (size_t)g * sv.w_cap + w) : 0u;
+        ur |= rw[g];
+        ue |= ew[g];
+      }
+      while (ur) {
+        const int bit = __ffs(ur) - 1;
+        ur &= ur - 1;
+        const int c = (w << 5) + bit;
+        int mk = 0;
+#pragma unroll
+        for (int g = 0; g < 8; g++) mk |= ((rw[g] >> bit) & 1u) << g;
+        const int s = __ldg(csize + c), o = __ldg(coff + c);
+        ru[ir] = c;
+        rmk[ir] = (uint8_t)mk;
+        ir++;
+        for (int j = 0; j < s; j += PR) pcs[ipc++] = make_int2(o + j, min(PR, s - j) | (mk << 8));
+      }
+      while (ue) {
+        const int bit = __ffs(ue) - 1;
+        ue &= ue - 1;
+        int mk = 0;
+#pragma unroll
+        for (int g = 0; g < 8; g++) mk |= ((ew[g] >> bit) & 1u) << g;
+        eu[ie] = (w << 5) + bit;
+        emk[ie] = (uint8_t)mk;
+        ie++;
+      }
+    }
+  }
+  if (t == 0) {
+    sv.cnt[u * 4 + 0] = fits ? n_ru : 0;
+    sv.cnt[u * 4 + 1] = fits ? n_rt : 0;
+    sv.cnt[u * 4 + 2] = fits ? n_eu : 0;
+    sv.cnt[u * 4 + 3] = fits ? n_pc : 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+template <int CAND, bool SMS>
+__global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepView sv, SelParams p) {
+  extern __shared__ __align__(16) unsigned char s6_raw[];  // Sel6Smem | SMS: scores [m] | bitmaps R, TRE [W]
+  Sel6Smem<CAND>& sm = *reinterpret_cast<Sel6Smem<CAND>*>(s6_raw);
+  float* s6_dyn = reinterpret_cast<float*>(s6_raw + ((sizeof(Sel6Smem<CAND>) + 15) & ~(size_t)15));
+  const int G = p.G, d = p.d;
+  const int u = blockIdx.x / G, g = blockIdx.x % G;
+  const int m = sv.m[u];
+  const int t = threadIdx.x, T = S6_T, lane = t & 31, warp = t >> 5;
+  const int W = (m + 31) >> 5;
+  float* scs = s6_dyn;
+  uint32_t* rbits = reinterpret_cast<uint32_t*>(s6_dyn + (SMS ? ((m + 3) & ~3) : 0));
+  uint32_t* tre = rbits + W;  // certain or selected members of the top r+e
+  float* tailp = sv.tail + ((size_t)u * G + g) * 4;
+  int r = 0, e = 0;
+  if (m > 0) {
+    r = (int)floor(p.retrieval_fraction * (double)m + 0.5);
+    if (r < 1) r = 1;
+    if (r > m) r = m;
+    e = (int)floor(p.estimation_fraction * (double)m + 0.5);
+    if (e > m - r) e = m - r;
+  }
+  if (t == 0 && g == 0) { sv.nr[u] = r; sv.ne[u] = e; }
+  const float* s = sv.scores + ((size_t)u * G + g) * ix.m_cap;
+  const float* q = sv.q + ((size_t)u * G + g) * d;
+  const double* C64 = ix.C64 + (size_t)u * ix.m_cap * d;
+  uint32_t* rb_out = sv.rbits + ((size_t)u * G + g) * sv.w_cap;
+  uint32_t* eb_out = sv.ebits + ((size_t)u * G + g) * sv.w_cap;
+  auto S_ = [&](int c) -> float { return SMS ? scs[c] : __ldcg(s + c); };
+  bool ok = m > 0 && r <= CAND && r <= sv.r_cap;
+  if (m > 0 && !ok) set_status(sv.status, kErrBandOverflow);
+  for (int w = t; w < W; w += T) { rbits[w] = 0u; tre[w] = 0u; }
+  double B2 = 0.0;
+  float bk_mn = 0.f, bk_scale = 0.f;
+  auto bucket = [&](float v) {
+    int b = (int)((v - bk_mn) * bk_scale);
+    return b < 0 ? 0 : (b >= S6_NB ? S6_NB - 1 : b);
+  };
+  // rigorous value range of bucket b under the float evaluation of bucket():
+  // fl(fl(v - mn) * scale) in [b, b + 1)  =>  v - mn in
+  // [b / (scale (1+u)^2), (b + 1) / (scale (1-u)^2)),  u = 2^-24
+  auto edge_lo = [&](int b) -> double {
+    return (double)bk_mn + (double)b / ((double)bk_scale * (1.0 + 1.1920928955078125e-07));
+  };
+  auto edge_hi = [&](int b) -> double {
+    return b >= S6_NB - 1 ? (double)INFINITY
+                          : (double)bk_mn + (double)(b + 1) / ((double)bk_scale * (1.0 - 1.1920928955078125e-07));
+  };
+  double hr = 0, lr = 0, he = 0, le = 0;
+  if (ok) {
+  S6_MARK(0);
+    // ---- pass A: stage scores, min / max, |q|^2 ----
+    float mn = INFINITY, mx = -INFINITY;
+    const int m4 = m >> 2;
+#pragma unroll 4
+    for (int i = t; i < m4; i += T) {
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(s) + i);
+      if (SMS) reinterpret_cast<float4*>(scs)[i] = v;
+      mn = fminf(mn, fminf(fminf(v.x, v.y), fminf(v.z, v.w)));
+      mx = fmaxf(mx, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
+    }
+    for (int i = 4 * m4 + t; i < m; i += T) {
+      const float v = __ldcg(s + i);
+      if (SMS) scs[i] = v;
+      mn = fminf(mn, v); mx = fmaxf(mx, v);
+    }
+    float qq = 0.f;
+    for (int i = t; i < d; i += T) { const float qi = q[i]; qq = fmaf(qi, qi, qq); }
+    for (int b = t; b < S6_NB; b += T) sm.x.hist[b] = 0;
+    if (t == 0) { sm.ncand = sm.nband_r = sm.nband_e = sm.n_in_e = sm.nx = sm.ovf = 0; sm.b1 = sm.b2 = -1; }
+    float nmn = -mn;
+    s6_reduce3(qq, mx, nmn, sm);
+    mn = -nmn;
+    const double B = score_error_bound_v2((double)qq, (double)ix.Cmax[u], d, p.score_mode);
+    B2 = 2.0 * B;
+    const float span = mx - mn;
+    bk_mn = mn;
+    bk_scale = span > 0.f ? (float)S6_NB / span : 0.f;
+  S6_MARK(1);
+    // ---- pass B: histogram ----
+#pragma unroll 4
+    for (int c = t; c < m; c += T) atomicAdd(&sm.x.hist[bucket(S_(c))], 1);
+    __syncthreads();
+    // buckets holding rank K1 = r and K2 = r + e (descending): thread t owns
+    // the 8 buckets 2047-8t .. 2040-8t
+    {
+      constexpr int PB = S6_NB / S6_T;
+      const int K1 = r, K2 = e > 0 ? r + e : 0;
+      const int top = S6_NB - 1 - PB * t;
+      int h[PB], x = 0;
+#pragma unroll
+      for (int i = 0; i < PB; i++) { h[i] = sm.x.hist[top - i]; x += h[i]; }
+      const int own = x;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) sm.wsum[0][warp] = x;
+      __syncthreads();
+      if (warp == 0) {
+        const int val = lane < S6_NW ? sm.wsum[0][lane] : 0;
+        int iv = val;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, iv, o);
+          if (lane >= o) iv += y;
+        }
+        if (lane < S6_NW) sm.wsum[0][lane] = iv - val;
+      }
+      __syncthreads();
+      int ab = sm.wsum[0][warp] + x - own;  // elements above this thread's buckets
+#pragma unroll
+      for (int i = 0; i < PB; i++) {
+        if (ab < K1 && ab + h[i] >= K1) sm.b1 = top - i;
+        if (K2 > 0 && ab < K2 && ab + h[i] >= K2) sm.b2 = top - i;
+        ab += h[i];
+      }
+    }
+    __syncthreads();
+  S6_MARK(2);
+    // tau_r (the r-th largest s') lies in bucket b1, tau_e in b2: rows above
+    // edge_hi + 2B are certainly in, rows below edge_lo - 2B certainly out
+    const int b1 = sm.b1, b2 = sm.b2;
+    if (b1 < 0 || (e > 0 && b2 < 0)) ok = false;
+    hr = edge_hi(b1) + B2; lr = edge_lo(b1) - B2;
+    if (e > 0) { he = edge_hi(b2) + B2; le = edge_lo(b2) - B2; }
+  }
+  S6_MARK(3);
+  if (ok) {
+    // ---- pass D: candidates for R (certain-in + band), band around tau_e,
+    //      certain members of the top r+e (bitmap, one ballot per word) ----
+    for (int base = 0; base < m; base += T) {
+      const int c = base + t;
+      const bool act = c < m;
+      const float v = act ? S_(c) : 0.f;
+      const double dv = (double)v;
+      const bool in_r = act && dv > hr;
+      const bool bd_r = act && !in_r && dv >= lr;
+      s6_append(in_r || bd_r, s6_key(v, c), sm.y.cand, &sm.ncand, CAND, &sm.ovf);
+      const unsigned mbr = __ballot_sync(0xffffffffu, bd_r);
+      if (lane == 0 && mbr) atomicAdd(&sm.nband_r, __popc(mbr));
+      if (e > 0) {
+        const bool in_e = act && dv > he;
+        const bool bd_e = act && !in_e && dv >= le;
+        const unsigned mie = __ballot_sync(0xffffffffu, in_e);
+        if (lane == 0 && mie) { tre[c >> 5] = mie; atomicAdd(&sm.n_in_e, __popc(mie)); }
+        s6_append(bd_e, c, sm.be_id, &sm.nband_e, S6_BAND, &sm.ovf);
+      }
+    }
+    __syncthreads();
+    const int nc = sm.ncand, nbr = sm.nband_r, nin_r = nc - nbr, nbe = sm.nband_e, nin_e = sm.n_in_e;
+    if (sm.ovf || nin_r > r || nc < r || (e > 0 && (nin_e > r + e || nin_e + nbe < r + e))) {
+      ok = false;
+    } else {
+  S6_MARK(4);
+      // ---- order candidates by (approx desc, id asc): rank by counting ----
+      for (int i = t; i < nc; i += T) {
+        const unsigned long long k = sm.y.cand[i];
+        int rk = 0;
+        for (int j = 0; j < nc; j++) rk += sm.y.cand[j] < k ? 1 : 0;
+        sm.cs[rk] = k;
+      }
+      __syncthreads();
+      // ---- positions needing an exact score: band rows and clump members ----
+      for (int base = 0; base < nc; base += T) {
+        const int i = base + t;
+        bool need = false;
+        if (i < nc) {
+          sm.y.cex[i] = 0.0;
+          if (i >= nin_r) need = true;
+          else {
+            const double si = (double)s6_score(sm.cs[i]);
+            need = (i > 0 && (double)s6_score(sm.cs[i - 1]) - si <= B2) ||
+                   (i + 1 < nc && si - (double)s6_score(sm.cs[i + 1]) <= B2);
+          }
+        }
+        s6_append(need, i, sm.xpos, &sm.nx, CAND, &sm.ovf);
+      }
+      __syncthreads();
+  S6_MARK(5);
+      // ---- one exact round: 8 rows per warp, 4 lanes per row ----
+      const int nx = sm.nx, nall = nx + nbe;
+      for (int b0 = warp * 8; b0 < nall; b0 += S6_NW * 8) {
+        const int it = b0 + (lane >> 2);
+        const bool act = it < nall;
+        const int c = !act ? 0 : (it < nx ? s6_id(sm.cs[sm.xpos[it]]) : sm.be_id[it - nx]);
+        const int cls = gemv_row_class(c, m, d, p.blas_threads);
+        const double ex = s6_exact_quad(C64 + (size_t)c * d, q, d, cls, act);
+        if (act && (lane & 3) == 0) {
+          if (it < nx) sm.y.cex[sm.xpos[it]] = ex;
+          else sm.be_ex[it - nx] = ex;
+        }
+      }
+      __syncthreads();
+  S6_MARK(6);
+      // ---- band winners for R: best (r - nin_r) band rows by exact score ----
+      const int need_r = r - nin_r;
+      for (int i = nin_r + t; i < nc; i += T) {
+        int rank = 0;
+        const double ci = sm.y.cex[i];
+        const int ii = s6_id(sm.cs[i]);
+        for (int j = nin_r; j < nc; j++) rank += s6_better(sm.y.cex[j], s6_id(sm.cs[j]), ci, ii) ? 1 : 0;
+        if (rank >= need_r) sm.cs[i] = ~0ull;  // dropped
+      }
+      // ---- band winners for the top r+e ----
+      const int need_e = r + e - nin_e;
+      for (int i = t; i < nbe; i += T) {
+        int rank = 0;
+        for (int j = 0; j < nbe; j++) rank += s6_better(sm.be_ex[j], sm.be_id[j], sm.be_ex[i], sm.be_id[i]) ? 1 : 0;
+        sm.be_sel[i] = rank < need_e ? 1 : 0;
+      }
+      __syncthreads();
+      // compact: certain-in keep their positions, band winners follow in approx order
+      for (int i = t; i < nc; i += T) {
+        if (i < nin_r) { sm.x.f.fin[i] = sm.cs[i]; sm.x.f.fex[i] = sm.y.cex[i]; continue; }
+        if (sm.cs[i] == ~0ull) continue;
+        int before = 0;
+        for (int j = nin_r; j < i; j++) before += sm.cs[j] != ~0ull ? 1 : 0;
+        sm.x.f.fin[nin_r + before] = sm.cs[i];
+        sm.x.f.fex[nin_r + before] = sm.y.cex[i];
+      }
+      for (int i = t; i < nbe; i += T)
+        if (sm.be_sel[i]) atomicOr(tre + (sm.be_id[i] >> 5), 1u << (sm.be_id[i] & 31));
+      __syncthreads();
+  S6_MARK(7);
+      // every maximal run of approx-order neighbours closer than 2B was
+      // exact-scored: sort each run exactly (insertion sort by its first thread)
+      for (int i = t; i < r; i += T) {
+        const double si = (double)s6_score(sm.x.f.fin[i]);
+        const bool lp = i > 0 && (double)s6_score(sm.x.f.fin[i - 1]) - si <= B2;
+        const bool ln = i + 1 < r && si - (double)s6_score(sm.x.f.fin[i + 1]) <= B2;
+        if (!lp && ln) {
+          int end = i + 1;
+          while (end + 1 < r && (double)s6_score(sm.x.f.fin[end]) - (double)s6_score(sm.x.f.fin[end + 1]) <= B2) end++;
+          for (int a = i + 1; a <= end; a++) {
+            const unsigned long long kk = sm.x.f.fin[a];
+            const double ev = sm.x.f.fex[a];
+            int b = a - 1;
+            while (b >= i && s6_better(ev, s6_id(kk), sm.x.f.fex[b], s6_id(sm.x.f.fin[b]))) {
+              sm.x.f.fin[b + 1] = sm.x.f.fin[b];
+              sm.x.f.fex[b + 1] = sm.x.f.fex[b];
+              b--;
+            }
+            sm.x.f.fin[b + 1] = kk;
+            sm.x.f.fex[b + 1] = ev;
+          }
+        }
+      }
+      __syncthreads();
+  S6_MARK(8);
+      // ---- outputs: ordered retrieval list, R bitmap ----
+      int32_t* rl_out = sv.rlist + ((size_t)u * G + g) * sv.r_cap;
+      for (int i = t; i < r; i += T) {
+        const int c = s6_id(sm.x.f.fin[i]);
+        rl_out[i] = c;
+        atomicOr(rbits + (c >> 5), 1u << (c & 31));
+      }
+      __syncthreads();
+      // E = top(r+e) minus R
+      int32_t* el_out = sv.elist ? sv.elist + ((size_t)u * G + g) * sv.e_cap : nullptr;
+      int ecnt = 0;
+      for (int w = t; w < W; w += T) {
+        const uint32_t ew = tre[w] & ~rbits[w];
+        rb_out[w] = rbits[w];
+        eb_out[w] = ew;
+        tre[w] = ew;
+        ecnt += __popc(ew);
+      }
+      if (el_out) {
+        int v4[4] = {ecnt, 0, 0, 0}, tot[4];
+        s6_scan4(v4, tot, sm);
+        int pos = v4[0];
+        for (int w = t; w < W; w += T) {
+          uint32_t ew = tre[w];
+          while (ew) {
+            el_out[pos++] = (w << 5) + __ffs(ew) - 1;
+            ew &= ew - 1;
+          }
+        }
+      }
+      if (p.need_tail || p.need_allc) {
+        __syncthreads();
+        const float isd = p.inv_sqrt_d;
+        const int* csize = ix.cl_size + (size_t)u * ix.m_cap;
+        float mx_t = -INFINITY, mx_a = -INFINITY;
+        for (int c = t; c < m; c += T) {
+          const float xv = S_(c) * isd;
+          mx_a = fmaxf(mx_a, xv);
+          const bool z = ((rbits[c >> 5] | tre[c >> 5]) >> (c & 31)) & 1u;
+          if (!z) mx_t = fmaxf(mx_t, xv);
+        }
+        float dummy = 0.f;
+        s6_reduce3(dummy, mx_t, mx_a, sm);
+        float dt = 0.f, da = 0.f, dz = -INFINITY;
+        for (int c = t; c < m; c += T) {
+          const float xv = S_(c) * isd;
+          const float sz = (float)csize[c];
+          da += sz * expf(xv - mx_a);
+          const bool z = ((rbits[c >> 5] | tre[c >> 5]) >> (c & 31)) & 1u;
+          if (!z) dt += sz * expf(xv - mx_t);
+        }
+        float dz2 = -INFINITY;
+        s6_reduce3(dt, dz, dz2, sm);
+        s6_reduce3(da, dz, dz2, sm);
+        if (t == 0) { tailp[0] = mx_t; tailp[1] = dt; tailp[2] = mx_a; tailp[3] = da; }
+      }
+    }
+  }
+  if (m > 0 && !ok) {
+    set_status(sv.status, kErrBandOverflow);
+    for (int w = t; w < W; w += T) { rb_out[w] = 0u; eb_out[w] = 0u; }
+  }
+  if (!ok && t == 0) { tailp[0] = -INFINITY; tailp[1] = 0.f; tailp[2] = -INFINITY; tailp[3] = 0.f; }
+  S6_MARK(9);
+  // ---- the last CTA of the unit builds the union ----
+  __threadfence();
+  __syncthreads();
+  if (t == 0) sm.last = (atomicAdd(sv.sel_done + u, 1) == G - 1);
+  __syncthreads();
+  if (!sm.last) return;
+  __threadfence();
+  if (t == 0) sv.sel_done[u] = 0;
+  S6_MARK(10);
+  s6_union(ix, sv, p, u, m, sm);
+  S6_MARK(11);
+  if (p.prof && t == 0) { g_sel_dbg[blockIdx.x][12] = sm.ncand; g_sel_dbg[blockIdx.x][13] = sm.nx; g_sel_dbg[blockIdx.x][14] = sm.nband_e; }
+}
+
+size_t select_v6_dyn_smem(int m_max, bool sms, int cand) {
+  const int W = (m_max + 31) >> 5;
+  const size_t hdr = cand <= 512 ? sizeof(Sel6Smem<512>) : sizeof(Sel6Smem<2048>);
+  return ((hdr + 15) & ~(size_t)15) + (size_t)(sms ? ((m_max + 3) & ~3) : 0) * 4 + (size_t)2 * W * 4;
+}
+
+template __global__ void select_v6_kernel<512, true>(IndexView, StepView, SelParams);
+template __global__ void select_v6_kernel<512, false>(IndexView, StepView, SelParams);
+template __global__ void select_v6_kernel<2048, false>(IndexView, StepView, SelParams);
+
+}  // namespace wk

@@ -6,6 +6,9 @@
 #include "decode_v3.cu"
 #include "select_v4.cu"
 #include "select_v5.cu"
+#include "select_v6.cu"
+#include "attend_v4.cu"
+#include "score_v4.cu"
 #include "cache.cu"
 #include "metrics.cu"
 #include "abi.cu"

@@ -75,7 +75,7 @@ class WaveLayer:
     def __init__(self, cfg: EngineConfig, U: int, G: int, d: int, *, max_prefill: int,
                  max_decode: int = 1024, store_dtype=torch.bfloat16, device="cuda",
                  blas_threads: int = 1, splits: int | None = None, keep_vs64: bool = False,
-                 with_elist: bool = False):
+                 with_elist: bool = False, score_mode: int | None = None):
         self.cfg = cfg.validate()
         ic = cfg.index
         if d <= 0 or d % 4 or d > 256:
@@ -98,13 +98,27 @@ class WaveLayer:
         k_upd = math.ceil(ic.update_segment / ic.centroid_ratio)
         m_pref = sum(math.ceil(min(ic.segment_size, n_idx - s) / ic.centroid_ratio)
                      for s in range(0, n_idx, ic.segment_size))
-        self.m_cap = max(4, -(-(m_pref + n_upd * k_upd) // 4) * 4)  # multiple of 4 (float4 scans)
+        # multiple of 32: float4 scans, 16-row C16 tiles, 32-bit zone bitmaps
+        self.m_cap = max(32, -(-(m_pref + n_upd * k_upd) // 32) * 32)
         self.s_cap = max(1, n_idx + n_upd * ic.update_segment)
         self.t_cap = ic.sink_tokens + ic.update_segment + ic.local_window + max(0, ic.local_window) + 8
         self.t_cap = max(self.t_cap, min(max_prefill, ic.sink_tokens + ic.local_window) + 8)
         self.r_cap = max(1, min(self.m_cap, round_half_up(ic.retrieval_fraction * self.m_cap) + 2))
         self.e_cap = max(1, min(self.m_cap, round_half_up(ic.estimation_fraction * self.m_cap) + 2))
-        self.S = splits or max(1, min(64, -(-2048 // U)))
+        # fast path (select_v6 / attend_v4 / score_v4): d in {64, 128}
+        self.fast = d in (64, 128)
+        hs = 4 if G <= 4 else 8
+        self.piece_rows = 32 // hs
+        if self.fast:
+            sms = torch.cuda.get_device_properties(self.dev).multi_processor_count
+            per_sm = 2 if (hs == 4 and store_dtype == torch.bfloat16) else 1
+            self.S = splits or max(1, min(per_sm * sms, 4 * U))  # persistent attention grid
+        else:
+            self.S = splits or max(1, min(64, -(-2048 // U)))
+        # 1: fp32 C scan with fp64 accumulation (estimation logits need ~fp32
+        # accuracy); 2: fp16 C16 tensor-core scan (selection exact, estimation
+        # logits approximate -- experimental)
+        self.score_mode = 1 if score_mode is None else int(score_mode)
         dev, f32, i32 = self.dev, torch.float32, torch.int32
         # ---- index arrays ----
         self.store_k = torch.zeros((U, self.s_cap, d), dtype=store_dtype, device=dev)
@@ -118,6 +132,10 @@ class WaveLayer:
         self.VS32 = torch.zeros((U, self.m_cap, d), dtype=f32, device=dev)
         self.VS64 = (torch.zeros((U, self.m_cap, d), dtype=torch.float64, device=dev)
                      if keep_vs64 else None)
+        self.Cmax = torch.zeros(U, dtype=f32, device=dev)
+        use16 = self.fast and self.score_mode == 2
+        self.C16 = torch.zeros((U, self.m_cap, d), dtype=torch.float16, device=dev) if use16 else None
+        self.Cscale = torch.zeros((U, self.m_cap), dtype=f32, device=dev) if use16 else None
         # ---- steady zone ----
         self.st_k = torch.zeros((U, self.t_cap, d), dtype=store_dtype, device=dev)
         self.st_v = torch.zeros((U, self.t_cap, d), dtype=store_dtype, device=dev)
@@ -131,23 +149,36 @@ class WaveLayer:
         self.elist = torch.zeros((U, G, self.e_cap), dtype=i32, device=dev) if with_elist else None
         self.nr = torch.zeros(U, dtype=i32, device=dev)
         self.ne = torch.zeros(U, dtype=i32, device=dev)
-        self.zmask = torch.zeros((U, self.m_cap), dtype=i32, device=dev)
         self.ru_cap = min(self.m_cap, G * self.r_cap)
         self.eu_cap = min(self.m_cap, G * self.e_cap)
         self.ru_ids = torch.zeros((U, self.ru_cap), dtype=i32, device=dev)
         self.ru_mask = torch.zeros((U, self.ru_cap), dtype=torch.uint8, device=dev)
-        self.ru_pre = torch.zeros((U, self.ru_cap + 1), dtype=i32, device=dev)
         self.eu_ids = torch.zeros((U, self.eu_cap), dtype=i32, device=dev)
         self.eu_mask = torch.zeros((U, self.eu_cap), dtype=torch.uint8, device=dev)
         self.cnt = torch.zeros((U, 4), dtype=i32, device=dev)
-        self.rt_cap = self.s_cap
-        self.rtok_row = torch.zeros((U, self.rt_cap), dtype=i32, device=dev)
-        self.rtok_mask = torch.zeros((U, self.rt_cap), dtype=torch.uint8, device=dev)
+        if self.fast:
+            self.zmask = self.ru_pre = self.rtok_row = self.rtok_mask = None
+            self.rt_cap = 0
+            self.w_cap = self.m_cap // 32
+            self.rbits = torch.zeros((U, G, self.w_cap), dtype=i32, device=dev)
+            self.ebits = torch.zeros((U, G, self.w_cap), dtype=i32, device=dev)
+            self.pc_cap = self.s_cap // self.piece_rows + self.ru_cap + 1
+            self.pieces = torch.zeros((U, self.pc_cap, 2), dtype=i32, device=dev)
+            self.woff = torch.zeros(U + 1, dtype=i32, device=dev)
+        else:
+            self.zmask = torch.zeros((U, self.m_cap), dtype=i32, device=dev)
+            self.ru_pre = torch.zeros((U, self.ru_cap + 1), dtype=i32, device=dev)
+            self.rt_cap = self.s_cap
+            self.rtok_row = torch.zeros((U, self.rt_cap), dtype=i32, device=dev)
+            self.rtok_mask = torch.zeros((U, self.rt_cap), dtype=torch.uint8, device=dev)
+            self.w_cap = self.pc_cap = 0
+            self.rbits = self.ebits = self.pieces = self.woff = None
         self.sel_done = torch.zeros(U, dtype=i32, device=dev)
         self.eu_x = torch.zeros((U, self.eu_cap, G), dtype=f32, device=dev)
         self.eu_sz = torch.zeros((U, self.eu_cap), dtype=f32, device=dev)
         self.tail = torch.zeros((U, G, 4), dtype=f32, device=dev)
-        self.part = torch.zeros((U, self.S, G, 3, 2 + d), dtype=f32, device=dev)
+        n_part = (self.S * 8 + U) if self.fast else U * self.S
+        self.part = torch.zeros((n_part, 3, G, (4 + d) if self.fast else (2 + d)), dtype=f32, device=dev)
         self.out = torch.zeros((U, G, d), dtype=f32, device=dev)
         self.logden = torch.zeros((U, G), dtype=f32, device=dev)
         self.cov = torch.zeros((U, G), dtype=f32, device=dev)
@@ -157,11 +188,11 @@ class WaveLayer:
         self._q = None
         self._zp = _lib.ZoneParamsC(G, d, self.blas_threads, ic.retrieval_fraction,
                                     ic.estimation_fraction, int(ic.tail_mode == "denominator_only"),
-                                    int(cfg.denominator_mode == "eq2"))
+                                    int(cfg.denominator_mode == "eq2"), self.score_mode, 0)
         self._ixv = _lib.IndexViewC(
             _ptr(self.store_k), _ptr(self.store_v), _ptr(self.store_tok), _ptr(self.cl_off),
             _ptr(self.cl_size), _ptr(self.C64), _ptr(self.C32), _ptr(self.Cnorm), _ptr(self.VS32),
-            _ptr(self.VS64), self.s_cap, self.m_cap)
+            _ptr(self.VS64), self.s_cap, self.m_cap, _ptr(self.Cmax), _ptr(self.C16), _ptr(self.Cscale))
         self._stv = _lib.SteadyViewC(_ptr(self.st_k), _ptr(self.st_v), _ptr(self.st_tok),
                                      _ptr(self.st_n), _ptr(self.next_tok), self.t_cap)
         self.prefilled = False
@@ -175,7 +206,8 @@ class WaveLayer:
             _ptr(self.tail), _ptr(self.part), _ptr(self.out), _ptr(self.logden), _ptr(self.cov),
             _ptr(self.status), self.r_cap, self.e_cap, self.ru_cap, self.eu_cap,
             _ptr(self.rtok_row), _ptr(self.rtok_mask), _ptr(self.sel_done), self.rt_cap, 0,
-            _ptr(self.eu_x), _ptr(self.eu_sz))
+            _ptr(self.eu_x), _ptr(self.eu_sz), _ptr(self.rbits), _ptr(self.ebits), _ptr(self.pieces),
+            _ptr(self.woff), self.w_cap, self.pc_cap)
 
     # --------------------------------------------------------------- clustering
     def _run_segments(self, segs: list[dict]):
