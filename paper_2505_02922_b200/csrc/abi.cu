@@ -57,11 +57,10 @@ template <typename T, int DPL, int HS, bool FULL>
 __global__ void attend_v4_kernel(IndexView, SteadyView, StepView, AttnParams, const int32_t*, int);
 template <typename T, int DPL, int HS, bool FULL>
 size_t attend_v4_smem();
+__global__ void att4_est_prep_kernel(IndexView, StepView, int, float);
 template <bool FULL, int DL>
 __global__ void att4_merge_kernel(SteadyView, StepView, AttnParams, const int32_t*, int, int, int);
 __global__ void km_pack16_kernel(const SegDesc*, IndexView, int);
-template <int KS, int NT>
-__global__ void score_v4_kernel(IndexView, StepView, int, int);
 // metrics.cu
 template <typename T>
 __global__ void recall_kernel(IndexView, SteadyView, StepView, const int32_t*, int, int, int, int, float*,
@@ -382,9 +381,12 @@ int wk_tripartite_attn(const wk_index_view* ix, const wk_steady_view* st, const 
   p.tail_denominator_only = zp->tail_denominator_only;
   p.denominator_eq2 = zp->denominator_eq2;
   dim3 grid(S, U);
-  if (v6_ok(ix, sv, zp->d))
+  if (v6_ok(ix, sv, zp->d)) {
+    att4_est_prep_kernel<<<dim3((sv->eu_cap + 255) / 256, U), 256, 0, s>>>(*ix, *sv, zp->G, p.inv_sqrt_d);
+    WK_CHECK_LAUNCH();
     return store_bf16 ? dispatch_attend_v4<__nv_bfloat16, false>(*ix, *st, *sv, p, nullptr, U, S, s)
                       : dispatch_attend_v4<float, false>(*ix, *st, *sv, p, nullptr, U, S, s);
+  }
   if (v2_ok(zp->d) && sv->rtok_row && sv->sel_done) {
     const int rc = store_bf16 ? dispatch_attend_v2<__nv_bfloat16, false>(*ix, *st, *sv, p, nullptr, U, S, s)
                               : dispatch_attend_v2<float, false>(*ix, *st, *sv, p, nullptr, U, S, s);

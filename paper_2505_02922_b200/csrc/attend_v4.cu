@@ -289,13 +289,11 @@ __global__ void __launch_bounds__(256, HS == 8 ? 1 : 2) attend_v4_kernel(IndexVi
         bulk_g2s(stage + lane * ROWV, ix.VS32 + ((size_t)u * ix.m_cap + c) * D, (uint32_t)ROWV, bars + sti);
       }
       if (lane == 0 && n < RG) bulk_g2s(stage + n * ROWV, g_zero4, (uint32_t)((RG - n) * ROWV), bars + sti);
-      // lane (row j_own, head h_own): logit sigma * q.C of its row (the ranking
-      // score, attention.py:98-100) and the cluster size as denominator weight
-      const int cj = __shfl_sync(0xffffffffu, c, j_own), mj = __shfl_sync(0xffffffffu, emk, j_own);
-      if (j_own < n) {
-        w = (float)__ldg(ix.cl_size + (size_t)u * ix.m_cap + cj);
-        if (h_own < G && ((mj >> h_own) & 1))
-          x = __ldcg(sv.scores + ((size_t)u * G + h_own) * ix.m_cap + cj) * isd;
+      // lane (row j_own, head h_own): logit sigma * q.C of its row and the
+      // cluster size (att4_est_prep_kernel)
+      if (j_own < n && h_own < G) {
+        x = __ldcg(sv.eu_x + ((size_t)u * sv.eu_cap + e0 + j_own) * G + h_own);
+        w = __ldcg(sv.eu_sz + (size_t)u * sv.eu_cap + e0 + j_own);
       }
       mk = x == -INFINITY ? 0 : allmask;
     }
@@ -431,6 +429,24 @@ __global__ void __launch_bounds__(256, HS == 8 ? 1 : 2) attend_v4_kernel(IndexVi
     }
     flush();
   }
+}
+
+// ---------------------------------------------------------------------------
+// estimation-row inputs of the union estimation list (attention.py:98-104):
+// per row the logit sigma * q.C of each head whose estimation zone holds the
+// cluster (-inf otherwise; reusing the ranking score, engine.py:186-189) and
+// the cluster size.  Grid-wide so attend_v4's chunk metadata is one level of
+// independent loads.
+// ---------------------------------------------------------------------------
+__global__ void att4_est_prep_kernel(IndexView ix, StepView sv, int G, float isd) {
+  const int u = blockIdx.y;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= sv.cnt[u * 4 + 2]) return;
+  const size_t row = (size_t)u * sv.eu_cap + e;
+  const int c = __ldcg(sv.eu_ids + row), mk = __ldcg(sv.eu_mask + row);
+  sv.eu_sz[row] = (float)__ldg(ix.cl_size + (size_t)u * ix.m_cap + c);
+  for (int h = 0; h < G; h++)
+    sv.eu_x[row * G + h] = ((mk >> h) & 1) ? __ldcg(sv.scores + ((size_t)u * G + h) * ix.m_cap + c) * isd : -INFINITY;
 }
 
 // ---------------------------------------------------------------------------
