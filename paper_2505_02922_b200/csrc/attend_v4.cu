@@ -123,7 +123,7 @@ struct Att4Cfg {
   static constexpr int WARPS = 8;
   static constexpr int MAXU = 1024;                // units per launch (smem chunk prefix)
   // per warp: ring + barriers + per-stage lane meta (mask, x, w) + stage tags
-  static constexpr int META = NST * 32 * 12 + NST * 16;
+  static constexpr int META = NST * 32 * 12 + NST * 16 + 32 * 4;  // + p broadcast buffer
   static constexpr size_t SMEM = (size_t)WARPS * NST * SB + (size_t)WARPS * NST * 8 + (size_t)WARPS * META +
                                  (size_t)(MAXU + 1) * 4 + 64;
 };
@@ -162,6 +162,7 @@ __global__ void __launch_bounds__(256, HS == 8 ? 1 : 2) attend_v4_kernel(IndexVi
   int* smask = reinterpret_cast<int*>(meta);
   float* sx = reinterpret_cast<float*>(meta + NST * 32 * 4);
   float* sw = reinterpret_cast<float*>(meta + NST * 32 * 8);
+  float* pbuf = reinterpret_cast<float*>(meta + NST * 32 * 12 + NST * 16);  // [RG][HS] chunk weights
   int4* stag = reinterpret_cast<int4*>(meta + NST * 32 * 12);  // (unit, kind)
   int* woff = reinterpret_cast<int*>(a4s + (size_t)CF::WARPS * NST * SB + (size_t)CF::WARPS * NST * 8 +
                                      (size_t)CF::WARPS * CF::META);
@@ -316,13 +317,20 @@ __global__ void __launch_bounds__(256, HS == 8 ? 1 : 2) attend_v4_kernel(IndexVi
       }
     qu = u;
   };
-  SoftState4<HS> ss;
+  // Lazily rescaled online softmax: per head a reference mref (uniform over
+  // the warp); weights p = exp(x - mref) <= e^10 are accumulated without
+  // rescaling, and the accumulators are rescaled only when some logit exceeds
+  // its head's reference by more than 10 (a warp vote).  Each lane keeps the
+  // denominator partial of its own (row, head) slot; partials are reduced
+  // over the lanes of a head at flush.  The merge is exact for any reference.
+  float mref[HS];
+  float dl;
   float2 acc[HS][DP2];
   auto reset = [&]() {
+    dl = 0.f;
 #pragma unroll
     for (int h = 0; h < HS; h++) {
-      ss.M[h] = -INFINITY;
-      ss.D[h] = 0.f;
+      mref[h] = -INFINITY;
 #pragma unroll
       for (int k = 0; k < DP2; k++) acc[h][k] = make_float2(0.f, 0.f);
     }
@@ -338,13 +346,16 @@ __global__ void __launch_bounds__(256, HS == 8 ? 1 : 2) attend_v4_kernel(IndexVi
         acc[h][k].x += __shfl_xor_sync(0xffffffffu, acc[h][k].x, 16);
         acc[h][k].y += __shfl_xor_sync(0xffffffffu, acc[h][k].y, 16);
       }
+    float dsum = dl;
+#pragma unroll
+    for (int off = HS; off < 32; off <<= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, off);
     const size_t slot = (size_t)(wg + cu);
     if (half == 0) {
 #pragma unroll
       for (int h = 0; h < HS; h++) {
         if (h < G) {
           float* dst = sv.part + ((slot * 3 + ck) * G + h) * (size_t)(4 + D);  // (M, D, -, -, num[D])
-          if (sub == 0) { dst[0] = ss.M[h]; dst[1] = ss.D[h]; }
+          if (sub == h) { dst[0] = mref[h]; dst[1] = dsum; }
 #pragma unroll
           for (int k = 0; k < DP2; k++) *reinterpret_cast<float2*>(dst + 4 + sub * DPL + 2 * k) = acc[h][k];
         }
@@ -355,8 +366,7 @@ __global__ void __launch_bounds__(256, HS == 8 ? 1 : 2) attend_v4_kernel(IndexVi
 
   auto compute = [&](int sti, int kind) {
     const unsigned char* stage = ring + sti * SB;
-    float alpha[HS];
-    float pw;
+    float x, wz;
     if (kind < 2) {
       float v[16];
 #pragma unroll
@@ -372,31 +382,58 @@ __global__ void __launch_bounds__(256, HS == 8 ? 1 : 2) attend_v4_kernel(IndexVi
           v[jj * HS + h] = a2.x + a2.y;
         }
       }
-#pragma unroll
-      for (int i = RH * HS; i < 16; i++) v[i] = 0.f;
-      float xl = att4_treduce16(v);
-      if (!((smask[sti * 32 + lane] >> h_own) & 1)) xl = -INFINITY;
-      pw = att4_softmax<HS>(xl, 1.f, ss, alpha);
+      x = att4_treduce16(v);
+      if (!((smask[sti * 32 + lane] >> h_own) & 1)) x = -INFINITY;
+      wz = 1.f;
     } else {
-      pw = att4_softmax<HS>(sx[sti * 32 + lane], sw[sti * 32 + lane], ss, alpha);
+      x = sx[sti * 32 + lane];
+      wz = sw[sti * 32 + lane];
     }
-    // broadcast p of (row j, head h) from lane (j&1)*16 + (j>>1)*HS + h
+    float mo = mref[0];
 #pragma unroll
-    for (int h = 0; h < HS; h++) {
-      const float2 a = make_float2(alpha[h], alpha[h]);
+    for (int h = 1; h < HS; h++)
+      if (h == h_own) mo = mref[h];
+    if (__any_sync(0xffffffffu, x > mo + 10.f)) {
+      // raise the references of the heads whose chunk max exceeds them
+      float mx = x;
 #pragma unroll
-      for (int k = 0; k < DP2; k++) acc[h][k] = __fmul2_rn(acc[h][k], a);
+      for (int off = HS; off < 32; off <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+#pragma unroll
+      for (int h = 0; h < HS; h++) {
+        const float mh = __shfl_sync(0xffffffffu, mx, h);
+        if (mh > mref[h]) {
+          const float alpha = mref[h] == -INFINITY ? 0.f : __expf(mref[h] - mh);
+          const float2 a2 = make_float2(alpha, alpha);
+#pragma unroll
+          for (int k = 0; k < DP2; k++) acc[h][k] = __fmul2_rn(acc[h][k], a2);
+          if (h == h_own) dl *= alpha;
+          mref[h] = mh;
+        }
+      }
+      mo = mref[0];
+#pragma unroll
+      for (int h = 1; h < HS; h++)
+        if (h == h_own) mo = mref[h];
     }
+    const float pw = x == -INFINITY ? 0.f : __expf(x - mo);
+    dl = fmaf(pw, wz, dl);
+    pbuf[j_own * HS + h_own] = pw;
+    __syncwarp();
 #pragma unroll
     for (int jj = 0; jj < RH; jj++) {
       const int j = half + 2 * jj;
       float2 vf[DP2];
       if (kind < 2) Row4<T, DPL>::ld(stage + RG * ROWT + j * ROWT + sub * DPL * (int)sizeof(T), vf);
       else Row4<float, DPL>::ld(stage + j * ROWV + sub * DPL * 4, vf);
+      float pj[HS];
+#pragma unroll
+      for (int h4 = 0; h4 < HS; h4 += 4) {
+        const float4 p4 = *reinterpret_cast<const float4*>(pbuf + j * HS + h4);
+        pj[h4] = p4.x; pj[h4 + 1] = p4.y; pj[h4 + 2] = p4.z; pj[h4 + 3] = p4.w;
+      }
 #pragma unroll
       for (int h = 0; h < HS; h++) {
-        const float pj = __shfl_sync(0xffffffffu, pw, (lane & 16) + jj * HS + h);
-        const float2 p2 = make_float2(pj, pj);
+        const float2 p2 = make_float2(pj[h], pj[h]);
 #pragma unroll
         for (int k = 0; k < DP2; k++) acc[h][k] = __ffma2_rn(p2, vf[k], acc[h][k]);
       }
