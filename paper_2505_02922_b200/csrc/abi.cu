@@ -178,6 +178,20 @@ static int launch_score_v4(const IndexView& ix, const StepView& sv, int G, int U
   return cudaGetLastError() == cudaSuccess ? 0 : WK_ECUDA;
 }
 
+template <int KG>
+static int launch_score_v5(const IndexView& ix, const StepView& sv, int G, int U, int m_max, cudaStream_t s) {
+  const long long groups = (m_max + 7) / 8;
+  // exactly one wave: 8 CTAs (32 warps) per SM, the same CTA count per unit
+  long long cpu = (148LL * 8) / U;
+  if (cpu < 1) cpu = 1;
+  long long gpw = (groups + cpu * 4 - 1) / (cpu * 4);
+  if (gpw < 1) gpw = 1;
+  cpu = (groups + gpw * 4 - 1) / (gpw * 4);
+  dim3 grid((unsigned)cpu, U);
+  score_v5_kernel<KG><<<grid, 128, 0, s>>>(ix, sv, G, (int)gpw);
+  return cudaGetLastError() == cudaSuccess ? 0 : WK_ECUDA;
+}
+
 static int launch_select_v6(const IndexView& ix, const StepView& sv, const SelParams& p, int U, int m_max,
                             cudaStream_t s) {
   const double r_max = floor(p.retrieval_fraction * (double)m_max + 0.5) + 1;
@@ -308,11 +322,8 @@ int wk_score_topk(const wk_index_view* ix, const wk_step_view* sv, const wk_zone
         else rc = nt == 1 ? launch_score_v4<4, 1>(*ix, *sv, zp->G, U, m_max, s)
                           : launch_score_v4<4, 2>(*ix, *sv, zp->G, U, m_max, s);
       } else {
-        const int hs = head_slots(zp->G);
-        if (zp->d == 128) rc = hs == 4 ? launch_score_v3<4, 4>(*ix, *sv, zp->G, U, m_max, s)
-                                       : launch_score_v3<8, 4>(*ix, *sv, zp->G, U, m_max, s);
-        else rc = hs == 4 ? launch_score_v3<4, 2>(*ix, *sv, zp->G, U, m_max, s)
-                          : launch_score_v3<8, 2>(*ix, *sv, zp->G, U, m_max, s);
+        rc = zp->d == 128 ? launch_score_v5<8>(*ix, *sv, zp->G, U, m_max, s)
+                          : launch_score_v5<4>(*ix, *sv, zp->G, U, m_max, s);
       }
       if (rc) return rc;
     }

@@ -229,41 +229,76 @@ __global__ void __launch_bounds__(256, HS == 8 ? 1 : 2) attend_v4_kernel(IndexVi
   int ic0 = 0, ic1 = 0, ic2 = 0;
   if (ca < cb) att4_counts<RG>(st, sv, n_store, FULL, iu, ic0, ic1, ic2);
 
-  auto issue = [&](int sti, long long ci) {
+  // chunk metadata is loaded one chunk ahead of its bulk-copy issue so the
+  // loads (piece words, estimation inputs) are in flight during a compute
+  int in_st = 0;  // steady rows of the cursor's unit
+  if (ca < cb) in_st = st.n[iu];
+  struct Meta {
+    int h;  // unit (bits 0-19) | kind + 1 (20-21) | n (22-26)
+    int a;  // first row (kinds 0/1) or the lane's estimation cluster (kind 2)
+    int mk; // head mask (kinds 0/1)
+    float x, w;
+  };
+  auto chunk_meta = [&](long long ci) {
+    Meta m{0, 0, 0, -INFINITY, 0.f};
+    if (ci >= cb) return m;
     while (ci >= woff[iu + 1]) {
       iu++;
       att4_counts<RG>(st, sv, n_store, FULL, iu, ic0, ic1, ic2);
+      in_st = st.n[iu];
     }
     int lc = (int)(ci - woff[iu]);
-    int kind;
-    if (lc < ic0) kind = 0;
-    else if (lc < ic0 + ic1) { kind = 1; lc -= ic0; }
-    else { kind = 2; lc -= ic0 + ic1; }
     const int u = iu;
+    int kind, n;
+    if (lc < ic0) {
+      kind = 0;
+      m.a = lc * RG;
+      n = min(RG, in_st - m.a);
+      m.mk = allmask;
+    } else if (lc < ic0 + ic1) {
+      kind = 1;
+      lc -= ic0;
+      if (FULL) {
+        m.a = lc * RG;
+        n = min(RG, n_store[u] - m.a);
+        m.mk = allmask;
+      } else {
+        const int2 pc = __ldcg(reinterpret_cast<const int2*>(sv.pieces) + (size_t)u * sv.pc_cap + lc);
+        m.a = pc.x;
+        n = -1;        // decoded at issue (pc.y in mk)
+        m.mk = pc.y;
+      }
+    } else {
+      kind = 2;
+      lc -= ic0 + ic1;
+      const int e0 = lc * RG;
+      n = min(RG, sv.cnt[u * 4 + 2] - e0);
+      if (lane < n) m.a = __ldcg(sv.eu_ids + (size_t)u * sv.eu_cap + e0 + lane);
+      // lane (row j_own, head h_own): logit sigma * q.C and cluster size
+      // (att4_est_prep_kernel)
+      if (j_own < n && h_own < G) {
+        m.x = __ldcg(sv.eu_x + ((size_t)u * sv.eu_cap + e0 + j_own) * G + h_own);
+        m.w = __ldcg(sv.eu_sz + (size_t)u * sv.eu_cap + e0 + j_own);
+      }
+    }
+    m.h = u | ((kind + 1) << 20) | ((n & 31) << 22);
+    return m;
+  };
+  auto issue = [&](int sti, const Meta& m) {
+    const int u = m.h & 0xfffff, kind = ((m.h >> 20) & 3) - 1;
+    int n = (m.h >> 22) & 31, mk = m.mk;
+    if (kind == 1 && !FULL) { n = m.mk & 0xff; mk = m.mk >> 8; }
     unsigned char* stage = ring + sti * SB;
-    int n = 0, mk = 0;
     float x = -INFINITY, w = 0.f;
     if (kind < 2) {
       const unsigned char* srck;
       const unsigned char* srcv;
       if (kind == 0) {
-        const int r0 = lc * RG;
-        n = min(RG, st.n[u] - r0);
-        mk = allmask;
-        srck = (const unsigned char*)st.k + ((size_t)u * st.t_cap + r0) * ROWT;
-        srcv = (const unsigned char*)st.v + ((size_t)u * st.t_cap + r0) * ROWT;
-      } else if (FULL) {
-        const int r0 = lc * RG;
-        n = min(RG, n_store[u] - r0);
-        mk = allmask;
-        srck = (const unsigned char*)ix.store_k + ((size_t)u * ix.s_cap + r0) * ROWT;
-        srcv = (const unsigned char*)ix.store_v + ((size_t)u * ix.s_cap + r0) * ROWT;
+        srck = (const unsigned char*)st.k + ((size_t)u * st.t_cap + m.a) * ROWT;
+        srcv = (const unsigned char*)st.v + ((size_t)u * st.t_cap + m.a) * ROWT;
       } else {
-        const int2 pc = __ldcg(reinterpret_cast<const int2*>(sv.pieces) + (size_t)u * sv.pc_cap + lc);
-        n = pc.y & 0xff;
-        mk = pc.y >> 8;
-        srck = (const unsigned char*)ix.store_k + ((size_t)u * ix.s_cap + pc.x) * ROWT;
-        srcv = (const unsigned char*)ix.store_v + ((size_t)u * ix.s_cap + pc.x) * ROWT;
+        srck = (const unsigned char*)ix.store_k + ((size_t)u * ix.s_cap + m.a) * ROWT;
+        srcv = (const unsigned char*)ix.store_v + ((size_t)u * ix.s_cap + m.a) * ROWT;
       }
       if (lane == 0) {
         mbar_arrive_expect_tx(bars + sti, (uint32_t)(2 * RG * ROWT));
@@ -278,24 +313,13 @@ __global__ void __launch_bounds__(256, HS == 8 ? 1 : 2) attend_v4_kernel(IndexVi
       x = 0.f;
       w = 1.f;
     } else {
-      const int e0 = lc * RG;
-      const int n_eu = sv.cnt[u * 4 + 2];
-      n = min(RG, n_eu - e0);
       if (lane == 0) mbar_arrive_expect_tx(bars + sti, (uint32_t)(RG * ROWV));
       __syncwarp();
-      int c = 0, emk = 0;
-      if (lane < n) {
-        c = __ldcg(sv.eu_ids + (size_t)u * sv.eu_cap + e0 + lane);
-        emk = __ldcg(sv.eu_mask + (size_t)u * sv.eu_cap + e0 + lane);
-        bulk_g2s(stage + lane * ROWV, ix.VS32 + ((size_t)u * ix.m_cap + c) * D, (uint32_t)ROWV, bars + sti);
-      }
+      if (lane < n)
+        bulk_g2s(stage + lane * ROWV, ix.VS32 + ((size_t)u * ix.m_cap + m.a) * D, (uint32_t)ROWV, bars + sti);
       if (lane == 0 && n < RG) bulk_g2s(stage + n * ROWV, g_zero4, (uint32_t)((RG - n) * ROWV), bars + sti);
-      // lane (row j_own, head h_own): logit sigma * q.C of its row and the
-      // cluster size (att4_est_prep_kernel)
-      if (j_own < n && h_own < G) {
-        x = __ldcg(sv.eu_x + ((size_t)u * sv.eu_cap + e0 + j_own) * G + h_own);
-        w = __ldcg(sv.eu_sz + (size_t)u * sv.eu_cap + e0 + j_own);
-      }
+      x = m.x;
+      w = m.w;
       mk = x == -INFINITY ? 0 : allmask;
     }
     smask[sti * 32 + lane] = mk;
@@ -444,13 +468,15 @@ __global__ void __launch_bounds__(256, HS == 8 ? 1 : 2) attend_v4_kernel(IndexVi
   if (nch > 0) {
 #pragma unroll
     for (int i = 0; i < NST - 1; i++)
-      if (i < nch) issue(i, ca + i);
+      if (i < nch) issue(i, chunk_meta(ca + i));
+    Meta mnext = chunk_meta(ca + NST - 1);
     for (int k = 0; k < nch; k++) {
       const int sti = k % NST;
       if (k + NST - 1 < nch) {
         fence_proxy_async();
         __syncwarp();
-        issue((k + NST - 1) % NST, ca + k + NST - 1);
+        issue((k + NST - 1) % NST, mnext);
+        mnext = chunk_meta(ca + k + NST);
       }
       __syncwarp();
       const int4 tg = stag[sti];
