@@ -160,6 +160,15 @@ static int dispatch_attend_v2(const IndexView& ix, const SteadyView& st, const S
 }
 
 // ---- v6 pipeline: score_v4 (tensor cores) | score_v3, select_v6, attend_v4 ----
+static int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+      n = 148;
+  }
+  return n;
+}
 static int g_sel_prof = 0;
 extern "C" int wk_debug_select_prof(int on) { g_sel_prof = on; return 0; }
 static bool v6_ok(const wk_index_view* ix, const wk_step_view* sv, int d) {
@@ -182,7 +191,7 @@ template <int KG>
 static int launch_score_v5(const IndexView& ix, const StepView& sv, int G, int U, int m_max, cudaStream_t s) {
   const long long groups = (m_max + 7) / 8;
   // exactly one wave: 8 CTAs (32 warps) per SM, the same CTA count per unit
-  long long cpu = (148LL * 8) / U;
+  long long cpu = ((long long)sm_count() * 8) / U;
   if (cpu < 1) cpu = 1;
   long long gpw = (groups + cpu * 4 - 1) / (cpu * 4);
   if (gpw < 1) gpw = 1;

@@ -534,60 +534,91 @@ __global__ void __launch_bounds__(128) att4_merge_kernel(SteadyView st, StepView
   }
   const long long ub = sv.woff[u];
   const long long kb[4] = {ub, ub + c0, ub + c0 + c1, ub + c0 + c1 + c2};
-  double kM[3], kD[3];
-  float num[3][DL];  // DL = d / 32 dims per lane
+  // the partials of all three kinds form one flat item list (kind, warp) so
+  // every global load of the merge is issued lane-parallel / unrolled
+  int nk[3], wk0[3];
 #pragma unroll
   for (int k = 0; k < 3; k++) {
-    kM[k] = -INFINITY;
-    kD[k] = 0.0;
-#pragma unroll
-    for (int i = 0; i < DL; i++) num[k][i] = 0.f;
-    if (kb[k + 1] <= kb[k]) continue;
-    const int w0 = att4_warp_of(kb[k], N, Wtot), w1 = att4_warp_of(kb[k + 1] - 1, N, Wtot);
-    // pass 1 (lane-parallel over partials): max
-    float Mx = -INFINITY;
-    for (int w = w0 + lane; w <= w1; w += 32) {
-      const long long a = N * w / Wtot, b = N * (w + 1) / Wtot;
-      if (a >= b) continue;  // empty warp range: no partial written
-      const float* src = sv.part + (((size_t)(w + u) * 3 + k) * G + g) * (size_t)D2;
-      if (__ldcg(src + 1) > 0.f) Mx = fmaxf(Mx, __ldcg(src));
+    nk[k] = 0;
+    wk0[k] = 0;
+    if (kb[k + 1] > kb[k]) {
+      wk0[k] = att4_warp_of(kb[k], N, Wtot);
+      nk[k] = att4_warp_of(kb[k + 1] - 1, N, Wtot) - wk0[k] + 1;
     }
-    Mx = warp_max(Mx);
-    if (Mx == -INFINITY) continue;
-    // pass 2: per-partial scale (lane-parallel), then independent numerator loads
-    float Dn = 0.f;
-    for (int w32 = w0; w32 <= w1; w32 += 32) {
-      const int w = w32 + lane;
-      float sc = 0.f;
-      if (w <= w1) {
-        const long long a = N * w / Wtot, b = N * (w + 1) / Wtot;
-        if (a < b) {
-          const float* src = sv.part + (((size_t)(w + u) * 3 + k) * G + g) * (size_t)D2;
-          const float dw = __ldcg(src + 1);
-          if (dw > 0.f) { sc = __expf(__ldcg(src) - Mx); Dn += dw * sc; }
-        }
-      }
-      const int nw = min(32, w1 - w32 + 1);
-      // partials of empty-range warps may hold stale bits: scale 0 and select
-#pragma unroll 8
-      for (int i = 0; i < nw; i++) {
-        const float sw = __shfl_sync(0xffffffffu, sc, i);
-        const float* src = sv.part + (((size_t)(w32 + i + u) * 3 + k) * G + g) * (size_t)D2 + 4 + lane * DL;
-        float v[DL];
-        if (DL == 4) {
-          const float4 x = __ldcg(reinterpret_cast<const float4*>(src));
-          v[0] = x.x; v[1] = x.y; v[2 % DL] = x.z; v[3 % DL] = x.w;
-        } else {
-          const float2 x = __ldcg(reinterpret_cast<const float2*>(src));
-          v[0] = x.x; v[1 % DL] = x.y;
-        }
-#pragma unroll
-        for (int j = 0; j < DL; j++) num[k][j] += sw != 0.f ? v[j] * sw : 0.f;
-      }
-    }
-    kM[k] = Mx;
-    kD[k] = warp_sum(Dn);
   }
+  const int S = nk[0] + nk[1] + nk[2];
+  auto item = [&](int i, int& k, int& w) {
+    k = i < nk[0] ? 0 : (i < nk[0] + nk[1] ? 1 : 2);
+    w = wk0[k] + i - (k == 0 ? 0 : (k == 1 ? nk[0] : nk[0] + nk[1]));
+  };
+  auto rec = [&](int k, int w) { return sv.part + (((size_t)(w + u) * 3 + k) * G + g) * (size_t)D2; };
+  auto live_w = [&](int w) { return N * w / Wtot < N * (w + 1) / Wtot; };  // empty ranges wrote nothing
+  // pass 1: per-kind max
+  float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY;
+  for (int i = lane; i < S; i += 32) {
+    int k, w;
+    item(i, k, w);
+    if (!live_w(w)) continue;
+    const float* r = rec(k, w);
+    if (__ldcg(r + 1) > 0.f) {
+      const float M = __ldcg(r);
+      if (k == 0) m0 = fmaxf(m0, M); else if (k == 1) m1 = fmaxf(m1, M); else m2 = fmaxf(m2, M);
+    }
+  }
+  m0 = warp_max(m0); m1 = warp_max(m1); m2 = warp_max(m2);
+  // pass 2: scales (lane-parallel), numerators (independent unrolled loads)
+  float d0 = 0.f, d1 = 0.f, d2 = 0.f;
+  float n0[DL], n1[DL], n2[DL];
+#pragma unroll
+  for (int j = 0; j < DL; j++) n0[j] = n1[j] = n2[j] = 0.f;
+  for (int i0 = 0; i0 < S; i0 += 32) {
+    float sc = 0.f;
+    {
+      const int i = i0 + lane;
+      if (i < S) {
+        int k, w;
+        item(i, k, w);
+        if (live_w(w)) {
+          const float* r = rec(k, w);
+          const float dw = __ldcg(r + 1);
+          const float mk = k == 0 ? m0 : (k == 1 ? m1 : m2);
+          if (dw > 0.f) {
+            sc = __expf(__ldcg(r) - mk);
+            if (k == 0) d0 += dw * sc; else if (k == 1) d1 += dw * sc; else d2 += dw * sc;
+          }
+        }
+      }
+    }
+    const int nw = min(32, S - i0);
+#pragma unroll 8
+    for (int j = 0; j < nw; j++) {
+      const float sw = __shfl_sync(0xffffffffu, sc, j);
+      int k, w;
+      item(i0 + j, k, w);
+      const float* src = rec(k, w) + 4 + lane * DL;
+      float v[DL];
+      if (DL == 4) {
+        const float4 x = __ldcg(reinterpret_cast<const float4*>(src));
+        v[0] = x.x; v[1] = x.y; v[2 % DL] = x.z; v[3 % DL] = x.w;
+      } else {
+        const float2 x = __ldcg(reinterpret_cast<const float2*>(src));
+        v[0] = x.x; v[1 % DL] = x.y;
+      }
+      // partials of empty-range warps may hold stale bits: weight 0 selects them out
+#pragma unroll
+      for (int jj = 0; jj < DL; jj++) {
+        const float add = sw != 0.f ? v[jj] * sw : 0.f;
+        n0[jj] += k == 0 ? add : 0.f;
+        n1[jj] += k == 1 ? add : 0.f;
+        n2[jj] += k == 2 ? add : 0.f;
+      }
+    }
+  }
+  double kM[3] = {m0, m1, m2};
+  double kD[3] = {warp_sum(d0), warp_sum(d1), warp_sum(d2)};
+  float num[3][DL];
+#pragma unroll
+  for (int j = 0; j < DL; j++) { num[0][j] = n0[j]; num[1][j] = n1[j]; num[2][j] = n2[j]; }
   const float zero4[4] = {-INFINITY, 0.f, -INFINITY, 0.f};
   const float* tl = (!FULL && sv.tail) ? sv.tail + ((size_t)u * G + g) * 4 : zero4;
   const bool live0 = kD[0] > 0, live1 = kD[1] > 0, live2 = kD[2] > 0;

@@ -47,7 +47,7 @@ struct Sel6Smem {
   unsigned char be_sel[S6_BAND];
   float red[3][S6_NW];
   int wsum[4][S6_NW];
-  int ncand, nband_r, nband_e, n_in_e, nx, ovf, last, b1, b2;
+  int ncand, n_in_r, nband_e, n_in_e, nx, ovf, last, b1, b2;
   int base[4];
   float fred[3];
 };
@@ -153,7 +153,7 @@ WK_DEVINL double s6_exact_quad(const double* __restrict__ row, const float* __re
   double acc = 0.0;
   if (act) {
     if (cls == 0) {
-#pragma unroll 8
+#pragma unroll 16
       for (int t = j; t < d; t += 4) acc = __fma_rn(__ldcg(row + t), (double)__ldg(q + t), acc);
     } else if (cls == 1) {
       if (j < 2) {
@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
     float qq = 0.f;
     for (int i = t; i < d; i += T) { const float qi = q[i]; qq = fmaf(qi, qi, qq); }
     for (int b = t; b < S6_NB; b += T) sm.x.hist[b] = 0;
-    if (t == 0) { sm.ncand = sm.nband_r = sm.nband_e = sm.n_in_e = sm.nx = sm.ovf = 0; sm.b1 = sm.b2 = -1; }
+    if (t == 0) { sm.ncand = sm.n_in_r = sm.nband_e = sm.n_in_e = sm.nx = sm.ovf = 0; sm.b1 = sm.b2 = -1; }
     float nmn = -mn;
     s6_reduce3(qq, mx, nmn, sm);
     mn = -nmn;
@@ -389,27 +389,39 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
   S6_MARK(3);
   if (ok) {
     // ---- pass D: candidates for R (certain-in + band), band around tau_e,
-    //      certain members of the top r+e (bitmap, one ballot per word) ----
+    //      certain members of the top r+e (bitmap, one ballot per word).
+    //      Float thresholds rounded outward (certain sets only shrink,
+    //      candidate sets only grow); counts kept in registers.  Band rows'
+    //      fp64 centroid rows are prefetched to L2 for the exact round. ----
+    const float fhr = __double2float_ru(hr), flr = __double2float_rd(lr);
+    const float fhe = e > 0 ? __double2float_ru(he) : INFINITY, fle = e > 0 ? __double2float_rd(le) : INFINITY;
+    int cnt_in_r = 0, cnt_in_e = 0;
+#pragma unroll 2
     for (int base = 0; base < m; base += T) {
       const int c = base + t;
-      const bool act = c < m;
-      const float v = act ? S_(c) : 0.f;
-      const double dv = (double)v;
-      const bool in_r = act && dv > hr;
-      const bool bd_r = act && !in_r && dv >= lr;
-      s6_append(in_r || bd_r, s6_key(v, c), sm.y.cand, &sm.ncand, CAND, &sm.ovf);
-      const unsigned mbr = __ballot_sync(0xffffffffu, bd_r);
-      if (lane == 0 && mbr) atomicAdd(&sm.nband_r, __popc(mbr));
-      if (e > 0) {
-        const bool in_e = act && dv > he;
-        const bool bd_e = act && !in_e && dv >= le;
-        const unsigned mie = __ballot_sync(0xffffffffu, in_e);
-        if (lane == 0 && mie) { tre[c >> 5] = mie; atomicAdd(&sm.n_in_e, __popc(mie)); }
-        s6_append(bd_e, c, sm.be_id, &sm.nband_e, S6_BAND, &sm.ovf);
+      const float v = c < m ? S_(c) : -INFINITY;
+      const bool cand = v >= flr;
+      const bool in_r = v > fhr;
+      const bool in_e = v > fhe;
+      const bool bd_e = !in_e && v >= fle;
+      const unsigned mir = __ballot_sync(0xffffffffu, in_r);
+      const unsigned mie = __ballot_sync(0xffffffffu, in_e);
+      cnt_in_r += __popc(mir);
+      cnt_in_e += __popc(mie);
+      if (lane == 0 && c < m) tre[c >> 5] = mie;
+      if ((cand && !in_r) || bd_e) {
+        const char* row = reinterpret_cast<const char*>(C64 + (size_t)c * d);
+        for (int o = 0; o < d * 8; o += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(row + o));
       }
+      s6_append(cand, s6_key(v, c), sm.y.cand, &sm.ncand, CAND, &sm.ovf);
+      s6_append(bd_e, c, sm.be_id, &sm.nband_e, S6_BAND, &sm.ovf);
+    }
+    if (lane == 0) {
+      atomicAdd(&sm.n_in_r, cnt_in_r);
+      atomicAdd(&sm.n_in_e, cnt_in_e);
     }
     __syncthreads();
-    const int nc = sm.ncand, nbr = sm.nband_r, nin_r = nc - nbr, nbe = sm.nband_e, nin_e = sm.n_in_e;
+    const int nc = sm.ncand, nin_r = sm.n_in_r, nbe = sm.nband_e, nin_e = e > 0 ? sm.n_in_e : 0;
     if (sm.ovf || nin_r > r || nc < r || (e > 0 && (nin_e > r + e || nin_e + nbe < r + e))) {
       ok = false;
     } else {
