@@ -26,6 +26,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 HQ, HKV, D = 32, 8, 128
+METRIC = "decode tokens/sec at 120K ctx (device-timed) and % HBM roofline vs full attn"
+# kernels per layer and step: append, score_v5, select_v6, est_prep, attend_v4, merge
+LAUNCHES_PER_LAYER = 6
 
 
 def parse():
@@ -42,6 +45,7 @@ def parse():
     ap.add_argument("--cpu-steps", type=int, default=8)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-flashinfer", action="store_true")
     return ap.parse_args()
 
 
@@ -131,6 +135,40 @@ def gen_queries(torch, centers, G, steps, seed, persistence=0.9, shared=0.25, pe
     return q.bfloat16().float().contiguous()
 
 
+# ------------------------------------------- library full-attention comparator
+def flashinfer_decode(torch, B, HQ, HKV, D, ctx, layers, reps, log, page=64):
+    """Full-attention decode through flashinfer's trtllm-gen sm100a kernels
+    (library code; SURVEY 8(d) names it as the comparator): same batch, heads,
+    context, bf16 paged KV (one layer's KV, >> L2, reused for every layer)."""
+    try:
+        from flashinfer.decode import trtllm_batch_decode_with_kv_cache
+        dev = torch.device("cuda")
+        pages_per = ctx // page
+        kv = torch.empty((B * pages_per, 2, HKV, page, D), device=dev, dtype=torch.bfloat16).normal_()
+        bt = torch.arange(B * pages_per, device=dev, dtype=torch.int32).view(B, pages_per)
+        sl = torch.full((B,), ctx, device=dev, dtype=torch.int32)
+        q = torch.randn((B, HQ, D), device=dev, dtype=torch.bfloat16)
+        ws = torch.zeros(256 << 20, device=dev, dtype=torch.uint8)
+        out = trtllm_batch_decode_with_kv_cache(q, kv, ws, bt, sl, ctx, bmm1_scale=D ** -0.5)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps * layers):
+            trtllm_batch_decode_with_kv_cache(q, kv, ws, bt, sl, ctx, bmm1_scale=D ** -0.5, out=out)
+        e1.record()
+        torch.cuda.synchronize()
+        ms_layer = e0.elapsed_time(e1) / (reps * layers)
+        nbytes = kv.numel() * 2
+        del kv, ws
+        torch.cuda.empty_cache()
+        return {"impl": "flashinfer trtllm_batch_decode_with_kv_cache (trtllm-gen sm100a, library)",
+                "ms_per_step": ms_layer * layers, "bytes_per_layer": nbytes,
+                "hbm_gbs": nbytes / (ms_layer / 1e3) / 1e9}
+    except Exception as exc:  # library comparator is optional
+        log(f"flashinfer comparator unavailable: {exc!r}")
+        return None
+
+
 # ------------------------------------------------------------- CPU reference
 def cpu_sample(ctx, steps, seed=0):
     """One q-head unit of the workload through the C oracle (tierkv's
@@ -183,7 +221,7 @@ def run_reference(a):
         wall = time.perf_counter() - t0
     unit_steps_per_s = sum(1.0 / p for p in per)
     tok_s = unit_steps_per_s / (HQ * a.layers)
-    line = {"impl": "reference", "metric": "decode tokens/sec at 120K ctx (device-timed)",
+    line = {"impl": "reference", "metric": METRIC,
             "value": tok_s, "unit": "tokens/s", "n_gpus": a.gpus, "steps": steps,
             "warmup": a.warmup, "ms_per_step": a.batch / tok_s * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -198,6 +236,10 @@ def run_reference(a):
 
 
 # ------------------------------------------------------------------- GPU arm
+def _ptr(t):
+    return t.data_ptr()
+
+
 def main():
     a = parse()
     if a.impl == "reference":
@@ -216,7 +258,7 @@ def main():
     G = HQ // HKV
     U = a.batch * HKV  # per-rank units (weak scaling: each rank serves `batch` requests)
     n_bufs = min(a.layer_bufs, a.layers)
-    total_steps = a.warmup + a.steps
+    total_steps = a.warmup + a.steps + 2  # + the per-op breakdown step
     log = lambda *x: print(*x, file=sys.stderr, flush=True) if rank == 0 else None
     cfg = EngineConfig()
     layers, qpool, kpool = [], [], []
@@ -276,43 +318,68 @@ def main():
         lay.check_status("bench")
     value = a.batch * world / (ms / 1e3)
 
-    # ---- roofline of the dominant op (tripartite attention) ----
-    lay = layers[0]
-    cnt = lay.cnt.cpu()
-    n_st = lay.st_n.cpu()
-    m = torch.tensor([s.m for s in lay.units])
-    elem = 2
-    attn_bytes = int(((cnt[:, 1] + n_st).sum() * 2 * D * elem) + cnt[:, 2].sum() * (D * 4 + 4))
-    score_bytes = int(m.sum() * D * 4)
-    # per-kernel events: re-run one step with events around each op
-    s_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(3)]
+    # ---- per-op device time inside one more step (events on the launch stream) ----
     import ctypes
     from paper_2505_02922_b200 import _lib
     from paper_2505_02922_b200.wave import _stream
-    q = qpool[0][0]
-    L = lay.L
-    sv = lay._step_view(q)
-    stream = ctypes.c_void_p(_stream())
-    reps = 5
-    t_score = t_attn = 0.0
-    for r in range(reps):
-        s_ev[0][0].record()
-        _lib.check(L.wk_score_topk(ctypes.byref(lay._ixv), ctypes.byref(sv), ctypes.byref(lay._zp),
-                                   lay.U, int(m.max()), stream), "score")
-        s_ev[0][1].record()
-        s_ev[1][0].record()
-        _lib.check(L.wk_tripartite_attn(ctypes.byref(lay._ixv), ctypes.byref(lay._stv), ctypes.byref(sv),
-                                        ctypes.byref(lay._zp), lay.U, lay.S, lay.store_bf16, stream), "attn")
-        s_ev[1][1].record()
-        torch.cuda.synchronize()
-        t_score += s_ev[0][0].elapsed_time(s_ev[0][1]) / reps
-        t_attn += s_ev[1][0].elapsed_time(s_ev[1][1]) / reps
-    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
-        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
-    peak = float(peaks.get("hbm_gbs", 6650.0))
-    achieved = attn_bytes / (t_attn / 1e3) / 1e9
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(a.layers)]
+    torch.cuda.synchronize()
+    for l in range(a.layers):
+        b_ = l % n_bufs
+        lay = layers[b_]
+        j = use[b_]
+        use[b_] += 1
+        q = qpool[b_][j]
+        stream = ctypes.c_void_p(_stream())
+        ev[l][0].record()
+        _lib.check(lay.L.wk_append_tokens(ctypes.byref(lay._stv), _ptr(kpool[b_][j, 0]), _ptr(kpool[b_][j, 1]),
+                                          lay.U, lay.d, lay.store_bf16, stream), "append")
+        ev[l][1].record()
+        sv = lay._step_view(q)
+        _lib.check(lay.L.wk_score_topk(ctypes.byref(lay._ixv), ctypes.byref(sv), ctypes.byref(lay._zp), lay.U,
+                                       max(s.m for s in lay.units), stream), "score_topk")
+        ev[l][2].record()
+        _lib.check(lay.L.wk_tripartite_attn(ctypes.byref(lay._ixv), ctypes.byref(lay._stv), ctypes.byref(sv),
+                                            ctypes.byref(lay._zp), lay.U, lay.S, lay.store_bf16, stream), "attn")
+        ev[l][3].record()
+        for s_ in lay.units:
+            s_.total += 1
+            s_.n_steady += 1
+    torch.cuda.synchronize()
+    t_app = sum(ev[l][0].elapsed_time(ev[l][1]) for l in range(a.layers)) / a.layers
+    t_score = sum(ev[l][1].elapsed_time(ev[l][2]) for l in range(a.layers)) / a.layers
+    t_attn = sum(ev[l][2].elapsed_time(ev[l][3]) for l in range(a.layers)) / a.layers
 
-    # ---- full-attention comparator (same buffers, same batch) ----
+    # ---- algorithmic bytes: per layer, from the live zone counts ----
+    elem = 2
+    zs = {"n_steady": 0.0, "n_retrieved_tokens": 0.0, "n_retrieval_pieces": 0.0, "n_estimation_rows": 0.0,
+          "m": 0.0}
+    attn_bytes_l, score_bytes_l = [], []
+    for lay in layers:
+        cnt = lay.cnt.cpu().double()
+        n_st = lay.st_n.cpu().double()
+        mm = torch.tensor([s_.m for s_ in lay.units], dtype=torch.float64)
+        attn_bytes_l.append(float((cnt[:, 1] + n_st).sum() * 2 * D * elem + cnt[:, 2].sum() * (D * 4 + 4)))
+        score_bytes_l.append(float(mm.sum() * D * 4))
+        zs["n_steady"] += float(n_st.mean()) / n_bufs
+        zs["n_retrieved_tokens"] += float(cnt[:, 1].mean()) / n_bufs
+        zs["n_retrieval_pieces"] += float(cnt[:, 3].mean()) / n_bufs
+        zs["n_estimation_rows"] += float(cnt[:, 2].mean()) / n_bufs
+        zs["m"] += float(mm.mean()) / n_bufs
+    attn_bytes = sum(attn_bytes_l) / n_bufs
+    score_bytes = sum(score_bytes_l) / n_bufs
+    step_bytes = (attn_bytes + score_bytes) * a.layers
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "B200_PROFILING.md fallback"
+    achieved = attn_bytes / (t_attn / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get("wk_tripartite_attn")
+
+    # ---- full-attention comparators (same batch, heads, context, bf16 KV) ----
     fa_ms = None
     if a.fa_steps > 0:
         outs = torch.empty((U, G, D), device=dev)
@@ -327,7 +394,10 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         fa_ms = e0.elapsed_time(e1) / a.fa_steps
-    fa_bytes_layer = sum(s.store_fill + s.n_steady for s in layers[0].units) * 2 * D * elem
+    fa_bytes_layer = sum(s_.store_fill + s_.n_steady for s_ in layers[0].units) * 2 * D * elem
+    fi = None
+    if a.fa_steps > 0 and not a.no_flashinfer:
+        fi = flashinfer_decode(torch, a.batch, HQ, HKV, D, a.ctx, a.layers, max(3, a.fa_steps), log)
 
     # ---- e2e: host buffers, copies inside the timed region ----
     e2e = None
@@ -367,30 +437,42 @@ def main():
                          f"extrapolated x{HQ} heads x{a.layers} layers"}
 
     if rank == 0:
+        fa_block = {"impl": "wk_full_attn (this repo, same kernel family reading every token)",
+                    "ms_per_step": fa_ms,
+                    "value": (a.batch * world / (fa_ms / 1e3)) if fa_ms else None,
+                    "speedup_wave_vs_full": (fa_ms / ms) if fa_ms else None,
+                    "bytes_per_layer": fa_bytes_layer,
+                    "hbm_gbs": (fa_bytes_layer * a.layers / (fa_ms / 1e3) / 1e9) if fa_ms else None}
+        if fi:
+            fi["speedup_wave_vs_full"] = fi["ms_per_step"] / ms
+            fi["value"] = a.batch * world / (fi["ms_per_step"] / 1e3)
         line = {
-            "metric": "decode tokens/sec at 120K ctx (device-timed)",
+            "metric": METRIC,
             "value": value, "unit": "tokens/s", "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "bf16 KV / fp32 accumulate", "data": "synthetic",
+            "vs_baseline": None, "dtype": "bf16 KV / fp32 accumulate (fp64 scoring)", "data": "synthetic",
             "config": {"workload": "llama3-8b-shape 32-layer decode, 120K ctx, batch 16 (configs[1])",
                        "batch_per_gpu": a.batch, "ctx": a.ctx, "layers": a.layers,
                        "layer_buffers": n_bufs, "heads": f"{HQ}q/{HKV}kv", "d": D,
                        "l2": "inputs larger than L2 (each layer buffer >> 126 MB, cycled)"},
-            "full_attention": {"ms_per_step": fa_ms,
-                               "value": (a.batch * world / (fa_ms / 1e3)) if fa_ms else None,
-                               "speedup_wave_vs_full": (fa_ms / ms) if fa_ms else None,
-                               "bytes_per_layer": fa_bytes_layer,
-                               "hbm_gbs": (fa_bytes_layer * a.layers / (fa_ms / 1e3) / 1e9) if fa_ms else None},
+            "full_attention": fi or fa_block,
+            "full_attention_own_kernel": fa_block,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
-                         "kernel": "wk_tripartite_attn (attend+merge)", "bytes_per_launch": attn_bytes,
-                         "ms_per_launch": t_attn},
-            "breakdown_ms_per_layer": {"score_topk": t_score, "tripartite_attn": t_attn},
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "kernel": "wk_tripartite_attn (est-prep + attend_v4 + merge)",
+                         "bytes_per_launch": attn_bytes, "ms_per_launch": t_attn},
+            "step_roofline": {"bytes_per_step": step_bytes, "achieved": step_bytes / (ms / 1e3) / 1e9,
+                              "frac": step_bytes / (ms / 1e3) / 1e9 / peak,
+                              "what": "HBM bytes touched per decode step (C32 scan + steady/retrieved K,V "
+                                      "+ estimation value sums) / device step time"},
+            "breakdown_ms_per_layer": {"append": t_app, "score_topk": t_score, "tripartite_attn": t_attn,
+                                       "score_scan_gbs": score_bytes / (t_score / 1e3) / 1e9},
+            "zone_stats_per_unit": zs,
             "build_s": t_build,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clk.summary(),
-            "gpu_launches": a.steps * a.layers * 6,
+            "gpu_launches": a.steps * a.layers * LAUNCHES_PER_LAYER,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
