@@ -26,6 +26,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 HQ, HKV, D = 32, 8, 128
+# head shapes of the BASELINE configs (configs[1] Llama-3-8B, configs[4] Qwen2.5-7B)
+MODELS = {"llama3-8b": (32, 8, 128, 32), "qwen2.5-7b": (28, 4, 128, 28)}
 METRIC = "decode tokens/sec at 120K ctx (device-timed) and % HBM roofline vs full attn"
 # kernels per layer and step: append, score_v5, select_v6, est_prep, attend_v4, merge
 LAUNCHES_PER_LAYER = 6
@@ -34,12 +36,13 @@ LAUNCHES_PER_LAYER = 6
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--model", default="llama3-8b", choices=sorted(MODELS))
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="wave", choices=["wave", "reference"])
     ap.add_argument("--batch", type=int, default=16)
     ap.add_argument("--ctx", type=int, default=122880)
-    ap.add_argument("--layers", type=int, default=32)
+    ap.add_argument("--layers", type=int, default=0, help="0: the model's layer count")
     ap.add_argument("--layer-bufs", type=int, default=4)
     ap.add_argument("--fa-steps", type=int, default=3)
     ap.add_argument("--cpu-steps", type=int, default=8)
@@ -225,7 +228,7 @@ def run_reference(a):
             "value": tok_s, "unit": "tokens/s", "n_gpus": a.gpus, "steps": steps,
             "warmup": a.warmup, "ms_per_step": a.batch / tok_s * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "llama3-8b-shape 32-layer decode, 120K ctx, batch 16",
+            "config": {"workload": f"{a.model}-shape {a.layers}-layer decode, {a.ctx // 1024}K ctx, batch {a.batch}",
                        "batch": a.batch, "ctx": a.ctx, "layers": a.layers},
             "cpu_baseline": {"value": tok_s, "unit": "tokens/s", "cores": cores, "kind": "port",
                              "sample": f"{cores} x one q-head unit at {a.ctx} ctx, {steps} decode "
@@ -241,7 +244,11 @@ def _ptr(t):
 
 
 def main():
+    global HQ, HKV, D
     a = parse()
+    HQ, HKV, D, n_layers = MODELS[a.model]
+    if a.layers <= 0:
+        a.layers = n_layers
     if a.impl == "reference":
         return run_reference(a)
     import torch
@@ -280,6 +287,8 @@ def main():
         log(f"layer buffer {li}: m={lay.units[0].m} build {t_build:.1f}s")
     use = [0] * n_bufs
 
+    gather_buf = torch.empty((world, U, G, D), device=dev) if world > 1 else None
+
     def wave_step(step_i, timers=None):
         for l in range(a.layers):
             b = l % n_bufs
@@ -294,6 +303,10 @@ def main():
             for s in lay.units:
                 s.total += 1
                 s.n_steady += 1
+        if world > 1:
+            # the path's one collective: final gather of the attention outputs
+            # (SURVEY 8(e)); NCCL over NVLink, ordered on the current stream
+            dist.all_gather_into_tensor(gather_buf, layers[(a.layers - 1) % n_bufs].out)
 
     # ---- warmup + timed wave steps ----
     for i in range(a.warmup):
@@ -451,7 +464,9 @@ def main():
             "value": value, "unit": "tokens/s", "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16 KV / fp32 accumulate (fp64 scoring)", "data": "synthetic",
-            "config": {"workload": "llama3-8b-shape 32-layer decode, 120K ctx, batch 16 (configs[1])",
+            "config": {"workload": (f"{a.model}-shape {a.layers}-layer decode, {a.ctx // 1024}K ctx, batch {a.batch}"
+                                    + (" (configs[1])" if a.model == "llama3-8b" else " (configs[4])")),
+                       "model_shape": a.model,
                        "batch_per_gpu": a.batch, "ctx": a.ctx, "layers": a.layers,
                        "layer_buffers": n_bufs, "heads": f"{HQ}q/{HKV}kv", "d": D,
                        "l2": "inputs larger than L2 (each layer buffer >> 126 MB, cycled)"},
