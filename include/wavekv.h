@@ -115,6 +115,13 @@ typedef struct wk_step_view {
   int32_t* pieces;    /* [U, pc_cap, 2] retrieval runs: (store row, n | mask<<8) */
   int32_t* woff;      /* [U + 1] attention chunk prefix (scratch)               */
   int32_t w_cap, pc_cap;
+  /* offload path (host store + HBM slot arena); pstride 2 = in-HBM store */
+  void* arena_k;      /* [U, arena_rows, d] cached blocks (block_tokens rows/slot) */
+  void* arena_v;
+  const int32_t* slot_ids; /* [U, slot_cap] physical slot of each cluster block  */
+  const int32_t* slot_off; /* [U, m_cap] first block of each cluster            */
+  int64_t arena_rows, slot_cap;
+  int32_t block_tokens, pstride; /* pieces: 2 ints (in HBM) or 4 (offload)      */
 } wk_step_view;
 
 typedef struct wk_zone_params {
@@ -159,6 +166,23 @@ typedef struct wk_cache_view {
   int64_t m_cap, slot_cap, heap_cap, ids_cap, ev_cap;
   int32_t block_bytes, token_bytes;
 } wk_cache_view;
+
+/* Offload block cache (cache_v2.cu): per kv-head unit, the union access
+ * stream of the GQA group, tierkv BlockCache lookup/assemble/commit
+ * (block_cache.py:79-213) in parallel, then the attention pieces (hits from
+ * the slot arena, misses from the pinned host store, admitted misses written
+ * through by the attention kernel). */
+typedef struct wk_cache2_view {
+  int32_t* nblk; int32_t* slot_off; int32_t* slot_ids; uint8_t* cached;
+  int32_t* touched; int32_t* first; int32_t* lru; int32_t* lru_tmp; int32_t* lru_n;
+  int32_t* freel; int32_t* free_n; int32_t* next_slot; int64_t* capacity; int64_t* occupied;
+  int64_t* counters;  /* [U, 8] hits, misses, bytes_slow_to_fast, bytes_fast_internal,
+                         store bytes_read_total, evictions, admissions, rejections */
+  int32_t* ids; int32_t* n_ids; uint8_t* snapshot; int32_t* scratch;
+  const int32_t* m_live;
+  int64_t m_cap, slot_cap, lru_cap, ids_cap;
+  int32_t block_bytes, token_bytes, block_tokens, pad_;
+} wk_cache2_view;
 
 int wk_version(void);
 
@@ -215,6 +239,15 @@ int wk_recall_at_k(const wk_index_view* ix, const wk_steady_view* st, const wk_s
                    const int32_t* n_store, int U, int G, int d, int metrics_k, int blas_threads,
                    float* s_scratch, uint8_t* rflag, int64_t n_cap, int store_bf16,
                    float* recall_out, void* stream);
+
+/* Offload cache step + attention pieces for U kv-head units (one CTA each). */
+int wk_cache_offload_step(const wk_cache2_view* cv, const wk_index_view* ix, const wk_steady_view* st,
+                          const wk_step_view* sv, int G, int64_t step, int U, void* stream);
+
+/* Pinned, device-mapped host memory for the offloaded store (cudaHostAlloc
+ * mapped|portable); the returned pointer is valid on host and device. */
+int wk_host_alloc(size_t bytes, void** ptr);
+int wk_host_free(void* ptr);
 
 #ifdef __cplusplus
 }

@@ -50,7 +50,9 @@ class StepViewC(ctypes.Structure):
                 ("e_cap", _I32), ("ru_cap", _I32), ("eu_cap", _I32), ("rtok_row", _P),
                 ("rtok_mask", _P), ("sel_done", _P), ("rt_cap", _I32), ("pad_", _I32),
                 ("eu_x", _P), ("eu_sz", _P), ("rbits", _P), ("ebits", _P), ("pieces", _P),
-                ("woff", _P), ("w_cap", _I32), ("pc_cap", _I32)]
+                ("woff", _P), ("w_cap", _I32), ("pc_cap", _I32), ("arena_k", _P), ("arena_v", _P),
+                ("slot_ids", _P), ("slot_off", _P), ("arena_rows", _I64), ("slot_cap", _I64),
+                ("block_tokens", _I32), ("pstride", _I32)]
 
 
 class CacheViewC(ctypes.Structure):
@@ -61,6 +63,15 @@ class CacheViewC(ctypes.Structure):
                 ("ev_n", _P), ("m_live", _P), ("m_cap", _I64), ("slot_cap", _I64),
                 ("heap_cap", _I64), ("ids_cap", _I64), ("ev_cap", _I64), ("block_bytes", _I32),
                 ("token_bytes", _I32)]
+
+
+class Cache2ViewC(ctypes.Structure):
+    _fields_ = [(n, _P) for n in ("nblk", "slot_off", "slot_ids", "cached", "touched", "first", "lru",
+                                  "lru_tmp", "lru_n", "freel", "free_n", "next_slot", "capacity",
+                                  "occupied", "counters", "ids", "n_ids", "snapshot", "scratch",
+                                  "m_live")] + [
+        ("m_cap", _I64), ("slot_cap", _I64), ("lru_cap", _I64), ("ids_cap", _I64),
+        ("block_bytes", _I32), ("token_bytes", _I32), ("block_tokens", _I32), ("pad_", _I32)]
 
 
 class ZoneParamsC(ctypes.Structure):
@@ -74,7 +85,8 @@ _lib = None
 
 # every symbol include/wavekv.h declares
 EXPORTS = ("wk_version", "wk_kmeans_segments", "wk_append_tokens", "wk_score_topk",
-           "wk_tripartite_attn", "wk_full_attn", "wk_cache_step", "wk_recall_at_k")
+           "wk_tripartite_attn", "wk_full_attn", "wk_cache_step", "wk_recall_at_k",
+           "wk_cache_offload_step", "wk_host_alloc", "wk_host_free")
 
 
 def lib():
@@ -102,6 +114,10 @@ def lib():
     L.wk_recall_at_k.argtypes = [R(IndexViewC), R(SteadyViewC), R(StepViewC), _P, ctypes.c_int,
                                  ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _P, _P, _I64,
                                  ctypes.c_int, _P, _P]
+    L.wk_cache_offload_step.argtypes = [R(Cache2ViewC), R(IndexViewC), R(SteadyViewC), R(StepViewC),
+                                        ctypes.c_int, _I64, ctypes.c_int, _P]
+    L.wk_host_alloc.argtypes = [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]
+    L.wk_host_free.argtypes = [_P]
     for name in EXPORTS:
         getattr(L, name).restype = ctypes.c_int
     _lib = L

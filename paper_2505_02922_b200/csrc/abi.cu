@@ -53,7 +53,7 @@ size_t attend_v2_smem_bytes(int d, int HS);
 template <int CAND, bool SMS>
 __global__ void select_v6_kernel(IndexView, StepView, SelParams);
 size_t select_v6_dyn_smem(int m_max, bool sms, int cand);
-template <typename T, int DPL, int HS, bool FULL>
+template <typename T, int DPL, int HS, bool FULL, bool OFF>
 __global__ void attend_v4_kernel(IndexView, SteadyView, StepView, AttnParams, const int32_t*, int);
 template <typename T, int DPL, int HS, bool FULL>
 size_t attend_v4_smem();
@@ -61,6 +61,8 @@ __global__ void att4_est_prep_kernel(IndexView, StepView, int, float);
 template <bool FULL, int DL>
 __global__ void att4_merge_kernel(SteadyView, StepView, AttnParams, const int32_t*, int, int, int);
 __global__ void km_pack16_kernel(const SegDesc*, IndexView, int);
+// cache_v2.cu
+__global__ void cache2_step_kernel(wk_cache2_view, IndexView, SteadyView, StepView, int, int64_t);
 // metrics.cu
 template <typename T>
 __global__ void recall_kernel(IndexView, SteadyView, StepView, const int32_t*, int, int, int, int, float*,
@@ -228,19 +230,19 @@ static int launch_select_v6(const IndexView& ix, const StepView& sv, const SelPa
   return cudaGetLastError() == cudaSuccess ? 0 : WK_ECUDA;
 }
 
-template <typename T, int DPL, int HS, bool FULL>
+template <typename T, int DPL, int HS, bool FULL, bool OFF>
 static int launch_attend_v4(const IndexView& ix, const SteadyView& st, const StepView& sv, const AttnParams& p,
                             const int32_t* n_store, int U, int P, cudaStream_t s) {
   if (U > 1024) return WK_ECONFIG;
   const size_t sm = attend_v4_smem<T, DPL, HS, FULL>();
   static bool configured = false;
   if (!configured) {
-    if (cudaFuncSetAttribute(attend_v4_kernel<T, DPL, HS, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(attend_v4_kernel<T, DPL, HS, FULL, OFF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sm) != cudaSuccess)
       return WK_ECUDA;
     configured = true;
   }
-  attend_v4_kernel<T, DPL, HS, FULL><<<P, 256, sm, s>>>(ix, st, sv, p, n_store, U);
+  attend_v4_kernel<T, DPL, HS, FULL, OFF><<<P, 256, sm, s>>>(ix, st, sv, p, n_store, U);
   if (cudaGetLastError() != cudaSuccess) return WK_ECUDA;
   const int RG = 32 / HS;
   att4_merge_kernel<FULL, DPL / 2><<<(U * p.G + 3) / 4, 128, 0, s>>>(st, sv, p, n_store, U, P * 8, RG);
@@ -251,12 +253,13 @@ template <typename T, bool FULL>
 static int dispatch_attend_v4(const IndexView& ix, const SteadyView& st, const StepView& sv, const AttnParams& p,
                               const int32_t* n_store, int U, int P, cudaStream_t s) {
   const int hs = head_slots(p.G);
-  if (p.d == 128) {
-    return hs == 4 ? launch_attend_v4<T, 8, 4, FULL>(ix, st, sv, p, n_store, U, P, s)
-                   : launch_attend_v4<T, 8, 8, FULL>(ix, st, sv, p, n_store, U, P, s);
-  }
-  return hs == 4 ? launch_attend_v4<T, 4, 4, FULL>(ix, st, sv, p, n_store, U, P, s)
-                 : launch_attend_v4<T, 4, 8, FULL>(ix, st, sv, p, n_store, U, P, s);
+  const bool off = !FULL && sv.pstride == 4;
+#define WK_ATT4(DPL, HS)                                                                  \
+  (off ? launch_attend_v4<T, DPL, HS, FULL, !FULL>(ix, st, sv, p, n_store, U, P, s)      \
+       : launch_attend_v4<T, DPL, HS, FULL, false>(ix, st, sv, p, n_store, U, P, s))
+  if (p.d == 128) return hs == 4 ? WK_ATT4(8, 4) : WK_ATT4(8, 8);
+  return hs == 4 ? WK_ATT4(4, 4) : WK_ATT4(4, 8);
+#undef WK_ATT4
 }
 
 extern "C" {
@@ -461,6 +464,22 @@ int wk_cache_step(const wk_cache_view* cv, const int32_t* rlist, const int32_t* 
   WK_CHECK_LAUNCH();
   return 0;
 }
+
+int wk_cache_offload_step(const wk_cache2_view* cv, const wk_index_view* ix, const wk_steady_view* st,
+                          const wk_step_view* sv, int G, int64_t step, int U, void* stream) {
+  if (!cv || !ix || !st || !sv || U <= 0 || G < 1 || G > 8 || sv->pstride != 4 || !sv->pieces) return WK_ECONFIG;
+  cudaStream_t s = (cudaStream_t)stream;
+  cache2_step_kernel<<<U, 512, 0, s>>>(*cv, *ix, *st, *sv, G, step);
+  WK_CHECK_LAUNCH();
+  return 0;
+}
+
+int wk_host_alloc(size_t bytes, void** ptr) {
+  if (!ptr) return WK_ECONFIG;
+  return cudaHostAlloc(ptr, bytes, cudaHostAllocMapped | cudaHostAllocPortable) == cudaSuccess ? 0 : WK_ECUDA;
+}
+
+int wk_host_free(void* ptr) { return cudaFreeHost(ptr) == cudaSuccess ? 0 : WK_ECUDA; }
 
 int wk_recall_at_k(const wk_index_view* ix, const wk_steady_view* st, const wk_step_view* sv,
                    const int32_t* n_store, int U, int G, int d, int metrics_k, int blas_threads,

@@ -146,7 +146,7 @@ WK_DEVINL void att4_counts(const SteadyView& st, const StepView& sv, const int32
 // first warp (of W) whose balanced range [N w / W, N (w+1) / W) holds chunk c
 WK_DEVINL int att4_warp_of(long long c, long long N, long long W) { return (int)(((c + 1) * W + N - 1) / N - 1); }
 
-template <typename T, int DPL, int HS, bool FULL>
+template <typename T, int DPL, int HS, bool FULL, bool OFF>
 __global__ void __launch_bounds__(256, HS == 8 ? 1 : 2) attend_v4_kernel(IndexView ix, SteadyView st, StepView sv, AttnParams p,
                                                             const int32_t* __restrict__ n_store, int U) {
   using CF = Att4Cfg<T, DPL, HS>;
@@ -262,6 +262,14 @@ __global__ void __launch_bounds__(256, HS == 8 ? 1 : 2) attend_v4_kernel(IndexVi
         m.a = lc * RG;
         n = min(RG, n_store[u] - m.a);
         m.mk = allmask;
+      } else if (OFF) {
+        // offload piece: (row, n | mask << 8 | flags << 16, cluster, first token)
+        const int4 pc = __ldcg(reinterpret_cast<const int4*>(sv.pieces) + (size_t)u * sv.pc_cap + lc);
+        m.a = pc.x;
+        n = -1;
+        m.mk = pc.y;
+        m.x = __int_as_float(pc.z);
+        m.w = __int_as_float(pc.w);
       } else {
         const int2 pc = __ldcg(reinterpret_cast<const int2*>(sv.pieces) + (size_t)u * sv.pc_cap + lc);
         m.a = pc.x;
@@ -286,8 +294,8 @@ __global__ void __launch_bounds__(256, HS == 8 ? 1 : 2) attend_v4_kernel(IndexVi
   };
   auto issue = [&](int sti, const Meta& m) {
     const int u = m.h & 0xfffff, kind = ((m.h >> 20) & 3) - 1;
-    int n = (m.h >> 22) & 31, mk = m.mk;
-    if (kind == 1 && !FULL) { n = m.mk & 0xff; mk = m.mk >> 8; }
+    int n = (m.h >> 22) & 31, mk = m.mk, flags = 0;
+    if (kind == 1 && !FULL) { n = m.mk & 0xff; mk = (m.mk >> 8) & 0xff; flags = OFF ? (m.mk >> 16) & 3 : 0; }
     unsigned char* stage = ring + sti * SB;
     float x = -INFINITY, w = 0.f;
     if (kind < 2) {
@@ -296,7 +304,10 @@ __global__ void __launch_bounds__(256, HS == 8 ? 1 : 2) attend_v4_kernel(IndexVi
       if (kind == 0) {
         srck = (const unsigned char*)st.k + ((size_t)u * st.t_cap + m.a) * ROWT;
         srcv = (const unsigned char*)st.v + ((size_t)u * st.t_cap + m.a) * ROWT;
-      } else {
+      } else if (OFF && (flags & 1)) {  // offload hit: the HBM slot arena
+        srck = (const unsigned char*)sv.arena_k + ((size_t)u * sv.arena_rows + m.a) * ROWT;
+        srcv = (const unsigned char*)sv.arena_v + ((size_t)u * sv.arena_rows + m.a) * ROWT;
+      } else {  // in-HBM store, or an offload miss: the pinned host store (zero-copy TMA)
         srck = (const unsigned char*)ix.store_k + ((size_t)u * ix.s_cap + m.a) * ROWT;
         srcv = (const unsigned char*)ix.store_v + ((size_t)u * ix.s_cap + m.a) * ROWT;
       }
@@ -325,7 +336,11 @@ __global__ void __launch_bounds__(256, HS == 8 ? 1 : 2) attend_v4_kernel(IndexVi
     smask[sti * 32 + lane] = mk;
     sx[sti * 32 + lane] = x;
     sw[sti * 32 + lane] = w;
-    if (lane == 0) stag[sti] = make_int4(u, kind, 0, 0);
+    // tag: (unit, kind, cluster, first token | rows << 24 | write-through << 31)
+    if (lane == 0)
+      stag[sti] = (OFF && kind == 1 && (flags & 2))
+                      ? make_int4(u, kind, __float_as_int(m.x), (__float_as_int(m.w) & 0xffffff) | (n << 24) | (int)0x80000000)
+                      : make_int4(u, kind, 0, 0);
   };
 
   // ---- q of the current unit (pre-scaled), softmax state, accumulators ----
@@ -488,6 +503,24 @@ __global__ void __launch_bounds__(256, HS == 8 ? 1 : 2) attend_v4_kernel(IndexVi
       }
       mbar_wait(bars + sti, (uint32_t)((k / NST) & 1));
       compute(sti, ck);
+      if (OFF && tg.w < 0) {
+        // admitted offload miss: write its rows through into the new slots
+        const int cl = tg.z, j0 = tg.w & 0xffffff, nrow = (tg.w >> 24) & 0x7f;
+        const int bt = sv.block_tokens;
+        const int32_t* sl = sv.slot_ids + (size_t)cu * sv.slot_cap;
+        const int so = __ldg(sv.slot_off + (size_t)cu * ix.m_cap + cl);
+        const unsigned char* stage = ring + sti * SB;
+        for (int i = half; i < nrow; i += 2) {
+          const int tok = j0 + i;
+          const size_t arow = (size_t)cu * sv.arena_rows + (size_t)__ldcg(sl + so + tok / bt) * bt + tok % bt;
+          for (int o = sub * 16; o < ROWT; o += 256) {
+            *reinterpret_cast<uint4*>((unsigned char*)sv.arena_k + arow * ROWT + o) =
+                *reinterpret_cast<const uint4*>(stage + i * ROWT + o);
+            *reinterpret_cast<uint4*>((unsigned char*)sv.arena_v + arow * ROWT + o) =
+                *reinterpret_cast<const uint4*>(stage + RG * ROWT + i * ROWT + o);
+          }
+        }
+      }
       __syncwarp();
     }
     flush();
@@ -667,10 +700,12 @@ template <typename T, int DPL, int HS, bool FULL>
 size_t attend_v4_smem() { return Att4Cfg<T, DPL, HS>::SMEM; }
 
 #define WK_INST_ATT4(T, DL, HS)                                                                                   \
-  template __global__ void attend_v4_kernel<T, DL, HS, false>(IndexView, SteadyView, StepView, AttnParams,          \
-                                                             const int32_t*, int);                                 \
-  template __global__ void attend_v4_kernel<T, DL, HS, true>(IndexView, SteadyView, StepView, AttnParams,           \
-                                                            const int32_t*, int);                                  \
+  template __global__ void attend_v4_kernel<T, DL, HS, false, false>(IndexView, SteadyView, StepView, AttnParams,   \
+                                                                    const int32_t*, int);                          \
+  template __global__ void attend_v4_kernel<T, DL, HS, false, true>(IndexView, SteadyView, StepView, AttnParams,    \
+                                                                   const int32_t*, int);                           \
+  template __global__ void attend_v4_kernel<T, DL, HS, true, false>(IndexView, SteadyView, StepView, AttnParams,    \
+                                                                   const int32_t*, int);                           \
   template size_t attend_v4_smem<T, DL, HS, false>();                                                              \
   template size_t attend_v4_smem<T, DL, HS, true>();
 WK_INST_ATT4(__nv_bfloat16, 8, 4)

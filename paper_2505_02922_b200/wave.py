@@ -75,7 +75,7 @@ class WaveLayer:
     def __init__(self, cfg: EngineConfig, U: int, G: int, d: int, *, max_prefill: int,
                  max_decode: int = 1024, store_dtype=torch.bfloat16, device="cuda",
                  blas_threads: int = 1, splits: int | None = None, keep_vs64: bool = False,
-                 with_elist: bool = False, score_mode: int | None = None):
+                 with_elist: bool = False, score_mode: int | None = None, offload: bool = False):
         self.cfg = cfg.validate()
         ic = cfg.index
         if d <= 0 or d % 4 or d > 256:
@@ -121,8 +121,19 @@ class WaveLayer:
         self.score_mode = 1 if score_mode is None else int(score_mode)
         dev, f32, i32 = self.dev, torch.float32, torch.int32
         # ---- index arrays ----
-        self.store_k = torch.zeros((U, self.s_cap, d), dtype=store_dtype, device=dev)
-        self.store_v = torch.zeros((U, self.s_cap, d), dtype=store_dtype, device=dev)
+        # offload (config 4): the cluster store is pinned host memory (the
+        # reference's slow tier); an HBM slot arena caches its blocks
+        self.offload = bool(offload)
+        if self.offload:
+            if not self.fast:
+                raise ConfigError("offload needs the fast path (d in {64, 128})")
+            from .block_cache import HostBuffer
+            self._host_k = HostBuffer((U, self.s_cap, d), store_dtype)
+            self._host_v = HostBuffer((U, self.s_cap, d), store_dtype)
+            self.store_k, self.store_v = self._host_k.tensor, self._host_v.tensor
+        else:
+            self.store_k = torch.zeros((U, self.s_cap, d), dtype=store_dtype, device=dev)
+            self.store_v = torch.zeros((U, self.s_cap, d), dtype=store_dtype, device=dev)
         self.store_tok = torch.full((U, self.s_cap), -1, dtype=i32, device=dev)
         self.cl_off = torch.zeros((U, self.m_cap), dtype=i32, device=dev)
         self.cl_size = torch.zeros((U, self.m_cap), dtype=i32, device=dev)
@@ -162,8 +173,11 @@ class WaveLayer:
             self.w_cap = self.m_cap // 32
             self.rbits = torch.zeros((U, G, self.w_cap), dtype=i32, device=dev)
             self.ebits = torch.zeros((U, G, self.w_cap), dtype=i32, device=dev)
-            self.pc_cap = self.s_cap // self.piece_rows + self.ru_cap + 1
-            self.pieces = torch.zeros((U, self.pc_cap, 2), dtype=i32, device=dev)
+            if self.offload:  # hits may fragment over arena slots
+                self.pc_cap = min(self.s_cap, 32 * self.ru_cap) + self.ru_cap + 1
+            else:
+                self.pc_cap = self.s_cap // self.piece_rows + self.ru_cap + 1
+            self.pieces = torch.zeros((U, self.pc_cap, 4 if self.offload else 2), dtype=i32, device=dev)
             self.woff = torch.zeros(U + 1, dtype=i32, device=dev)
         else:
             self.zmask = torch.zeros((U, self.m_cap), dtype=i32, device=dev)
@@ -195,6 +209,10 @@ class WaveLayer:
             _ptr(self.VS64), self.s_cap, self.m_cap, _ptr(self.Cmax), _ptr(self.C16), _ptr(self.Cscale))
         self._stv = _lib.SteadyViewC(_ptr(self.st_k), _ptr(self.st_v), _ptr(self.st_tok),
                                      _ptr(self.st_n), _ptr(self.next_tok), self.t_cap)
+        self.cache = None
+        if self.offload:
+            from .block_cache import OffloadCache
+            self.cache = OffloadCache(self)
         self.prefilled = False
 
     # ------------------------------------------------------------------ views
@@ -207,7 +225,11 @@ class WaveLayer:
             _ptr(self.status), self.r_cap, self.e_cap, self.ru_cap, self.eu_cap,
             _ptr(self.rtok_row), _ptr(self.rtok_mask), _ptr(self.sel_done), self.rt_cap, 0,
             _ptr(self.eu_x), _ptr(self.eu_sz), _ptr(self.rbits), _ptr(self.ebits), _ptr(self.pieces),
-            _ptr(self.woff), self.w_cap, self.pc_cap)
+            _ptr(self.woff), self.w_cap, self.pc_cap,
+            _ptr(self.cache.arena_k) if self.cache else None, _ptr(self.cache.arena_v) if self.cache else None,
+            _ptr(self.cache.slot_ids) if self.cache else None, _ptr(self.cache.slot_off) if self.cache else None,
+            self.cache.phys * self.cache.bt if self.cache else 0, self.cache.list_cap if self.cache else 0,
+            self.cache.bt if self.cache else 0, 4 if self.offload else 2)
 
     # --------------------------------------------------------------- clustering
     def _run_segments(self, segs: list[dict]):
@@ -307,6 +329,8 @@ class WaveLayer:
         self.m_dev.copy_(torch.tensor([s.m for s in self.units], dtype=torch.int32))
         self.n_store_dev.copy_(torch.tensor([s.store_fill for s in self.units], dtype=torch.int32))
         self.check_status("prefill")
+        if self.cache is not None:
+            self.cache.register_new()
         self.prefilled = True
         return self
 
@@ -339,6 +363,8 @@ class WaveLayer:
         m_max = max(s.m for s in self.units)
         _lib.check(L.wk_score_topk(ctypes.byref(self._ixv), ctypes.byref(sv), ctypes.byref(self._zp),
                                    self.U, m_max, stream), "wk_score_topk")
+        if self.cache is not None:  # wave buffer: lookup, replacement, miss plan
+            self.cache.step(sv)
         _lib.check(L.wk_tripartite_attn(ctypes.byref(self._ixv), ctypes.byref(self._stv),
                                         ctypes.byref(sv), ctypes.byref(self._zp), self.U, self.S,
                                         self.store_bf16, stream), "wk_tripartite_attn")
@@ -390,7 +416,9 @@ class WaveLayer:
             todo = self.needs_update()
 
     def on_clusters_added(self, units, k):
-        """Hook for the block-cache registration (engine.py:212-214)."""
+        """Block-cache registration of the new clusters (engine.py:212-214)."""
+        if self.cache is not None:
+            self.cache.register_new(units)
 
     # ----------------------------------------------------------- full attention
     def full_attention(self, q: torch.Tensor, out=None):
