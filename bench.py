@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-flashinfer", action="store_true")
+    ap.add_argument("--offload", action="store_true",
+                    help="configs[3]: host-KV offload (pinned store + HBM wave buffer); "
+                         "use with e.g. --ctx 1048576 --batch 4")
     return ap.parse_args()
 
 
@@ -238,6 +241,92 @@ def run_reference(a):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------- offload (config 4)
+def run_offload(a, torch, dev, log):
+    """configs[3]: long context with the cluster store in pinned host memory
+    and the wave buffer (HBM slot arena, cache_fraction of the blocks) on the
+    device.  Reports the cumulative hit ratio (per cluster), miss
+    bytes, and stall time = offload step time - the same step with the store
+    resident in HBM (same data, same zones)."""
+    from paper_2505_02922_b200 import EngineConfig, WaveLayer
+    G = HQ // HKV
+    U = a.batch * HKV
+    n_bufs = min(a.layer_bufs, a.layers)
+    per_buf = math.ceil(a.layers / n_bufs)
+    total_steps = a.warmup + a.steps
+    cfg = EngineConfig()
+    lay_o, lay_h, qpool, kpool = [], [], [], []
+    t_build = 0.0
+    for li in range(n_bufs):
+        keys, vals, cen = gen_layer(torch, U, a.ctx, D, li, dev)
+        for off, dst in ((True, lay_o), (False, lay_h)):
+            lay = WaveLayer(cfg, U, G, D, max_prefill=a.ctx, max_decode=64, store_dtype=torch.bfloat16,
+                            offload=off)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            lay.prefill(keys, vals)
+            torch.cuda.synchronize()
+            t_build += time.perf_counter() - t0
+            dst.append(lay)
+        qpool.append(gen_queries(torch, cen, G, total_steps * per_buf, 7 + li))
+        kpool.append(torch.randn((total_steps * per_buf, 2, U, D), device=dev).bfloat16().float())
+        del keys, vals, cen
+        torch.cuda.empty_cache()
+        log(f"layer buffer {li}: m={lay_o[-1].units[0].m} built (offload + hbm) {t_build:.1f}s")
+
+    def run(layers, steps, start):
+        use = [start * per_buf] * n_bufs
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(steps):
+            for l in range(a.layers):
+                b = l % n_bufs
+                j = use[b]
+                use[b] += 1
+                layers[b].launch_step(qpool[b][j], kpool[b][j, 0], kpool[b][j, 1])
+                for s_ in layers[b].units:
+                    s_.total += 1
+                    s_.n_steady += 1
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / max(1, steps)
+
+    run(lay_o, a.warmup, 0)
+    run(lay_h, a.warmup, 0)
+    c0 = [l.cache.counters.sum(0).clone() for l in lay_o]
+    with ClockSampler(0) as clk:
+        ms_o = run(lay_o, a.steps, a.warmup)
+    ms_h = run(lay_h, a.steps, a.warmup)
+    for l in lay_o + lay_h:
+        l.check_status("offload bench")
+    dk = sum((l.cache.counters.sum(0) - c) for l, c in zip(lay_o, c0)).tolist()
+    tot = sum(l.cache.counters.sum(0) for l in lay_o).tolist()
+    hits, misses = tot[0], tot[1]
+    # physical miss bytes: bf16 K+V rows of missed clusters read over the host link
+    per_step_miss_blocks = dk[2] / cfg.block_size_bytes / a.steps
+    bt = lay_o[0].cache.bt
+    line = {"metric": "decode tokens/sec with host-KV offload (device-timed); hit ratio, miss bytes, stall", "impl": "wave-offload", "value": a.batch / (ms_o / 1e3), "unit": "tokens/s",
+            "n_gpus": 1, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_o, "higher_is_better": True,
+            "data": "synthetic", "dtype": "bf16 KV / fp32 accumulate (fp64 scoring)",
+            "config": {"workload": f"{a.model}-shape {a.layers}-layer decode, {a.ctx} ctx, batch {a.batch}, "
+                                   "host-KV offload (configs[3])",
+                       "layer_buffers": n_bufs, "cache_fraction": cfg.cache_fraction,
+                       "host_store_gb_per_layer_buffer": 2 * U * lay_o[0].s_cap * D * 2 / 1e9},
+            "cache": {"hit_ratio_cumulative": hits / max(1, hits + misses), "hits": hits, "misses": misses,
+                      "hit_ratio_timed": dk[0] / max(1, dk[0] + dk[1]),
+                      "miss_blocks_per_step": per_step_miss_blocks,
+                      "miss_bytes_per_step_bf16": per_step_miss_blocks * bt * 2 * D * 2,
+                      "evictions_per_step": dk[5] / a.steps, "admissions_per_step": dk[6] / a.steps,
+                      "rejections_per_step": dk[7] / a.steps},
+            "hbm_resident": {"ms_per_step": ms_h, "value": a.batch / (ms_h / 1e3)},
+            "stall_ms_per_step": ms_o - ms_h,
+            "host_link_gbs": per_step_miss_blocks * bt * 2 * D * 2 / ((ms_o - ms_h) / 1e3) / 1e9
+            if ms_o > ms_h else None,
+            "build_s": t_build, "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+
+
 # ------------------------------------------------------------------- GPU arm
 def _ptr(t):
     return t.data_ptr()
@@ -262,6 +351,9 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    log = lambda *x: print(*x, file=sys.stderr, flush=True) if rank == 0 else None
+    if a.offload:
+        return run_offload(a, torch, dev, log)
     G = HQ // HKV
     U = a.batch * HKV  # per-rank units (weak scaling: each rank serves `batch` requests)
     n_bufs = min(a.layer_bufs, a.layers)
