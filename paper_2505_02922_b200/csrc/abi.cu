@@ -11,6 +11,7 @@ namespace wk {
 // kmeans.cu
 __global__ void km_prep_kernel(const SegDesc*, float*, int);
 __global__ void km_seed_kernel(const SegDesc*, const float*, float*, float*, int, int, int);
+__global__ void km_seed_v2_kernel(const SegDesc*, const float*, float*, float*, int, int, int);
 __global__ void km_assign_kernel(const SegDesc*, const float*, const float*, int32_t*, int);
 __global__ void km_assign_small_kernel(const SegDesc*, const float*, const float*, int32_t*, int);
 __global__ void km_update_kernel(const SegDesc*, const float*, float*, int32_t*, int32_t*, float*, int, int);
@@ -86,6 +87,7 @@ static int configure_smem() {
   if (g_smem_configured) return 0;
   // opt in to large dynamic shared memory where the kernels need it
   if (cudaFuncSetAttribute(km_seed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess) return WK_ECUDA;
+  if (cudaFuncSetAttribute(km_seed_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 72 * 1024) != cudaSuccess) return WK_ECUDA;
   if (cudaFuncSetAttribute(km_assign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024) != cudaSuccess) return WK_ECUDA;
   if (cudaFuncSetAttribute(km_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess) return WK_ECUDA;
   if (cudaFuncSetAttribute(km_finalize_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess) return WK_ECUDA;
@@ -277,10 +279,18 @@ int wk_kmeans_segments(const wk_index_view* ix, const wk_segment* segs, int n_se
   const SegDesc* sd = scr->segs_dev;
   km_prep_kernel<<<n_segs, 256, d * sizeof(float), s>>>(sd, scr->P, d);
   WK_CHECK_LAUNCH();
-  const int smem_rows = ((200 * 1024) / 4 - d) / 2;
-  const size_t seed_smem = (size_t)(d + 2 * (max_L <= smem_rows ? max_L : 0)) * sizeof(float);
-  km_seed_kernel<<<n_segs, 512, seed_smem, s>>>(sd, scr->P, scr->C, scr->md, d, blas_threads,
-                                                 max_L <= smem_rows ? smem_rows : 0);
+  if ((d % 8) == 0) {
+    // v2: 256 threads, <= 72 KB of smem so 3 segments share an SM
+    const int smem_rows = ((72 * 1024) / 4 - d) / 2;
+    const size_t seed_smem = (size_t)(d + 2 * (max_L <= smem_rows ? max_L : 0)) * sizeof(float);
+    km_seed_v2_kernel<<<n_segs, 256, seed_smem, s>>>(sd, scr->P, scr->C, scr->md, d, blas_threads,
+                                                      max_L <= smem_rows ? smem_rows : 0);
+  } else {
+    const int smem_rows = ((200 * 1024) / 4 - d) / 2;
+    const size_t seed_smem = (size_t)(d + 2 * (max_L <= smem_rows ? max_L : 0)) * sizeof(float);
+    km_seed_kernel<<<n_segs, 512, seed_smem, s>>>(sd, scr->P, scr->C, scr->md, d, blas_threads,
+                                                   max_L <= smem_rows ? smem_rows : 0);
+  }
   WK_CHECK_LAUNCH();
   const dim3 ag((max_L + 63) / 64, n_segs);
   const size_t asmem = (size_t)2 * d * 65 * sizeof(float);

@@ -115,6 +115,111 @@ __global__ void km_seed_kernel(const SegDesc* __restrict__ segs, const float* __
 }
 
 // ---------------------------------------------------------------------------
+// phase 2 (v2): the same k-means++ steps with a coalesced, recipe-exact sgemv.
+// A main row (OpenBLAS group-of-4 row, gemv_row_class 0) is served by two
+// lanes: lane h owns the accumulators a[4h .. 4h+3] of the reference's 8-way
+// FMA split (t mod 8) and streams its 16-byte slices t = 8s + 4h; the two
+// halves are combined in the recipe order ((a_l + a_{l+4}), then
+// (s0+s1)+(s2+s3)).  A warp covers 16 rows per 16-byte load instruction
+// (512 contiguous-row bytes).  Chunk-tail rows (classes 1, 2) keep the
+// per-thread recipe.  The fp32 cumsum stays the reference's sequential chain.
+// grid = n_segments, block = 256
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) km_seed_v2_kernel(const SegDesc* __restrict__ segs, const float* __restrict__ P_all,
+                                                         float* __restrict__ C_all, float* __restrict__ scratch_all,
+                                                         int d, int blas_threads, int smem_rows) {
+  const SegDesc sg = segs[blockIdx.x];
+  if (sg.k <= 1) return;
+  extern __shared__ __align__(16) float sm2[];
+  float* cent = sm2;  // d floats: current centroid
+  const int L = sg.L;
+  float *md, *cdf;
+  if (L <= smem_rows) {
+    md = sm2 + d;
+    cdf = md + L;
+  } else {
+    md = scratch_all + (size_t)sg.p_off * 2;
+    cdf = md + L;
+  }
+  const float* P = P_all + (size_t)sg.p_off * d;
+  float* C = C_all + (size_t)sg.c_off * d;
+  __shared__ Pcg64 g;
+  __shared__ long long s_idx;
+  if (threadIdx.x == 0) {
+    g.hi = sg.rng[0]; g.lo = sg.rng[1]; g.ihi = sg.rng[2]; g.ilo = sg.rng[3];
+    g.has32 = 0; g.u32 = 0;
+    s_idx = pcg_integers(g, L);
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const int h = lane & 1, rsub = lane >> 1;  // 16 rows per warp, 2 lanes per row
+  const int nq = d >> 3;                     // 16-byte slices per lane (d % 8 == 0)
+  // rows [0, main_end) of every chunk are class 0; find the first non-main row
+  for (int c = 0; c < sg.k; c++) {
+    const long long idx = s_idx;
+    for (int t = threadIdx.x; t < d; t += blockDim.x) {
+      const float v = P[(size_t)idx * d + t];
+      cent[t] = v;
+      C[(size_t)c * d + t] = v;
+    }
+    __syncthreads();
+    if (c == sg.k - 1) break;
+    for (int base = warp * 16; base < L; base += nwarp * 16) {
+      const int i = base + rsub;
+      const bool act = i < L;
+      const int cls = act ? gemv_row_class(i, L, d, blas_threads) : 0;
+      float dot = 0.f;
+      const unsigned both = __ballot_sync(0xffffffffu, act && cls == 0);
+      if (act && cls == 0) {
+        const float4* row = reinterpret_cast<const float4*>(P + (size_t)i * d) + h;
+        const float4* cv = reinterpret_cast<const float4*>(cent) + h;
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll 4
+        for (int q = 0; q < nq; q++) {
+          const float4 x = __ldcg(row + 2 * q), y = cv[2 * q];
+          a0 = __fmaf_rn(x.x, y.x, a0);
+          a1 = __fmaf_rn(x.y, y.y, a1);
+          a2 = __fmaf_rn(x.z, y.z, a2);
+          a3 = __fmaf_rn(x.w, y.w, a3);
+        }
+        // lane h = 0 holds a0..a3, h = 1 holds a4..a7: s_l = a_l + a_{l+4}
+        const unsigned pm = both & (0x3u << (lane & ~1));
+        const float b0 = __shfl_xor_sync(pm, a0, 1), b1 = __shfl_xor_sync(pm, a1, 1);
+        const float b2 = __shfl_xor_sync(pm, a2, 1), b3 = __shfl_xor_sync(pm, a3, 1);
+        const float s0 = __fadd_rn(a0, b0), s1 = __fadd_rn(a1, b1), s2 = __fadd_rn(a2, b2), s3 = __fadd_rn(a3, b3);
+        dot = __fadd_rn(0.f, __fadd_rn(__fadd_rn(s0, s1), __fadd_rn(s2, s3)));
+      } else if (act && h == 0) {
+        dot = sgemv_row(P + (size_t)i * d, cent, d, cls);
+      }
+      if (act && h == 0) {
+        float v = __fsub_rn(1.0f, dot);
+        v = v < 0.f ? 0.f : v;
+        if (c == 0) md[i] = v;
+        else if (!(md[i] <= v)) md[i] = v;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float sacc = md[0];
+      cdf[0] = sacc;
+      for (int i = 1; i < L; i++) { sacc = __fadd_rn(sacc, md[i]); cdf[i] = sacc; }
+      long long nidx;
+      if (sacc <= 0.0f) {
+        nidx = pcg_integers(g, L);
+      } else {
+        const float u = (float)pcg_next_double(g);
+        const float thr = __fmul_rn(u, sacc);
+        int lo = 0, hi = L;
+        while (lo < hi) { const int mid = (lo + hi) >> 1; if (cdf[mid] <= thr) lo = mid + 1; else hi = mid; }
+        nidx = lo > L - 1 ? L - 1 : lo;
+      }
+      s_idx = nidx;
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
 // phase 3: assignment = argmax(points @ centroids.T) (clustering.py:85,96).
 // Every score is the reference's sequential fp32 FMA chain over t; register
 // tiled 64 points x 64 centroids per CTA iteration, transposed smem tiles.
