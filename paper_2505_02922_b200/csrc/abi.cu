@@ -27,29 +27,6 @@ template <typename T, bool FULL>
 __global__ void attend_kernel(IndexView, SteadyView, StepView, AttnParams, const int32_t*);
 __global__ void merge_kernel(StepView, AttnParams, int);
 size_t select_smem_bytes();
-// decode_v2.cu
-template <int HS>
-__global__ void score_v2_kernel(IndexView, StepView, int, int, int);
-// select_v5.cu
-__global__ void select_v5_kernel(IndexView, StepView, SelParams);
-// select_v4.cu
-template <int PT>
-__global__ void select_v4_kernel(IndexView, StepView, SelParams);
-size_t select_v4_smem();
-// decode_v3.cu
-__global__ void select_v3_kernel(IndexView, StepView, SelParams, int, int);
-size_t sel_smem_bytes(int m_max, int r_max);
-template <typename T, int DL, int HS, bool FULL>
-__global__ void attend_v3_kernel(IndexView, SteadyView, StepView, AttnParams, const int32_t*);
-template <typename T, int DL, int HS, bool FULL>
-size_t attend_v3_smem();
-template <int HS, int DL>
-__global__ void score_v3_kernel(IndexView, StepView, int, int);
-template <int HS, int DL>
-size_t score_v3_smem();
-template <typename T, int DL, int HS, bool FULL>
-__global__ void attend_v2_kernel(IndexView, SteadyView, StepView, AttnParams, const int32_t*);
-size_t attend_v2_smem_bytes(int d, int HS);
 // select_v6.cu / attend_v4.cu / score_v4.cu
 template <int CAND, bool SMS>
 __global__ void select_v6_kernel(IndexView, StepView, SelParams);
@@ -98,10 +75,6 @@ static int configure_smem() {
   if (cudaFuncSetAttribute(attend_kernel<__nv_bfloat16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, at) != cudaSuccess) return WK_ECUDA;
   if (cudaFuncSetAttribute(attend_kernel<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, at) != cudaSuccess) return WK_ECUDA;
   if (cudaFuncSetAttribute(attend_kernel<__nv_bfloat16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, at) != cudaSuccess) return WK_ECUDA;
-  if (cudaFuncSetAttribute(select_v3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess) return WK_ECUDA;
-  if (cudaFuncSetAttribute(select_v5_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024) != cudaSuccess) return WK_ECUDA;
-  if (cudaFuncSetAttribute(select_v4_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)select_v4_smem()) != cudaSuccess) return WK_ECUDA;
-  if (cudaFuncSetAttribute(select_v4_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)select_v4_smem()) != cudaSuccess) return WK_ECUDA;
   const int rs = (int)recall_smem_bytes();
   if (cudaFuncSetAttribute(recall_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, rs) != cudaSuccess) return WK_ECUDA;
   if (cudaFuncSetAttribute(recall_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, rs) != cudaSuccess) return WK_ECUDA;
@@ -110,59 +83,6 @@ static int configure_smem() {
 }
 
 static int head_slots(int G) { return G <= 4 ? 4 : 8; }
-static bool v2_ok(int d) { return d == 64 || d == 128; }
-static int g_max_smem = 0;
-
-template <typename T, int DL, int HS, bool FULL>
-static int launch_attend_v2(const IndexView& ix, const SteadyView& st, const StepView& sv, const AttnParams& p,
-                            const int32_t* n_store, int U, int S, cudaStream_t s) {
-  const size_t sm = attend_v3_smem<T, DL, HS, FULL>();
-  static bool configured = false;
-  if (!configured) {
-    if (cudaFuncSetAttribute(attend_v3_kernel<T, DL, HS, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sm) != cudaSuccess)
-      return WK_ECUDA;
-    configured = true;
-  }
-  attend_v3_kernel<T, DL, HS, FULL><<<dim3(S, U), 256, sm, s>>>(ix, st, sv, p, n_store);
-  return cudaGetLastError() == cudaSuccess ? 0 : WK_ECUDA;
-}
-
-template <int HS, int DL>
-static int launch_score_v3(const IndexView& ix, const StepView& sv, int G, int U, int m_max, cudaStream_t s) {
-  const size_t sm = score_v3_smem<HS, DL>();
-  static bool configured = false;
-  if (!configured) {
-    if (cudaFuncSetAttribute(score_v3_kernel<HS, DL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) !=
-        cudaSuccess)
-      return WK_ECUDA;
-    configured = true;
-  }
-  const int quantum = 4 * (32 / HS);
-  long long want = ((long long)m_max * U + 148 * 12 - 1) / (148 * 12);
-  int rows = (int)((want + quantum - 1) / quantum) * quantum;
-  if (rows < quantum) rows = quantum;
-  dim3 g((m_max + rows - 1) / rows, U);
-  score_v3_kernel<HS, DL><<<g, 128, sm, s>>>(ix, sv, G, rows);
-  return cudaGetLastError() == cudaSuccess ? 0 : WK_ECUDA;
-}
-
-template <typename T, bool FULL>
-static int dispatch_attend_v2(const IndexView& ix, const SteadyView& st, const StepView& sv, const AttnParams& p,
-                              const int32_t* n_store, int U, int S, cudaStream_t s) {
-  const int hs = head_slots(p.G);
-  if (p.d == 128) {
-    switch (hs) {
-      case 4: return launch_attend_v2<T, 8, 4, FULL>(ix, st, sv, p, n_store, U, S, s);
-      default: return launch_attend_v2<T, 8, 8, FULL>(ix, st, sv, p, n_store, U, S, s);
-    }
-  }
-  switch (hs) {
-    case 4: return launch_attend_v2<T, 4, 4, FULL>(ix, st, sv, p, n_store, U, S, s);
-    default: return launch_attend_v2<T, 4, 8, FULL>(ix, st, sv, p, n_store, U, S, s);
-  }
-}
-
 // ---- v6 pipeline: score_v4 (tensor cores) | score_v3, select_v6, attend_v4 ----
 static int sm_count() {
   static int n = 0;
@@ -362,20 +282,9 @@ int wk_score_topk(const wk_index_view* ix, const wk_step_view* sv, const wk_zone
     p.prof = g_sel_prof;
     return launch_select_v6(*ix, *sv, p, U, m_max, s);
   }
-  const bool v2 = v2_ok(zp->d) && sv->rtok_row && sv->sel_done;
   if (m_max > 0) {
-    if (v2) {
-      const int hs = head_slots(zp->G);
-      int rc;
-      if (zp->d == 128) rc = hs == 4 ? launch_score_v3<4, 4>(*ix, *sv, zp->G, U, m_max, s)
-                                     : launch_score_v3<8, 4>(*ix, *sv, zp->G, U, m_max, s);
-      else rc = hs == 4 ? launch_score_v3<4, 2>(*ix, *sv, zp->G, U, m_max, s)
-                        : launch_score_v3<8, 2>(*ix, *sv, zp->G, U, m_max, s);
-      if (rc) return rc;
-    } else {
-      dim3 g1((m_max + 63) / 64, U);
-      score_kernel<<<g1, 256, 0, s>>>(*ix, *sv, zp->d, zp->G);
-    }
+    dim3 g1((m_max + 63) / 64, U);
+    score_kernel<<<g1, 256, 0, s>>>(*ix, *sv, zp->d, zp->G);
     WK_CHECK_LAUNCH();
   }
   SelParams p;
@@ -385,16 +294,10 @@ int wk_score_topk(const wk_index_view* ix, const wk_step_view* sv, const wk_zone
   p.inv_sqrt_d = (float)(1.0 / sqrt((double)zp->d));
   p.need_tail = zp->tail_denominator_only;
   p.need_allc = zp->denominator_eq2;
-  p.score_fp64 = v2 ? 1 : 0;
-  if (v2) {
-    const double r_max = floor(zp->retrieval_fraction * (double)m_max + 0.5) + 1;
-    if (r_max <= 384 && (zp->d % 32) == 0 && m_max <= 16384)
-      select_v5_kernel<<<U * zp->G, 256, (size_t)((m_max + 7) & ~7) * 2, s>>>(*ix, *sv, p);
-    else
-      select_v3_kernel<<<U * zp->G, 256, sel_smem_bytes(m_max, sv->r_cap), s>>>(*ix, *sv, p, m_max, sv->r_cap);
-    WK_CHECK_LAUNCH();
-    return 0;
-  }
+  p.score_fp64 = 0;
+  p.score_mode = 0;
+  p.piece_rows = 0;
+  p.prof = 0;
   select_kernel<<<U * zp->G, 512, select_smem_bytes(), s>>>(*ix, *sv, p);
   WK_CHECK_LAUNCH();
   union_kernel<<<U, 1024, 0, s>>>(*ix, *sv);
@@ -420,11 +323,7 @@ int wk_tripartite_attn(const wk_index_view* ix, const wk_steady_view* st, const 
     return store_bf16 ? dispatch_attend_v4<__nv_bfloat16, false>(*ix, *st, *sv, p, nullptr, U, S, s)
                       : dispatch_attend_v4<float, false>(*ix, *st, *sv, p, nullptr, U, S, s);
   }
-  if (v2_ok(zp->d) && sv->rtok_row && sv->sel_done) {
-    const int rc = store_bf16 ? dispatch_attend_v2<__nv_bfloat16, false>(*ix, *st, *sv, p, nullptr, U, S, s)
-                              : dispatch_attend_v2<float, false>(*ix, *st, *sv, p, nullptr, U, S, s);
-    if (rc) return rc;
-  } else if (store_bf16)
+  if (store_bf16)
     attend_kernel<__nv_bfloat16, false><<<grid, 128, attend_smem_bytes(zp->d, 2), s>>>(*ix, *st, *sv, p, nullptr);
   else
     attend_kernel<float, false><<<grid, 128, attend_smem_bytes(zp->d, 4), s>>>(*ix, *st, *sv, p, nullptr);
@@ -451,11 +350,7 @@ int wk_full_attn(const wk_index_view* ix, const wk_steady_view* st, const wk_ste
   if (v6_ok(ix, sv, d))
     return store_bf16 ? dispatch_attend_v4<__nv_bfloat16, true>(*ix, *st, v, p, n_store, U, S, s)
                       : dispatch_attend_v4<float, true>(*ix, *st, v, p, n_store, U, S, s);
-  if (v2_ok(d)) {
-    const int rc = store_bf16 ? dispatch_attend_v2<__nv_bfloat16, true>(*ix, *st, v, p, n_store, U, S, s)
-                              : dispatch_attend_v2<float, true>(*ix, *st, v, p, n_store, U, S, s);
-    if (rc) return rc;
-  } else if (store_bf16)
+  if (store_bf16)
     attend_kernel<__nv_bfloat16, true><<<grid, 128, attend_smem_bytes(d, 2), s>>>(*ix, *st, v, p, n_store);
   else
     attend_kernel<float, true><<<grid, 128, attend_smem_bytes(d, 4), s>>>(*ix, *st, v, p, n_store);

@@ -29,43 +29,6 @@ namespace wk {
 
 __device__ __align__(128) unsigned char g_zero4[8192];
 
-template <int HS>
-struct SoftState4 {
-  float M[HS], D[HS];
-};
-
-// online-softmax update for one chunk; x = the lane's logit for (row j_own,
-// head h_own), wz = its denominator weight (1 for tokens, the cluster size for
-// estimation rows).  Returns the lane's numerator weight; fills alpha[].
-template <int HS>
-WK_DEVINL float att4_softmax(float x, float wz, SoftState4<HS>& st, float (&alpha)[HS]) {
-  float mx = x;
-#pragma unroll
-  for (int off = HS; off < 32; off <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-  const int h_own = (threadIdx.x & 31) % HS;
-  float mo_own = st.M[0];
-#pragma unroll
-  for (int h = 1; h < HS; h++)
-    if (h == h_own) mo_own = st.M[h];
-  const float mnew_own = fmaxf(mo_own, mx);
-  const float pw = (x == -INFINITY) ? 0.f : __expf(x - mnew_own);
-  float ps = pw * wz;
-#pragma unroll
-  for (int off = HS; off < 32; off <<= 1) ps += __shfl_xor_sync(0xffffffffu, ps, off);
-#pragma unroll
-  for (int h = 0; h < HS; h++) {
-    const float mn = __shfl_sync(0xffffffffu, mnew_own, h);
-    const float sd = __shfl_sync(0xffffffffu, ps, h);
-    const float mo = st.M[h];
-    float a = (mo == -INFINITY) ? 0.f : __expf(mo - mn);
-    if (mn == -INFINITY) a = 1.f;
-    alpha[h] = a;
-    st.D[h] = st.D[h] * a + sd;
-    st.M[h] = mn;
-  }
-  return pw;
-}
-
 template <typename T, int DPL> struct Row4;
 template <> struct Row4<__nv_bfloat16, 8> {
   static WK_DEVINL void ld(const unsigned char* p, float2 (&o)[4]) {

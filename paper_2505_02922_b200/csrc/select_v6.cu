@@ -24,6 +24,8 @@
 
 namespace wk {
 
+__device__ long long g_sel_dbg[4096][16];  // per-CTA phase timestamps (globaltimer, ns), SelParams.prof
+
 constexpr int S6_T = 256;
 constexpr int S6_NW = S6_T / 32;
 constexpr int S6_NB = 2048;    // histogram buckets (linear over [min, max])
@@ -610,3 +612,7 @@ template __global__ void select_v6_kernel<512, false>(IndexView, StepView, SelPa
 template __global__ void select_v6_kernel<2048, false>(IndexView, StepView, SelParams);
 
 }  // namespace wk
+
+extern "C" int wk_debug_select_timing(long long* out, int n) {
+  return cudaMemcpyFromSymbol(out, wk::g_sel_dbg, sizeof(long long) * 16 * (size_t)n) == cudaSuccess ? 0 : -2;
+}

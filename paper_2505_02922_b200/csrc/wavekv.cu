@@ -2,10 +2,6 @@
 // (sm_100a) from the kernel sources and the C ABI.
 #include "kmeans.cu"
 #include "decode.cu"
-#include "decode_v2.cu"
-#include "decode_v3.cu"
-#include "select_v4.cu"
-#include "select_v5.cu"
 #include "select_v6.cu"
 #include "attend_v4.cu"
 #include "score_v4.cu"
