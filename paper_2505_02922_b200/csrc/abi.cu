@@ -167,7 +167,7 @@ static int launch_attend_v4(const IndexView& ix, const SteadyView& st, const Ste
   attend_v4_kernel<T, DPL, HS, FULL, OFF><<<P, 256, sm, s>>>(ix, st, sv, p, n_store, U);
   if (cudaGetLastError() != cudaSuccess) return WK_ECUDA;
   const int RG = 32 / HS;
-  att4_merge_kernel<FULL, DPL / 2><<<(U * p.G + 3) / 4, 128, 0, s>>>(st, sv, p, n_store, U, P * 8, RG);
+  att4_merge_kernel<FULL, DPL / 2><<<U * p.G, 128, 0, s>>>(st, sv, p, n_store, U, P * 8, RG);
   return cudaGetLastError() == cudaSuccess ? 0 : WK_ECUDA;
 }
 

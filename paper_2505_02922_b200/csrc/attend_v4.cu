@@ -503,9 +503,16 @@ __global__ void att4_est_prep_kernel(IndexView ix, StepView sv, int G, float isd
   if (e >= sv.cnt[u * 4 + 2]) return;
   const size_t row = (size_t)u * sv.eu_cap + e;
   const int c = __ldcg(sv.eu_ids + row), mk = __ldcg(sv.eu_mask + row);
-  sv.eu_sz[row] = (float)__ldg(ix.cl_size + (size_t)u * ix.m_cap + c);
-  for (int h = 0; h < G; h++)
-    sv.eu_x[row * G + h] = ((mk >> h) & 1) ? __ldcg(sv.scores + ((size_t)u * G + h) * ix.m_cap + c) * isd : -INFINITY;
+  // all loads first (one round trip), then the stores
+  const float sz = (float)__ldg(ix.cl_size + (size_t)u * ix.m_cap + c);
+  float x[8];
+#pragma unroll
+  for (int h = 0; h < 8; h++)
+    x[h] = (h < G && ((mk >> h) & 1)) ? __ldcg(sv.scores + ((size_t)u * G + h) * ix.m_cap + c) * isd : -INFINITY;
+  sv.eu_sz[row] = sz;
+#pragma unroll
+  for (int h = 0; h < 8; h++)
+    if (h < G) sv.eu_x[row * G + h] = x[h];
 }
 
 // ---------------------------------------------------------------------------
@@ -515,11 +522,14 @@ template <bool FULL, int DL>
 __global__ void __launch_bounds__(128) att4_merge_kernel(SteadyView st, StepView sv, AttnParams p,
                                                           const int32_t* __restrict__ n_store, int U, int Wtot,
                                                           int RG) {
+  // one CTA (4 warps) per (unit, head): the partial records are split over
+  // the warps so ~4x more loads are in flight than with one warp per head
   const int G = p.G, d = p.d, D2 = 4 + d;  // partial record: (M, D, -, -, num[d])
-  const int gw = blockIdx.x * 4 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (gw >= U * G) return;
-  const int u = gw / G, g = gw % G;
+  const int u = blockIdx.x / G, g = blockIdx.x % G;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, t = threadIdx.x;
+  __shared__ float s_m[3][4];
+  __shared__ float s_d[3][4];
+  __shared__ float s_n[3][4][128];
   const long long N = sv.woff[U];
   int c0, c1, c2;
   {
@@ -530,8 +540,6 @@ __global__ void __launch_bounds__(128) att4_merge_kernel(SteadyView st, StepView
   }
   const long long ub = sv.woff[u];
   const long long kb[4] = {ub, ub + c0, ub + c0 + c1, ub + c0 + c1 + c2};
-  // the partials of all three kinds form one flat item list (kind, warp) so
-  // every global load of the merge is issued lane-parallel / unrolled
   int nk[3], wk0[3];
 #pragma unroll
   for (int k = 0; k < 3; k++) {
@@ -549,9 +557,9 @@ __global__ void __launch_bounds__(128) att4_merge_kernel(SteadyView st, StepView
   };
   auto rec = [&](int k, int w) { return sv.part + (((size_t)(w + u) * 3 + k) * G + g) * (size_t)D2; };
   auto live_w = [&](int w) { return N * w / Wtot < N * (w + 1) / Wtot; };  // empty ranges wrote nothing
-  // pass 1: per-kind max
+  // pass 1: per-kind max over all items (thread-parallel)
   float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY;
-  for (int i = lane; i < S; i += 32) {
+  for (int i = t; i < S; i += 128) {
     int k, w;
     item(i, k, w);
     if (!live_w(w)) continue;
@@ -562,18 +570,24 @@ __global__ void __launch_bounds__(128) att4_merge_kernel(SteadyView st, StepView
     }
   }
   m0 = warp_max(m0); m1 = warp_max(m1); m2 = warp_max(m2);
-  // pass 2: scales (lane-parallel), numerators (independent unrolled loads)
+  if (lane == 0) { s_m[0][warp] = m0; s_m[1][warp] = m1; s_m[2][warp] = m2; }
+  __syncthreads();
+  m0 = fmaxf(fmaxf(s_m[0][0], s_m[0][1]), fmaxf(s_m[0][2], s_m[0][3]));
+  m1 = fmaxf(fmaxf(s_m[1][0], s_m[1][1]), fmaxf(s_m[1][2], s_m[1][3]));
+  m2 = fmaxf(fmaxf(s_m[2][0], s_m[2][1]), fmaxf(s_m[2][2], s_m[2][3]));
+  // pass 2: warp w folds items i = w, w + 4, ... (scales lane-parallel, loads unrolled)
   float d0 = 0.f, d1 = 0.f, d2 = 0.f;
   float n0[DL], n1[DL], n2[DL];
 #pragma unroll
   for (int j = 0; j < DL; j++) n0[j] = n1[j] = n2[j] = 0.f;
-  for (int i0 = 0; i0 < S; i0 += 32) {
+  const int Sw = (S - warp + 3) / 4;  // items of this warp
+  for (int i0 = 0; i0 < Sw; i0 += 32) {
     float sc = 0.f;
     {
-      const int i = i0 + lane;
-      if (i < S) {
+      const int ii = i0 + lane;
+      if (ii < Sw) {
         int k, w;
-        item(i, k, w);
+        item(warp + 4 * ii, k, w);
         if (live_w(w)) {
           const float* r = rec(k, w);
           const float dw = __ldcg(r + 1);
@@ -585,12 +599,12 @@ __global__ void __launch_bounds__(128) att4_merge_kernel(SteadyView st, StepView
         }
       }
     }
-    const int nw = min(32, S - i0);
+    const int nw = min(32, Sw - i0);
 #pragma unroll 8
     for (int j = 0; j < nw; j++) {
-      const float sw = __shfl_sync(0xffffffffu, sc, j);
+      const float swt = __shfl_sync(0xffffffffu, sc, j);
       int k, w;
-      item(i0 + j, k, w);
+      item(warp + 4 * (i0 + j), k, w);
       const float* src = rec(k, w) + 4 + lane * DL;
       float v[DL];
       if (DL == 4) {
@@ -603,18 +617,35 @@ __global__ void __launch_bounds__(128) att4_merge_kernel(SteadyView st, StepView
       // partials of empty-range warps may hold stale bits: weight 0 selects them out
 #pragma unroll
       for (int jj = 0; jj < DL; jj++) {
-        const float add = sw != 0.f ? v[jj] * sw : 0.f;
+        const float add = swt != 0.f ? v[jj] * swt : 0.f;
         n0[jj] += k == 0 ? add : 0.f;
         n1[jj] += k == 1 ? add : 0.f;
         n2[jj] += k == 2 ? add : 0.f;
       }
     }
   }
+  d0 = warp_sum(d0); d1 = warp_sum(d1); d2 = warp_sum(d2);
+  if (lane == 0) { s_d[0][warp] = d0; s_d[1][warp] = d1; s_d[2][warp] = d2; }
+#pragma unroll
+  for (int jj = 0; jj < DL; jj++) {
+    s_n[0][warp][lane * DL + jj] = n0[jj];
+    s_n[1][warp][lane * DL + jj] = n1[jj];
+    s_n[2][warp][lane * DL + jj] = n2[jj];
+  }
+  __syncthreads();
+  if (warp != 0) return;
   double kM[3] = {m0, m1, m2};
-  double kD[3] = {warp_sum(d0), warp_sum(d1), warp_sum(d2)};
+  double kD[3];
   float num[3][DL];
 #pragma unroll
-  for (int j = 0; j < DL; j++) { num[0][j] = n0[j]; num[1][j] = n1[j]; num[2][j] = n2[j]; }
+  for (int k = 0; k < 3; k++) {
+    kD[k] = (double)s_d[k][0] + s_d[k][1] + s_d[k][2] + s_d[k][3];
+#pragma unroll
+    for (int jj = 0; jj < DL; jj++) {
+      const int o = lane * DL + jj;
+      num[k][jj] = ((s_n[k][0][o] + s_n[k][1][o]) + (s_n[k][2][o] + s_n[k][3][o]));
+    }
+  }
   const float zero4[4] = {-INFINITY, 0.f, -INFINITY, 0.f};
   const float* tl = (!FULL && sv.tail) ? sv.tail + ((size_t)u * G + g) * 4 : zero4;
   const bool live0 = kD[0] > 0, live1 = kD[1] > 0, live2 = kD[2] > 0;
