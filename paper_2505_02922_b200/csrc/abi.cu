@@ -35,6 +35,8 @@ template <typename T, int DPL, int HS, bool FULL, bool OFF>
 __global__ void attend_v4_kernel(IndexView, SteadyView, StepView, AttnParams, const int32_t*, int);
 template <typename T, int DPL, int HS, bool FULL>
 size_t attend_v4_smem();
+template <typename T, int DPL, int HS>
+int attend_v4_warps();
 __global__ void att4_est_prep_kernel(IndexView, StepView, int, float);
 template <bool FULL, int DL>
 __global__ void att4_merge_kernel(SteadyView, StepView, AttnParams, const int32_t*, int, int, int);
@@ -164,10 +166,11 @@ static int launch_attend_v4(const IndexView& ix, const SteadyView& st, const Ste
       return WK_ECUDA;
     configured = true;
   }
-  attend_v4_kernel<T, DPL, HS, FULL, OFF><<<P, 256, sm, s>>>(ix, st, sv, p, n_store, U);
+  const int warps = attend_v4_warps<T, DPL, HS>();
+  attend_v4_kernel<T, DPL, HS, FULL, OFF><<<P, warps * 32, sm, s>>>(ix, st, sv, p, n_store, U);
   if (cudaGetLastError() != cudaSuccess) return WK_ECUDA;
-  const int RG = 32 / HS;
-  att4_merge_kernel<FULL, DPL / 2><<<U * p.G, 128, 0, s>>>(st, sv, p, n_store, U, P * 8, RG);
+  const int RG = HS == 4 ? 16 : 4;  // Att4Cfg::RG
+  att4_merge_kernel<FULL, DPL / 2><<<U * p.G, 128, 0, s>>>(st, sv, p, n_store, U, P * warps, RG);
   return cudaGetLastError() == cudaSuccess ? 0 : WK_ECUDA;
 }
 
@@ -278,7 +281,7 @@ int wk_score_topk(const wk_index_view* ix, const wk_step_view* sv, const wk_zone
     p.need_allc = zp->denominator_eq2;
     p.score_fp64 = 1;
     p.score_mode = tc ? 2 : 1;
-    p.piece_rows = 32 / head_slots(zp->G);
+    p.piece_rows = head_slots(zp->G) == 4 ? 16 : 4;  // attend_v4 chunk rows (Att4Cfg::RG)
     p.prof = g_sel_prof;
     return launch_select_v6(*ix, *sv, p, U, m_max, s);
   }

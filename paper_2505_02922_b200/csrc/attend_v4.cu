@@ -77,16 +77,18 @@ WK_DEVINL float att4_treduce16(float (&v)[16]) {
 
 template <typename T, int DPL, int HS>
 struct Att4Cfg {
-  static constexpr int RG = 32 / HS;               // rows per chunk
-  static constexpr int NST = 3;                    // ring stages per warp
+  static constexpr int RG = HS == 4 ? 16 : 4;      // rows per chunk
+  static constexpr int NL = (RG / 2) * HS / 16;    // (row, head) logits per lane after the reduction
+  static constexpr int NST = RG == 16 ? 2 : 3;     // ring stages per warp
   static constexpr int D = 16 * DPL;
   static constexpr int ROWT = D * (int)sizeof(T);  // K or V row bytes
   static constexpr int ROWV = D * 4;               // value-sum row bytes
   static constexpr int SB = ((2 * RG * ROWT > RG * ROWV ? 2 * RG * ROWT : RG * ROWV) + 127) / 128 * 128;
-  static constexpr int WARPS = 8;
+  // one CTA per SM: 12 warps when the ring fits (<= 168 registers, no spills)
+  static constexpr int WARPS = HS == 8 ? 8 : (SB <= 8192 ? 12 : 6);
   static constexpr int MAXU = 1024;                // units per launch (smem chunk prefix)
-  // per warp: ring + barriers + per-stage lane meta (mask, x, w) + stage tags
-  static constexpr int META = NST * 32 * 12 + NST * 16 + 32 * 4;  // + p broadcast buffer
+  // per warp: stage tags + per-stage estimation inputs (x, w per lane slot) + p broadcast buffer
+  static constexpr int META = NST * (16 + NL * 32 * 8) + RG * HS * 4;
   static constexpr size_t SMEM = (size_t)WARPS * NST * SB + (size_t)WARPS * NST * 8 + (size_t)WARPS * META +
                                  (size_t)(MAXU + 1) * 4 + 64;
 };
@@ -110,10 +112,10 @@ WK_DEVINL void att4_counts(const SteadyView& st, const StepView& sv, const int32
 WK_DEVINL int att4_warp_of(long long c, long long N, long long W) { return (int)(((c + 1) * W + N - 1) / N - 1); }
 
 template <typename T, int DPL, int HS, bool FULL, bool OFF>
-__global__ void __launch_bounds__(256, HS == 8 ? 1 : 2) attend_v4_kernel(IndexView ix, SteadyView st, StepView sv, AttnParams p,
+__global__ void __launch_bounds__(Att4Cfg<T, DPL, HS>::WARPS * 32, 1) attend_v4_kernel(IndexView ix, SteadyView st, StepView sv, AttnParams p,
                                                             const int32_t* __restrict__ n_store, int U) {
   using CF = Att4Cfg<T, DPL, HS>;
-  constexpr int RG = CF::RG, NST = CF::NST, ROWT = CF::ROWT, ROWV = CF::ROWV, SB = CF::SB;
+  constexpr int RG = CF::RG, NST = CF::NST, ROWT = CF::ROWT, ROWV = CF::ROWV, SB = CF::SB, NL = CF::NL;
   constexpr int D = CF::D, RH = RG / 2, DP2 = DPL / 2;
   const int G = p.G;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -122,11 +124,10 @@ __global__ void __launch_bounds__(256, HS == 8 ? 1 : 2) attend_v4_kernel(IndexVi
   unsigned char* ring = a4s + (size_t)warp * NST * SB;
   uint64_t* bars = reinterpret_cast<uint64_t*>(a4s + (size_t)CF::WARPS * NST * SB) + warp * NST;
   unsigned char* meta = a4s + (size_t)CF::WARPS * NST * SB + (size_t)CF::WARPS * NST * 8 + (size_t)warp * CF::META;
-  int* smask = reinterpret_cast<int*>(meta);
-  float* sx = reinterpret_cast<float*>(meta + NST * 32 * 4);
-  float* sw = reinterpret_cast<float*>(meta + NST * 32 * 8);
-  float* pbuf = reinterpret_cast<float*>(meta + NST * 32 * 12 + NST * 16);  // [RG][HS] chunk weights
-  int4* stag = reinterpret_cast<int4*>(meta + NST * 32 * 12);  // (unit, kind)
+  int4* stag = reinterpret_cast<int4*>(meta);                          // [NST] chunk tags
+  float* sx = reinterpret_cast<float*>(meta + NST * 16);               // [NST][NL][32] estimation logits
+  float* sw = sx + NST * NL * 32;                                      // [NST][NL][32] their weights
+  float* pbuf = reinterpret_cast<float*>(meta + NST * (16 + NL * 32 * 8));  // [RG][HS] chunk weights
   int* woff = reinterpret_cast<int*>(a4s + (size_t)CF::WARPS * NST * SB + (size_t)CF::WARPS * NST * 8 +
                                      (size_t)CF::WARPS * CF::META);
 
@@ -147,7 +148,7 @@ __global__ void __launch_bounds__(256, HS == 8 ? 1 : 2) attend_v4_kernel(IndexVi
         const int y = __shfl_up_sync(0xffffffffu, x, o);
         if (lane >= o) x += y;
       }
-      int* ws = woff + CF::MAXU + 1;  // 8 ints of scratch past woff (within the +64 pad)
+      int* ws = woff + CF::MAXU + 1;  // <= 16 ints of scratch past woff (within the +64 pad)
       if (lane == 31) ws[warp] = x;
       __syncthreads();
       int wbase = 0;
@@ -176,7 +177,9 @@ __global__ void __launch_bounds__(256, HS == 8 ? 1 : 2) attend_v4_kernel(IndexVi
 
   const float isd = p.inv_sqrt_d;
   const int allmask = (1 << G) - 1;
-  const int j_own = half + 2 * (sub / HS), h_own = sub % HS;
+  // after the reduction lane (half, sub) holds the logits of (row jl(l), head h_own), l < NL
+  const int h_own = sub % HS;
+  auto jl = [&](int l) { return half + 2 * ((l * 16 + sub) / HS); };
 
   // ---- issue cursor: (unit, kind, local chunk) of chunk ci ----
   int iu = 0;
@@ -200,10 +203,13 @@ __global__ void __launch_bounds__(256, HS == 8 ? 1 : 2) attend_v4_kernel(IndexVi
     int h;  // unit (bits 0-19) | kind + 1 (20-21) | n (22-26)
     int a;  // first row (kinds 0/1) or the lane's estimation cluster (kind 2)
     int mk; // head mask (kinds 0/1)
-    float x, w;
+    float x[NL], w[NL];  // kind 2: lane slots' logits / weights; offload kind 1: cluster, first token
   };
   auto chunk_meta = [&](long long ci) {
-    Meta m{0, 0, 0, -INFINITY, 0.f};
+    Meta m;
+    m.h = 0; m.a = 0; m.mk = 0;
+#pragma unroll
+    for (int l = 0; l < NL; l++) { m.x[l] = -INFINITY; m.w[l] = 0.f; }
     if (ci >= cb) return m;
     while (ci >= woff[iu + 1]) {
       iu++;
@@ -231,8 +237,8 @@ __global__ void __launch_bounds__(256, HS == 8 ? 1 : 2) attend_v4_kernel(IndexVi
         m.a = pc.x;
         n = -1;
         m.mk = pc.y;
-        m.x = __int_as_float(pc.z);
-        m.w = __int_as_float(pc.w);
+        m.x[0] = __int_as_float(pc.z);
+        m.w[0] = __int_as_float(pc.w);
       } else {
         const int2 pc = __ldcg(reinterpret_cast<const int2*>(sv.pieces) + (size_t)u * sv.pc_cap + lc);
         m.a = pc.x;
@@ -245,12 +251,14 @@ __global__ void __launch_bounds__(256, HS == 8 ? 1 : 2) attend_v4_kernel(IndexVi
       const int e0 = lc * RG;
       n = min(RG, sv.cnt[u * 4 + 2] - e0);
       if (lane < n) m.a = __ldcg(sv.eu_ids + (size_t)u * sv.eu_cap + e0 + lane);
-      // lane (row j_own, head h_own): logit sigma * q.C and cluster size
+      // lane slot (row jl, head h_own): logit sigma * q.C and cluster size
       // (att4_est_prep_kernel)
-      if (j_own < n && h_own < G) {
-        m.x = __ldcg(sv.eu_x + ((size_t)u * sv.eu_cap + e0 + j_own) * G + h_own);
-        m.w = __ldcg(sv.eu_sz + (size_t)u * sv.eu_cap + e0 + j_own);
-      }
+#pragma unroll
+      for (int l = 0; l < NL; l++)
+        if (jl(l) < n && h_own < G) {
+          m.x[l] = __ldcg(sv.eu_x + ((size_t)u * sv.eu_cap + e0 + jl(l)) * G + h_own);
+          m.w[l] = __ldcg(sv.eu_sz + (size_t)u * sv.eu_cap + e0 + jl(l));
+        }
     }
     m.h = u | ((kind + 1) << 20) | ((n & 31) << 22);
     return m;
@@ -260,7 +268,6 @@ __global__ void __launch_bounds__(256, HS == 8 ? 1 : 2) attend_v4_kernel(IndexVi
     int n = (m.h >> 22) & 31, mk = m.mk, flags = 0;
     if (kind == 1 && !FULL) { n = m.mk & 0xff; mk = (m.mk >> 8) & 0xff; flags = OFF ? (m.mk >> 16) & 3 : 0; }
     unsigned char* stage = ring + sti * SB;
-    float x = -INFINITY, w = 0.f;
     if (kind < 2) {
       const unsigned char* srck;
       const unsigned char* srcv;
@@ -283,27 +290,23 @@ __global__ void __launch_bounds__(256, HS == 8 ? 1 : 2) attend_v4_kernel(IndexVi
           bulk_g2s(stage + RG * ROWT + n * ROWT, g_zero4, (uint32_t)((RG - n) * ROWT), bars + sti);
         }
       }
-      mk = j_own < n ? mk : 0;
-      x = 0.f;
-      w = 1.f;
     } else {
       if (lane == 0) mbar_arrive_expect_tx(bars + sti, (uint32_t)(RG * ROWV));
       __syncwarp();
       if (lane < n)
         bulk_g2s(stage + lane * ROWV, ix.VS32 + ((size_t)u * ix.m_cap + m.a) * D, (uint32_t)ROWV, bars + sti);
       if (lane == 0 && n < RG) bulk_g2s(stage + n * ROWV, g_zero4, (uint32_t)((RG - n) * ROWV), bars + sti);
-      x = m.x;
-      w = m.w;
-      mk = x == -INFINITY ? 0 : allmask;
+#pragma unroll
+      for (int l = 0; l < NL; l++) {
+        sx[(sti * NL + l) * 32 + lane] = m.x[l];
+        sw[(sti * NL + l) * 32 + lane] = m.w[l];
+      }
     }
-    smask[sti * 32 + lane] = mk;
-    sx[sti * 32 + lane] = x;
-    sw[sti * 32 + lane] = w;
-    // tag: (unit, kind, cluster, first token | rows << 24 | write-through << 31)
+    // tag: (unit, kind + 1 | rows << 8 | head mask << 16, cluster, first token | write-through << 31)
     if (lane == 0)
-      stag[sti] = (OFF && kind == 1 && (flags & 2))
-                      ? make_int4(u, kind, __float_as_int(m.x), (__float_as_int(m.w) & 0xffffff) | (n << 24) | (int)0x80000000)
-                      : make_int4(u, kind, 0, 0);
+      stag[sti] = make_int4(u, (kind + 1) | (n << 8) | (mk << 16),
+                            (OFF && kind == 1 && (flags & 2)) ? __float_as_int(m.x[0]) : 0,
+                            (OFF && kind == 1 && (flags & 2)) ? ((__float_as_int(m.w[0]) & 0xffffff) | (int)0x80000000) : 0);
   };
 
   // ---- q of the current unit (pre-scaled), softmax state, accumulators ----
@@ -366,11 +369,13 @@ __global__ void __launch_bounds__(256, HS == 8 ? 1 : 2) attend_v4_kernel(IndexVi
     reset();
   };
 
-  auto compute = [&](int sti, int kind) {
+  // tg = the stage's tag: kind + 1 | rows << 8 | head mask << 16
+  auto compute = [&](int sti, int tagw) {
+    const int kind = (tagw & 0xff) - 1, nrow = (tagw >> 8) & 0xff, hmask = (tagw >> 16) & 0xff;
     const unsigned char* stage = ring + sti * SB;
-    float x, wz;
+    float x[NL], wz[NL];
     if (kind < 2) {
-      float v[16];
+      float v[NL][16];
 #pragma unroll
       for (int jj = 0; jj < RH; jj++) {
         const int j = half + 2 * jj;
@@ -381,23 +386,34 @@ __global__ void __launch_bounds__(256, HS == 8 ? 1 : 2) attend_v4_kernel(IndexVi
           float2 a2 = __fmul2_rn(kf[0], qv[h][0]);
 #pragma unroll
           for (int k = 1; k < DP2; k++) a2 = __ffma2_rn(kf[k], qv[h][k], a2);
-          v[jj * HS + h] = a2.x + a2.y;
+          const int idx = jj * HS + h;
+          v[idx >> 4][idx & 15] = a2.x + a2.y;
         }
       }
-      x = att4_treduce16(v);
-      if (!((smask[sti * 32 + lane] >> h_own) & 1)) x = -INFINITY;
-      wz = 1.f;
+      const bool hon = (hmask >> h_own) & 1;
+#pragma unroll
+      for (int l = 0; l < NL; l++) {
+        x[l] = att4_treduce16(v[l]);
+        if (!(hon && jl(l) < nrow)) x[l] = -INFINITY;
+        wz[l] = 1.f;
+      }
     } else {
-      x = sx[sti * 32 + lane];
-      wz = sw[sti * 32 + lane];
+#pragma unroll
+      for (int l = 0; l < NL; l++) {
+        x[l] = sx[(sti * NL + l) * 32 + lane];
+        wz[l] = sw[(sti * NL + l) * 32 + lane];
+      }
     }
     float mo = mref[0];
 #pragma unroll
     for (int h = 1; h < HS; h++)
       if (h == h_own) mo = mref[h];
-    if (__any_sync(0xffffffffu, x > mo + 10.f)) {
+    float xm = x[0];
+#pragma unroll
+    for (int l = 1; l < NL; l++) xm = fmaxf(xm, x[l]);
+    if (__any_sync(0xffffffffu, xm > mo + 10.f)) {
       // raise the references of the heads whose chunk max exceeds them
-      float mx = x;
+      float mx = xm;
 #pragma unroll
       for (int off = HS; off < 32; off <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
 #pragma unroll
@@ -417,9 +433,12 @@ __global__ void __launch_bounds__(256, HS == 8 ? 1 : 2) attend_v4_kernel(IndexVi
       for (int h = 1; h < HS; h++)
         if (h == h_own) mo = mref[h];
     }
-    const float pw = x == -INFINITY ? 0.f : __expf(x - mo);
-    dl = fmaf(pw, wz, dl);
-    pbuf[j_own * HS + h_own] = pw;
+#pragma unroll
+    for (int l = 0; l < NL; l++) {
+      const float pw = x[l] == -INFINITY ? 0.f : __expf(x[l] - mo);
+      dl = fmaf(pw, wz[l], dl);
+      pbuf[jl(l) * HS + h_own] = pw;
+    }
     __syncwarp();
 #pragma unroll
     for (int jj = 0; jj < RH; jj++) {
@@ -458,17 +477,18 @@ __global__ void __launch_bounds__(256, HS == 8 ? 1 : 2) attend_v4_kernel(IndexVi
       }
       __syncwarp();
       const int4 tg = stag[sti];
-      if (tg.x != cu || tg.y != ck) {
+      const int tkind = (tg.y & 0xff) - 1;
+      if (tg.x != cu || tkind != ck) {
         flush();
         cu = tg.x;
-        ck = tg.y;
+        ck = tkind;
         if (qu != cu) load_q(cu);
       }
       mbar_wait(bars + sti, (uint32_t)((k / NST) & 1));
-      compute(sti, ck);
+      compute(sti, tg.y);
       if (OFF && tg.w < 0) {
         // admitted offload miss: write its rows through into the new slots
-        const int cl = tg.z, j0 = tg.w & 0xffffff, nrow = (tg.w >> 24) & 0x7f;
+        const int cl = tg.z, j0 = tg.w & 0xffffff, nrow = (tg.y >> 8) & 0xff;
         const int bt = sv.block_tokens;
         const int32_t* sl = sv.slot_ids + (size_t)cu * sv.slot_cap;
         const int so = __ldg(sv.slot_off + (size_t)cu * ix.m_cap + cl);
@@ -692,6 +712,8 @@ __global__ void __launch_bounds__(128) att4_merge_kernel(SteadyView st, StepView
 
 template <typename T, int DPL, int HS, bool FULL>
 size_t attend_v4_smem() { return Att4Cfg<T, DPL, HS>::SMEM; }
+template <typename T, int DPL, int HS>
+int attend_v4_warps() { return Att4Cfg<T, DPL, HS>::WARPS; }
 
 #define WK_INST_ATT4(T, DL, HS)                                                                                   \
   template __global__ void attend_v4_kernel<T, DL, HS, false, false>(IndexView, SteadyView, StepView, AttnParams,   \
@@ -701,7 +723,8 @@ size_t attend_v4_smem() { return Att4Cfg<T, DPL, HS>::SMEM; }
   template __global__ void attend_v4_kernel<T, DL, HS, true, false>(IndexView, SteadyView, StepView, AttnParams,    \
                                                                    const int32_t*, int);                           \
   template size_t attend_v4_smem<T, DL, HS, false>();                                                              \
-  template size_t attend_v4_smem<T, DL, HS, true>();
+  template size_t attend_v4_smem<T, DL, HS, true>();                                                               \
+  template int attend_v4_warps<T, DL, HS>();
 WK_INST_ATT4(__nv_bfloat16, 8, 4)
 WK_INST_ATT4(__nv_bfloat16, 8, 8)
 WK_INST_ATT4(__nv_bfloat16, 4, 4)

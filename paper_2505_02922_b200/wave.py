@@ -108,11 +108,11 @@ class WaveLayer:
         # fast path (select_v6 / attend_v4 / score_v4): d in {64, 128}
         self.fast = d in (64, 128)
         hs = 4 if G <= 4 else 8
-        self.piece_rows = 32 // hs
+        self.piece_rows = 16 if hs == 4 else 4  # attend_v4 chunk rows
         if self.fast:
             sms = torch.cuda.get_device_properties(self.dev).multi_processor_count
-            per_sm = 2 if (hs == 4 and store_dtype == torch.bfloat16) else 1
-            self.S = splits or max(1, min(per_sm * sms, 4 * U))  # persistent attention grid
+            self.S = splits or max(1, min(sms, 4 * U))  # persistent attention grid: 1 CTA / SM
+            self.attn_warps = 8 if hs == 8 else (12 if (store_dtype == torch.bfloat16 or d == 64) else 6)
         else:
             self.S = splits or max(1, min(64, -(-2048 // U)))
         # 1: fp32 C scan with fp64 accumulation (estimation logits need ~fp32
@@ -191,7 +191,7 @@ class WaveLayer:
         self.eu_x = torch.zeros((U, self.eu_cap, G), dtype=f32, device=dev)
         self.eu_sz = torch.zeros((U, self.eu_cap), dtype=f32, device=dev)
         self.tail = torch.zeros((U, G, 4), dtype=f32, device=dev)
-        n_part = (self.S * 8 + U) if self.fast else U * self.S
+        n_part = (self.S * self.attn_warps + U) if self.fast else U * self.S
         self.part = torch.zeros((n_part, 3, G, (4 + d) if self.fast else (2 + d)), dtype=f32, device=dev)
         self.out = torch.zeros((U, G, d), dtype=f32, device=dev)
         self.logden = torch.zeros((U, G), dtype=f32, device=dev)
