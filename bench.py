@@ -29,8 +29,8 @@ HQ, HKV, D = 32, 8, 128
 # head shapes of the BASELINE configs (configs[1] Llama-3-8B, configs[4] Qwen2.5-7B)
 MODELS = {"llama3-8b": (32, 8, 128, 32), "qwen2.5-7b": (28, 4, 128, 28)}
 METRIC = "decode tokens/sec at 120K ctx (device-timed) and % HBM roofline vs full attn"
-# kernels per layer and step: append, score_v5, select_v6, est_prep, attend_v4, merge
-LAUNCHES_PER_LAYER = 6
+# kernels per layer and step: score_v5, select_v6 (+ fused append), est_prep, attend_v4, merge
+LAUNCHES_PER_LAYER = 5
 
 
 def parse():

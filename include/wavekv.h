@@ -240,6 +240,14 @@ int wk_recall_at_k(const wk_index_view* ix, const wk_steady_view* st, const wk_s
                    float* s_scratch, uint8_t* rflag, int64_t n_cap, int store_bf16,
                    float* recall_out, void* stream);
 
+/* One decode step of the in-HBM path in one call: append (fused into the
+ * zone-planning kernel), centroid scan, exact zone planning + unions,
+ * tripartite attention and merge (HeadEngine.decode_step minus the metrics,
+ * engine.py:174-210). */
+int wk_decode_step(const wk_index_view* ix, const wk_steady_view* st, const wk_step_view* sv,
+                   const wk_zone_params* zp, const float* k_new, const float* v_new, int U, int m_max, int S,
+                   int store_bf16, void* stream);
+
 /* Offload cache step + attention pieces for U kv-head units (one CTA each). */
 int wk_cache_offload_step(const wk_cache2_view* cv, const wk_index_view* ix, const wk_steady_view* st,
                           const wk_step_view* sv, int G, int64_t step, int U, void* stream);

@@ -86,7 +86,7 @@ _lib = None
 # every symbol include/wavekv.h declares
 EXPORTS = ("wk_version", "wk_kmeans_segments", "wk_append_tokens", "wk_score_topk",
            "wk_tripartite_attn", "wk_full_attn", "wk_cache_step", "wk_recall_at_k",
-           "wk_cache_offload_step", "wk_host_alloc", "wk_host_free")
+           "wk_cache_offload_step", "wk_host_alloc", "wk_host_free", "wk_decode_step")
 
 
 def lib():
@@ -116,6 +116,8 @@ def lib():
                                  ctypes.c_int, _P, _P]
     L.wk_cache_offload_step.argtypes = [R(Cache2ViewC), R(IndexViewC), R(SteadyViewC), R(StepViewC),
                                         ctypes.c_int, _I64, ctypes.c_int, _P]
+    L.wk_decode_step.argtypes = [R(IndexViewC), R(SteadyViewC), R(StepViewC), R(ZoneParamsC), _P, _P,
+                                 ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _P]
     L.wk_host_alloc.argtypes = [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]
     L.wk_host_free.argtypes = [_P]
     for name in EXPORTS:

@@ -96,6 +96,9 @@ static int sm_count() {
   return n;
 }
 static int g_sel_prof = 0;
+// wk_decode_step hands the token append to wk_score_topk's select kernel
+struct AppendArgs { int on; const float* k; const float* v; SteadyView st; int bf16; };
+static thread_local AppendArgs g_append = {0, nullptr, nullptr, {}, 0};
 extern "C" int wk_debug_select_prof(int on) { g_sel_prof = on; return 0; }
 static bool v6_ok(const wk_index_view* ix, const wk_step_view* sv, int d) {
   return (d == 64 || d == 128) && sv->rbits && sv->ebits && sv->pieces && sv->woff && sv->sel_done && ix->Cmax;
@@ -283,6 +286,8 @@ int wk_score_topk(const wk_index_view* ix, const wk_step_view* sv, const wk_zone
     p.score_mode = tc ? 2 : 1;
     p.piece_rows = head_slots(zp->G) == 4 ? 16 : 4;  // attend_v4 chunk rows (Att4Cfg::RG)
     p.prof = g_sel_prof;
+    p.k_new = nullptr; p.v_new = nullptr; p.store_bf16 = 0;
+    if (g_append.on) { p.k_new = g_append.k; p.v_new = g_append.v; p.st = g_append.st; p.store_bf16 = g_append.bf16; }
     return launch_select_v6(*ix, *sv, p, U, m_max, s);
   }
   if (m_max > 0) {
@@ -380,6 +385,25 @@ int wk_cache_offload_step(const wk_cache2_view* cv, const wk_index_view* ix, con
   cache2_step_kernel<<<U, 512, 0, s>>>(*cv, *ix, *st, *sv, G, step);
   WK_CHECK_LAUNCH();
   return 0;
+}
+
+int wk_decode_step(const wk_index_view* ix, const wk_steady_view* st, const wk_step_view* sv,
+                   const wk_zone_params* zp, const float* k_new, const float* v_new, int U, int m_max, int S,
+                   int store_bf16, void* stream) {
+  if (!ix || !st || !sv || !zp || !k_new || !v_new || U <= 0) return WK_ECONFIG;
+  if (!v6_ok(ix, sv, zp->d) || sv->pstride != 2 || m_max <= 0) {
+    // generic path: separate append
+    int rc = wk_append_tokens(st, k_new, v_new, U, zp->d, store_bf16, stream);
+    if (rc) return rc;
+    rc = wk_score_topk(ix, sv, zp, U, m_max, stream);
+    if (rc) return rc;
+    return wk_tripartite_attn(ix, st, sv, zp, U, S, store_bf16, stream);
+  }
+  g_append = {1, k_new, v_new, *st, store_bf16};
+  const int rc = wk_score_topk(ix, sv, zp, U, m_max, stream);
+  g_append.on = 0;
+  if (rc) return rc;
+  return wk_tripartite_attn(ix, st, sv, zp, U, S, store_bf16, stream);
 }
 
 int wk_host_alloc(size_t bytes, void** ptr) {

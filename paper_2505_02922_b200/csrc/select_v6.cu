@@ -270,6 +270,26 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
   const int m = sv.m[u];
   const int t = threadIdx.x, T = S6_T, lane = t & 31, warp = t >> 5;
   const int W = (m + 31) >> 5;
+  if (p.k_new && g == 0) {
+    // append this step's token to the unit's steady buffer (engine.py:178-182)
+    const int row = p.st.n[u];
+    const size_t o = ((size_t)u * p.st.t_cap + row) * d;
+    for (int i = t; i < d; i += T) {
+      const float kv = p.k_new[(size_t)u * d + i], vv = p.v_new[(size_t)u * d + i];
+      if (p.store_bf16) {
+        reinterpret_cast<__nv_bfloat16*>(p.st.k)[o + i] = __float2bfloat16_rn(kv);
+        reinterpret_cast<__nv_bfloat16*>(p.st.v)[o + i] = __float2bfloat16_rn(vv);
+      } else {
+        reinterpret_cast<float*>(p.st.k)[o + i] = kv;
+        reinterpret_cast<float*>(p.st.v)[o + i] = vv;
+      }
+    }
+    if (t == 0) {
+      p.st.tok[(size_t)u * p.st.t_cap + row] = p.st.next_tok[u];
+      p.st.next_tok[u] += 1;
+      p.st.n[u] = row + 1;
+    }
+  }
   float* scs = s6_dyn;
   uint32_t* rbits = reinterpret_cast<uint32_t*>(s6_dyn + (SMS ? ((m + 3) & ~3) : 0));
   uint32_t* tre = rbits + W;  // certain or selected members of the top r+e

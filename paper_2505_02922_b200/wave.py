@@ -357,10 +357,15 @@ class WaveLayer:
         self._q = q
         stream = ctypes.c_void_p(_stream())
         L = self.L
-        _lib.check(L.wk_append_tokens(ctypes.byref(self._stv), _ptr(k_new), _ptr(v_new), self.U,
-                                      self.d, self.store_bf16, stream), "wk_append_tokens")
         sv = self._step_view(q)
         m_max = max(s.m for s in self.units)
+        if self.cache is None:  # one fused call: append + scan + zones + attention
+            _lib.check(L.wk_decode_step(ctypes.byref(self._ixv), ctypes.byref(self._stv), ctypes.byref(sv),
+                                        ctypes.byref(self._zp), _ptr(k_new), _ptr(v_new), self.U, m_max,
+                                        self.S, self.store_bf16, stream), "wk_decode_step")
+            return
+        _lib.check(L.wk_append_tokens(ctypes.byref(self._stv), _ptr(k_new), _ptr(v_new), self.U,
+                                      self.d, self.store_bf16, stream), "wk_append_tokens")
         _lib.check(L.wk_score_topk(ctypes.byref(self._ixv), ctypes.byref(sv), ctypes.byref(self._zp),
                                    self.U, m_max, stream), "wk_score_topk")
         if self.cache is not None:  # wave buffer: lookup, replacement, miss plan
