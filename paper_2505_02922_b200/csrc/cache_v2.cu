@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(C2_T) cache2_step_kernel(Cache2View cv, IndexV
   for (int i = q0; i < q1; i++) {
     const int cl = ids[i], s = csize[cl];
     int mk = 0;
-    for (int g = 0; g < G; g++) mk |= (int)((rb[(size_t)g * sv.w_cap + (cl >> 5)] >> (cl & 31)) & 1u) << g;
+    for (int g = 0; g < G; g++) mk |= (int)((rb[(size_t)g * sv.w_cap + zb_word(cl)] >> zb_bit(cl)) & 1u) << g;
     if (!snap[i]) {
       const int fill = cached[cl] ? 2 : 0;
       for (int j = 0; j < s; j += PR)

@@ -266,6 +266,15 @@ WK_DEVINL double score_error_bound_v2(double qnorm2, double cmax, int d, int mod
   return score_error_bound(qnorm2, cmax, d, mode == 1);
 }
 
+// Zone bitmaps (per-head R / E sets, select_v6 -> unions -> cache_v2) use a
+// permuted layout so one warp ballot over 32 lanes x float4 covers a word:
+// cluster c <-> word ((c >> 7) << 2) | (c & 3), bit (c >> 2) & 31.
+// Words per unit: 4 * ceil(m / 128).
+__host__ __device__ __forceinline__ int zb_word(int c) { return ((c >> 7) << 2) | (c & 3); }
+__host__ __device__ __forceinline__ int zb_bit(int c) { return (c >> 2) & 31; }
+__host__ __device__ __forceinline__ int zb_cluster(int w, int b) { return ((w >> 2) << 7) | (b << 2) | (w & 3); }
+__host__ __device__ __forceinline__ int zb_words(int m) { return ((m + 127) >> 7) << 2; }
+
 WK_DEVINL float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

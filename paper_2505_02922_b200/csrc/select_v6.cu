@@ -181,7 +181,7 @@ template <int CAND>
 __device__ void s6_union(const IndexView& ix, const StepView& sv, const SelParams& p, int u, int m,
                          Sel6Smem<CAND>& sm) {
   const int G = p.G, T = S6_T, t = threadIdx.x;
-  const int W = (m + 31) >> 5;
+  const int W = zb_words(m);
   const int w0 = (int)((long long)W * t / T), w1 = (int)((long long)W * (t + 1) / T);
   const uint32_t* rb = sv.rbits + (size_t)u * G * sv.w_cap;
   const uint32_t* eb = sv.ebits + (size_t)u * G * sv.w_cap;
@@ -196,7 +196,7 @@ __device__ void s6_union(const IndexView& ix, const StepView& sv, const SelParam
     v[0] += __popc(ur);
     v[3] += __popc(ue);
     while (ur) {
-      const int c = (w << 5) + __ffs(ur) - 1;
+      const int c = zb_cluster(w, __ffs(ur) - 1);
       ur &= ur - 1;
       const int s = __ldg(csize + c);
       v[1] += s;
@@ -229,7 +229,7 @@ __device__ void s6_union(const IndexView& ix, const StepView& sv, const SelParam
       while (ur) {
         const int bit = __ffs(ur) - 1;
         ur &= ur - 1;
-        const int c = (w << 5) + bit;
+        const int c = zb_cluster(w, bit);
         int mk = 0;
 #pragma unroll
         for (int g = 0; g < 8; g++) mk |= ((rw[g] >> bit) & 1u) << g;
@@ -245,7 +245,7 @@ __device__ void s6_union(const IndexView& ix, const StepView& sv, const SelParam
         int mk = 0;
 #pragma unroll
         for (int g = 0; g < 8; g++) mk |= ((ew[g] >> bit) & 1u) << g;
-        eu[ie] = (w << 5) + bit;
+        eu[ie] = zb_cluster(w, bit);
         emk[ie] = (uint8_t)mk;
         ie++;
       }
@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
   const int u = blockIdx.x / G, g = blockIdx.x % G;
   const int m = sv.m[u];
   const int t = threadIdx.x, T = S6_T, lane = t & 31, warp = t >> 5;
-  const int W = (m + 31) >> 5;
+  const int W = zb_words(m);
   if (p.k_new && g == 0) {
     // append this step's token to the unit's steady buffer (engine.py:178-182)
     const int row = p.st.n[u];
@@ -418,26 +418,51 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
     const float fhr = __double2float_ru(hr), flr = __double2float_rd(lr);
     const float fhe = e > 0 ? __double2float_ru(he) : INFINITY, fle = e > 0 ? __double2float_rd(le) : INFINITY;
     int cnt_in_r = 0, cnt_in_e = 0;
-#pragma unroll 2
-    for (int base = 0; base < m; base += T) {
-      const int c = base + t;
-      const float v = c < m ? S_(c) : -INFINITY;
-      const bool cand = v >= flr;
-      const bool in_r = v > fhr;
-      const bool in_e = v > fhe;
-      const bool bd_e = !in_e && v >= fle;
-      const unsigned mir = __ballot_sync(0xffffffffu, in_r);
-      const unsigned mie = __ballot_sync(0xffffffffu, in_e);
-      cnt_in_r += __popc(mir);
-      cnt_in_e += __popc(mie);
-      if (lane == 0 && c < m) tre[c >> 5] = mie;
-      if ((cand && !in_r) || bd_e) {
-        const char* row = reinterpret_cast<const char*>(C64 + (size_t)c * d);
-        for (int o = 0; o < d * 8; o += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(row + o));
+    // four clusters per lane: a warp covers 128 clusters = 4 zone-bitmap words
+    const int mq = (m + 3) >> 2;
+    for (int base = 0; base < mq; base += T) {
+      const int qi = base + t;
+      float v[4];
+      if (SMS && qi < (m >> 2)) {
+        const float4 f = reinterpret_cast<const float4*>(scs)[qi];
+        v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; k++) v[k] = 4 * qi + k < m ? S_(4 * qi + k) : -INFINITY;
       }
-      s6_append(cand, s6_key(v, c), sm.y.cand, &sm.ncand, CAND, &sm.ovf);
-      s6_append(bd_e, c, sm.be_id, &sm.nband_e, S6_BAND, &sm.ovf);
+      bool cand[4], bd_e[4];
+      bool anyc = false, anyb = false;
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        const bool in_r = v[k] > fhr, in_e = v[k] > fhe;
+        cand[k] = v[k] >= flr;
+        bd_e[k] = !in_e && v[k] >= fle;
+        cnt_in_r += in_r;
+        cnt_in_e += in_e;
+        const unsigned mie = __ballot_sync(0xffffffffu, in_e);
+        if (lane == k && 4 * (base + 32 * warp) + k < m) tre[((base + 32 * warp) >> 5) * 4 + k] = mie;
+        anyc |= cand[k] && !in_r;
+        anyb |= bd_e[k];
+      }
+      if (anyc || anyb) {
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+          if ((cand[k] && !(v[k] > fhr)) || bd_e[k]) {
+            const char* row = reinterpret_cast<const char*>(C64 + (size_t)(4 * qi + k) * d);
+            for (int o = 0; o < d * 8; o += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(row + o));
+          }
+      }
+      if (__any_sync(0xffffffffu, cand[0] || cand[1] || cand[2] || cand[3])) {
+#pragma unroll
+        for (int k = 0; k < 4; k++) s6_append(cand[k], s6_key(v[k], 4 * qi + k), sm.y.cand, &sm.ncand, CAND, &sm.ovf);
+      }
+      if (__any_sync(0xffffffffu, anyb)) {
+#pragma unroll
+        for (int k = 0; k < 4; k++) s6_append(bd_e[k], 4 * qi + k, sm.be_id, &sm.nband_e, S6_BAND, &sm.ovf);
+      }
     }
+    cnt_in_r = __reduce_add_sync(0xffffffffu, cnt_in_r);
+    cnt_in_e = __reduce_add_sync(0xffffffffu, cnt_in_e);
     if (lane == 0) {
       atomicAdd(&sm.n_in_r, cnt_in_r);
       atomicAdd(&sm.n_in_e, cnt_in_e);
@@ -515,7 +540,7 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
         sm.x.f.fex[nin_r + before] = sm.y.cex[i];
       }
       for (int i = t; i < nbe; i += T)
-        if (sm.be_sel[i]) atomicOr(tre + (sm.be_id[i] >> 5), 1u << (sm.be_id[i] & 31));
+        if (sm.be_sel[i]) atomicOr(tre + zb_word(sm.be_id[i]), 1u << zb_bit(sm.be_id[i]));
       __syncthreads();
   S6_MARK(7);
       // every maximal run of approx-order neighbours closer than 2B was
@@ -548,7 +573,7 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
       for (int i = t; i < r; i += T) {
         const int c = s6_id(sm.x.f.fin[i]);
         rl_out[i] = c;
-        atomicOr(rbits + (c >> 5), 1u << (c & 31));
+        atomicOr(rbits + zb_word(c), 1u << zb_bit(c));
       }
       __syncthreads();
       // E = top(r+e) minus R
@@ -568,7 +593,7 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
         for (int w = t; w < W; w += T) {
           uint32_t ew = tre[w];
           while (ew) {
-            el_out[pos++] = (w << 5) + __ffs(ew) - 1;
+            el_out[pos++] = zb_cluster(w, __ffs(ew) - 1);
             ew &= ew - 1;
           }
         }
@@ -581,7 +606,7 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
         for (int c = t; c < m; c += T) {
           const float xv = S_(c) * isd;
           mx_a = fmaxf(mx_a, xv);
-          const bool z = ((rbits[c >> 5] | tre[c >> 5]) >> (c & 31)) & 1u;
+          const bool z = ((rbits[zb_word(c)] | tre[zb_word(c)]) >> zb_bit(c)) & 1u;
           if (!z) mx_t = fmaxf(mx_t, xv);
         }
         float dummy = 0.f;
@@ -591,7 +616,7 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
           const float xv = S_(c) * isd;
           const float sz = (float)csize[c];
           da += sz * expf(xv - mx_a);
-          const bool z = ((rbits[c >> 5] | tre[c >> 5]) >> (c & 31)) & 1u;
+          const bool z = ((rbits[zb_word(c)] | tre[zb_word(c)]) >> zb_bit(c)) & 1u;
           if (!z) dt += sz * expf(xv - mx_t);
         }
         float dz2 = -INFINITY;
@@ -622,7 +647,7 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
 }
 
 size_t select_v6_dyn_smem(int m_max, bool sms, int cand) {
-  const int W = (m_max + 31) >> 5;
+  const int W = zb_words(m_max);
   const size_t hdr = cand <= 512 ? sizeof(Sel6Smem<512>) : sizeof(Sel6Smem<2048>);
   return ((hdr + 15) & ~(size_t)15) + (size_t)(sms ? ((m_max + 3) & ~3) : 0) * 4 + (size_t)2 * W * 4;
 }

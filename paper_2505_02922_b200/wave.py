@@ -98,8 +98,8 @@ class WaveLayer:
         k_upd = math.ceil(ic.update_segment / ic.centroid_ratio)
         m_pref = sum(math.ceil(min(ic.segment_size, n_idx - s) / ic.centroid_ratio)
                      for s in range(0, n_idx, ic.segment_size))
-        # multiple of 32: float4 scans, 16-row C16 tiles, 32-bit zone bitmaps
-        self.m_cap = max(32, -(-(m_pref + n_upd * k_upd) // 32) * 32)
+        # multiple of 128: float4 scans, 16-row C16 tiles, zone bitmaps (4 words / 128 clusters)
+        self.m_cap = max(128, -(-(m_pref + n_upd * k_upd) // 128) * 128)
         self.s_cap = max(1, n_idx + n_upd * ic.update_segment)
         self.t_cap = ic.sink_tokens + ic.update_segment + ic.local_window + max(0, ic.local_window) + 8
         self.t_cap = max(self.t_cap, min(max_prefill, ic.sink_tokens + ic.local_window) + 8)
