@@ -172,7 +172,7 @@ static int launch_attend_v4(const IndexView& ix, const SteadyView& st, const Ste
   const int warps = attend_v4_warps<T, DPL, HS>();
   attend_v4_kernel<T, DPL, HS, FULL, OFF><<<P, warps * 32, sm, s>>>(ix, st, sv, p, n_store, U);
   if (cudaGetLastError() != cudaSuccess) return WK_ECUDA;
-  const int RG = HS == 4 ? 16 : 4;  // Att4Cfg::RG
+  const int RG = HS == 4 ? 16 : 8;  // Att4Cfg::RG
   att4_merge_kernel<FULL, DPL / 2><<<U * p.G, 128, 0, s>>>(st, sv, p, n_store, U, P * warps, RG);
   return cudaGetLastError() == cudaSuccess ? 0 : WK_ECUDA;
 }
@@ -284,7 +284,7 @@ int wk_score_topk(const wk_index_view* ix, const wk_step_view* sv, const wk_zone
     p.need_allc = zp->denominator_eq2;
     p.score_fp64 = 1;
     p.score_mode = tc ? 2 : 1;
-    p.piece_rows = head_slots(zp->G) == 4 ? 16 : 4;  // attend_v4 chunk rows (Att4Cfg::RG)
+    p.piece_rows = head_slots(zp->G) == 4 ? 16 : 8;  // attend_v4 chunk rows (Att4Cfg::RG)
     p.prof = g_sel_prof;
     p.k_new = nullptr; p.v_new = nullptr; p.store_bf16 = 0;
     if (g_append.on) { p.k_new = g_append.k; p.v_new = g_append.v; p.st = g_append.st; p.store_bf16 = g_append.bf16; }

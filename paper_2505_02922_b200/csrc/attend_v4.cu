@@ -77,7 +77,7 @@ WK_DEVINL float att4_treduce16(float (&v)[16]) {
 
 template <typename T, int DPL, int HS>
 struct Att4Cfg {
-  static constexpr int RG = HS == 4 ? 16 : 4;      // rows per chunk
+  static constexpr int RG = HS == 4 ? 16 : 8;      // rows per chunk
   static constexpr int NL = (RG / 2) * HS / 16;    // (row, head) logits per lane after the reduction
   static constexpr int NST = RG == 16 ? 2 : 3;     // ring stages per warp
   static constexpr int D = 16 * DPL;

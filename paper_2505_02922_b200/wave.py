@@ -108,7 +108,7 @@ class WaveLayer:
         # fast path (select_v6 / attend_v4 / score_v4): d in {64, 128}
         self.fast = d in (64, 128)
         hs = 4 if G <= 4 else 8
-        self.piece_rows = 16 if hs == 4 else 4  # attend_v4 chunk rows
+        self.piece_rows = 16 if hs == 4 else 8  # attend_v4 chunk rows
         if self.fast:
             sms = torch.cuda.get_device_properties(self.dev).multi_processor_count
             self.S = splits or max(1, min(sms, 4 * U))  # persistent attention grid: 1 CTA / SM

@@ -84,13 +84,15 @@ def test_engine_trace_matches_reference(name, store):
     assert lay.units[0].m == int(z["metrics"][-1][9])
 
 
-def test_batched_gqa_matches_per_head_oracle():
-    """U=2 units x G=4 heads, bf16 store, bf16-representable inputs: every
-    (unit, head) must equal an independent oracle HeadEngine."""
+@pytest.mark.parametrize("Gh,d", [(4, 128), (7, 128), (2, 64), (8, 64)])
+def test_batched_gqa_matches_per_head_oracle(Gh, d):
+    """U=2 units x G heads (Llama G=4, Qwen G=7, ...), bf16 store,
+    bf16-representable inputs: every (unit, head) must equal an independent
+    oracle HeadEngine (both head-slot widths of the attention kernel)."""
     from oracle import oracle as O
     from paper_2505_02922_b200 import EngineConfig, WaveLayer
-    rng = np.random.default_rng(11)
-    U, Gh, d, n, steps = 2, 4, 128, 3000, 6
+    rng = np.random.default_rng(11 + Gh)
+    U, n, steps = 2, 3000, 6
     cen = rng.standard_normal((40, d)).astype(np.float32)
     keys = G.bf16_round(cen[rng.integers(40, size=(U, n))] + 0.3 * rng.standard_normal((U, n, d)).astype(np.float32))
     vals = G.bf16_round(rng.standard_normal((U, n, d)).astype(np.float32))
