@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-flashinfer", action="store_true")
+    ap.add_argument("--build", action="store_true",
+                    help="configs[2]: segmented clustering index build at 120K and 256K, "
+                         "throughput + sampled assignment parity vs the CPU oracle")
     ap.add_argument("--offload", action="store_true",
                     help="configs[3]: host-KV offload (pinned store + HBM wave buffer); "
                          "use with e.g. --ctx 1048576 --batch 4")
@@ -241,6 +244,74 @@ def run_reference(a):
     print(json.dumps(line), flush=True)
 
 
+# -------------------------------------------------------------- build (config 3)
+def run_build(a, torch, dev, log):
+    """configs[2]: prefill index build (segmented spherical k-means, finalize,
+    store pack) of B x H_kv units at 122,880 and 262,144 tokens.  Throughput in
+    tokens/s and GFLOP/s (Lloyd 11 x 2Lkd + seeding 2Ld(k-1) per segment,
+    SURVEY 8(d)); assignment parity: sampled segments of unit 0 re-clustered by
+    the CPU oracle (tierkv's algorithm, oracle/) must match bit-for-bit."""
+    import numpy as np
+    from oracle import oracle as O
+    from paper_2505_02922_b200 import EngineConfig, WaveLayer
+    cfg = EngineConfig()
+    ic = cfg.index
+    G = HQ // HKV
+    U = a.batch * HKV
+    rows = []
+    for ctx in (122880, 262144):
+        keys, vals, _ = gen_layer(torch, U, ctx, D, 11, dev)
+        lay = WaveLayer(cfg, U, G, D, max_prefill=ctx, max_decode=64, store_dtype=torch.bfloat16)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        lay.prefill(keys, vals)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        n_idx = ctx - ic.sink_tokens - ic.local_window
+        flop = 0.0
+        for s0 in range(0, n_idx, ic.segment_size):
+            L = min(ic.segment_size, n_idx - s0)
+            k = math.ceil(L / ic.centroid_ratio)
+            flop += (ic.kmeans_iters + 1) * 2.0 * L * k * D + 2.0 * L * D * (k - 1)
+        flop *= U
+        # parity on sampled segments of unit 0 (first and last)
+        segs = list(range(0, n_idx, ic.segment_size))
+        sample = sorted({0, len(segs) - 1})
+        kh = keys[0].cpu().numpy()
+        tok = lay.store_tok[0].cpu().numpy()
+        off = lay.cl_off[0].cpu().numpy()
+        size = lay.cl_size[0].cpu().numpy()
+        ok, checked = True, 0
+        cid = 0
+        for si, s0 in enumerate(segs):
+            L = min(ic.segment_size, n_idx - s0)
+            k = math.ceil(L / ic.centroid_ratio)
+            if si in sample:
+                base = ic.sink_tokens + s0
+                ref = O.spherical_kmeans(kh[base:base + L], k, ic.kmeans_iters,
+                                         np.random.SeedSequence([ic.rng_seed, 1, si]))
+                mine = np.empty(L, np.int64)
+                for c in range(k):
+                    o, z = int(off[cid + c]), int(size[cid + c])
+                    mine[tok[o:o + z] - base] = c
+                ok &= bool(np.array_equal(mine, ref))
+                checked += L
+            cid += k
+        rows.append({"ctx": ctx, "units": U, "tokens": U * n_idx, "seconds": dt,
+                     "tokens_per_s": U * n_idx / dt, "gflop_per_s": flop / dt / 1e9,
+                     "segments": U * len(segs), "parity_segments_checked": len(sample),
+                     "parity_points_checked": checked, "assignment_parity": ok})
+        log(f"build ctx={ctx}: {dt:.2f}s, parity={ok}")
+        del keys, vals, lay
+        torch.cuda.empty_cache()
+    print(json.dumps({"metric": "prefill index build throughput (segmented spherical k-means), tokens/s",
+                      "impl": "wave-build", "unit": "tokens/s", "value": rows[0]["tokens_per_s"],
+                      "higher_is_better": True, "data": "synthetic",
+                      "config": {"workload": f"{a.model}-shape build, {a.batch} requests x {HKV} kv heads "
+                                             "(configs[2])", "kmeans_iters": ic.kmeans_iters},
+                      "runs": rows}), flush=True)
+
+
 # ----------------------------------------------------------- offload (config 4)
 def run_offload(a, torch, dev, log):
     """configs[3]: long context with the cluster store in pinned host memory
@@ -354,6 +425,8 @@ def main():
     log = lambda *x: print(*x, file=sys.stderr, flush=True) if rank == 0 else None
     if a.offload:
         return run_offload(a, torch, dev, log)
+    if a.build:
+        return run_build(a, torch, dev, log)
     G = HQ // HKV
     U = a.batch * HKV  # per-rank units (weak scaling: each rank serves `batch` requests)
     n_bufs = min(a.layer_bufs, a.layers)
