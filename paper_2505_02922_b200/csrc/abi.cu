@@ -13,6 +13,8 @@ __global__ void km_prep_kernel(const SegDesc*, float*, int);
 __global__ void km_seed_kernel(const SegDesc*, const float*, float*, float*, int, int, int);
 __global__ void km_seed_v2_kernel(const SegDesc*, const float*, float*, float*, int, int, int);
 __global__ void km_assign_kernel(const SegDesc*, const float*, const float*, int32_t*, int);
+template <int KS>
+__global__ void km_assign_tc_kernel(const SegDesc*, const float*, const float*, int32_t*);
 __global__ void km_assign_small_kernel(const SegDesc*, const float*, const float*, int32_t*, int);
 __global__ void km_update_kernel(const SegDesc*, const float*, float*, int32_t*, int32_t*, float*, int, int);
 template <typename T>
@@ -219,14 +221,22 @@ int wk_kmeans_segments(const wk_index_view* ix, const wk_segment* segs, int n_se
   }
   WK_CHECK_LAUNCH();
   const dim3 ag((max_L + 63) / 64, n_segs);
+  // Lloyd assignment: tensor-core first pass + exact verification when the
+  // head dim tiles by 16 (<= 128), else the exact FFMA kernel
+  auto assign = [&]() {
+    if (d == 128) km_assign_tc_kernel<8><<<ag, 128, 0, s>>>(sd, scr->P, scr->C, scr->A);
+    else if (d == 64) km_assign_tc_kernel<4><<<ag, 128, 0, s>>>(sd, scr->P, scr->C, scr->A);
+    else if (d == 32) km_assign_tc_kernel<2><<<ag, 128, 0, s>>>(sd, scr->P, scr->C, scr->A);
+    else km_assign_kernel<<<ag, 256, (size_t)2 * d * 65 * sizeof(float), s>>>(sd, scr->P, scr->C, scr->A, d);
+  };
   const size_t asmem = (size_t)2 * d * 65 * sizeof(float);
   const size_t usmem = (size_t)(2 * max_k + 1) * sizeof(int);
-  km_assign_kernel<<<ag, 256, asmem, s>>>(sd, scr->P, scr->C, scr->A, d);
+  assign();
   km_assign_small_kernel<<<n_segs, 256, 0, s>>>(sd, scr->P, scr->C, scr->A, d);
   WK_CHECK_LAUNCH();
   for (int it = 0; it < kmeans_iters; it++) {
     km_update_kernel<<<n_segs, 512, usmem, s>>>(sd, scr->P, scr->C, scr->A, scr->perm, scr->sims, d, 0);
-    km_assign_kernel<<<ag, 256, asmem, s>>>(sd, scr->P, scr->C, scr->A, d);
+    assign();
     km_assign_small_kernel<<<n_segs, 256, 0, s>>>(sd, scr->P, scr->C, scr->A, d);
     WK_CHECK_LAUNCH();
   }

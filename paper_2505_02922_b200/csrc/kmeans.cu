@@ -220,6 +220,172 @@ __global__ void __launch_bounds__(256) km_seed_v2_kernel(const SegDesc* __restri
 }
 
 // ---------------------------------------------------------------------------
+// phase 3 (tensor cores): assignment = argmax(points @ centroids.T), the
+// reference's sequential fp32 FMA chain per score (clustering.py:85,96), via
+// a tensor-core first pass + exact verification.
+//   * first pass: bf16x3 split products (p_hi c_hi + p_hi c_lo + p_lo c_hi) on
+//     mma.sync.m16n8k16 with fp32 accumulation; rows are unit vectors, so
+//     |s' - s_exact| <= B = 1e-4 for every (point, centroid) (split residuals
+//     3 * 2^-18, accumulation 384 * 2^-23, the reference chain's own gamma_128);
+//   * each lane keeps the top 4 s' of its rows; the quad merges them;
+//   * every centroid within 2B of the best s' is re-scored with the exact
+//     fp32 chain and the first index of the exact max wins (np.argmax); if
+//     the 4th candidate is still within 2B the point falls back to an exact
+//     scan of all centroids.
+// grid = (ceil(Lmax / 64), n_segments), block = 128 (4 warps x 16 points);
+// smem: a chunk of 64 centroids as bf16 hi / lo rows padded to 136 elements.
+// ---------------------------------------------------------------------------
+constexpr int KTC_CH = 64;     // centroids per smem chunk
+constexpr int KTC_PAD = 136;   // padded bf16 row (conflict-free B fragment loads)
+constexpr float KTC_B = 1e-4f;
+
+WK_DEVINL void ktc_mma(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+WK_DEVINL uint32_t ktc_pack(float x, float y) {
+  return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(x)) |
+         ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(y)) << 16);
+}
+WK_DEVINL void ktc_split(float x, float y, uint32_t& hi, uint32_t& lo) {
+  const float hx = __bfloat162float(__float2bfloat16_rn(x)), hy = __bfloat162float(__float2bfloat16_rn(y));
+  hi = ktc_pack(hx, hy);
+  lo = ktc_pack(x - hx, y - hy);
+}
+// insert (v, i) into a descending top-4 list
+WK_DEVINL void ktc_ins(float (&tv)[4], int (&ti)[4], float v, int i) {
+  if (!(v > tv[3])) return;
+  if (v > tv[2]) { tv[3] = tv[2]; ti[3] = ti[2]; } else { tv[3] = v; ti[3] = i; return; }
+  if (v > tv[1]) { tv[2] = tv[1]; ti[2] = ti[1]; } else { tv[2] = v; ti[2] = i; return; }
+  if (v > tv[0]) { tv[1] = tv[0]; ti[1] = ti[0]; tv[0] = v; ti[0] = i; } else { tv[1] = v; ti[1] = i; }
+}
+WK_DEVINL float ktc_exact(const float* __restrict__ p, const float* __restrict__ c, int d) {
+  float acc = 0.f;
+#pragma unroll 16
+  for (int t = 0; t < d; t++) acc = __fmaf_rn(__ldg(p + t), __ldg(c + t), acc);
+  return acc;
+}
+
+template <int KS>
+__global__ void __launch_bounds__(128) km_assign_tc_kernel(const SegDesc* __restrict__ segs,
+                                                            const float* __restrict__ P_all,
+                                                            const float* __restrict__ C_all,
+                                                            int32_t* __restrict__ A_all) {
+  constexpr int d = KS * 16;
+  const SegDesc sg = segs[blockIdx.y];
+  if (sg.k <= 1) return;
+  if ((long long)sg.L * sg.k <= 1200) return;  // OpenBLAS small-kernel shapes: km_assign_small_kernel
+  const int p0 = blockIdx.x * 64;
+  if (p0 >= sg.L) return;
+  __shared__ __align__(16) __nv_bfloat16 csh[2][KTC_CH][KTC_PAD];  // [hi/lo][centroid][dim]
+  const float* P = P_all + (size_t)sg.p_off * d;
+  const float* C = C_all + (size_t)sg.c_off * d;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+  const int r0 = p0 + warp * 16 + g, r1 = r0 + 8;  // this lane's two point rows
+  // A fragments (points, hi / lo), resident for the whole centroid loop
+  uint32_t ah[KS][4], al[KS][4];
+  {
+    const float* pr0 = P + (size_t)min(r0, sg.L - 1) * d;
+    const float* pr1 = P + (size_t)min(r1, sg.L - 1) * d;
+#pragma unroll
+    for (int s = 0; s < KS; s++) {
+      const int k0 = 16 * s + 2 * t;
+      const float2 x00 = *reinterpret_cast<const float2*>(pr0 + k0), x10 = *reinterpret_cast<const float2*>(pr1 + k0);
+      const float2 x01 = *reinterpret_cast<const float2*>(pr0 + k0 + 8), x11 = *reinterpret_cast<const float2*>(pr1 + k0 + 8);
+      ktc_split(x00.x, x00.y, ah[s][0], al[s][0]);
+      ktc_split(x10.x, x10.y, ah[s][1], al[s][1]);
+      ktc_split(x01.x, x01.y, ah[s][2], al[s][2]);
+      ktc_split(x11.x, x11.y, ah[s][3], al[s][3]);
+    }
+  }
+  float tv0[4], tv1[4];
+  int ti0[4], ti1[4];
+#pragma unroll
+  for (int i = 0; i < 4; i++) { tv0[i] = tv1[i] = -INFINITY; ti0[i] = ti1[i] = 0x7fffffff; }
+  for (int c0 = 0; c0 < sg.k; c0 += KTC_CH) {
+    const int nc = min(KTC_CH, sg.k - c0);
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < KTC_CH * (d / 2); idx += blockDim.x) {
+      const int c = idx / (d / 2), t2 = (idx % (d / 2)) * 2;
+      float2 x = make_float2(0.f, 0.f);
+      if (c < nc) x = *reinterpret_cast<const float2*>(C + (size_t)(c0 + c) * d + t2);
+      uint32_t hi, lo;
+      ktc_split(x.x, x.y, hi, lo);
+      *reinterpret_cast<uint32_t*>(&csh[0][c][t2]) = hi;
+      *reinterpret_cast<uint32_t*>(&csh[1][c][t2]) = lo;
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int nt = 0; nt < KTC_CH / 8; nt++) {
+      if (nt * 8 >= nc) break;
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      const int cn = nt * 8 + g;
+#pragma unroll
+      for (int s = 0; s < KS; s++) {
+        const int k0 = 16 * s + 2 * t;
+        const uint32_t bh0 = *reinterpret_cast<const uint32_t*>(&csh[0][cn][k0]);
+        const uint32_t bh1 = *reinterpret_cast<const uint32_t*>(&csh[0][cn][k0 + 8]);
+        const uint32_t bl0 = *reinterpret_cast<const uint32_t*>(&csh[1][cn][k0]);
+        const uint32_t bl1 = *reinterpret_cast<const uint32_t*>(&csh[1][cn][k0 + 8]);
+        ktc_mma(acc, ah[s], bh0, bh1);
+        ktc_mma(acc, ah[s], bl0, bl1);
+        ktc_mma(acc, al[s], bh0, bh1);
+      }
+      const int ca = c0 + nt * 8 + 2 * t;
+      if (nt * 8 + 2 * t < nc) { ktc_ins(tv0, ti0, acc[0], ca); ktc_ins(tv1, ti1, acc[2], ca); }
+      if (nt * 8 + 2 * t + 1 < nc) { ktc_ins(tv0, ti0, acc[1], ca + 1); ktc_ins(tv1, ti1, acc[3], ca + 1); }
+    }
+  }
+  // merge the quad's lists: every lane ends with the top 4 of its two rows
+#pragma unroll
+  for (int o = 1; o < 4; o <<= 1) {
+    float ov0[4], ov1[4];
+    int oi0[4], oi1[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      ov0[i] = __shfl_xor_sync(0xffffffffu, tv0[i], o); oi0[i] = __shfl_xor_sync(0xffffffffu, ti0[i], o);
+      ov1[i] = __shfl_xor_sync(0xffffffffu, tv1[i], o); oi1[i] = __shfl_xor_sync(0xffffffffu, ti1[i], o);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; i++) { ktc_ins(tv0, ti0, ov0[i], oi0[i]); ktc_ins(tv1, ti1, ov1[i], oi1[i]); }
+  }
+  // exact verification: lane t takes row r0 (t < 2) or r1 (t >= 2)
+  const int r = t < 2 ? r0 : r1;
+  if (r >= sg.L) return;
+  float tv[4];
+  int ti[4];
+#pragma unroll
+  for (int i = 0; i < 4; i++) { tv[i] = t < 2 ? tv0[i] : tv1[i]; ti[i] = t < 2 ? ti0[i] : ti1[i]; }
+  if ((t & 1) == 1) return;  // one lane per row
+  const float* pr = P + (size_t)r * d;
+  const float lim = tv[0] - 2.f * KTC_B;
+  float best = -INFINITY;
+  int bi = 0x7fffffff;
+  if (tv[3] >= lim) {
+    // too many near-ties for the list: exact scan of every centroid
+    for (int c = 0; c < sg.k; c++) {
+      const float v = ktc_exact(pr, C + (size_t)c * d, d);
+      if (v > best) { best = v; bi = c; }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      if (!(tv[i] >= lim)) break;
+      const float v = ktc_exact(pr, C + (size_t)ti[i] * d, d);
+      if (v > best || (v == best && ti[i] < bi)) { best = v; bi = ti[i]; }
+    }
+    if (bi == 0x7fffffff) bi = ti[0];  // non-finite scores: keep the first-pass winner
+  }
+  A_all[sg.p_off + r] = bi;
+}
+template __global__ void km_assign_tc_kernel<8>(const SegDesc*, const float*, const float*, int32_t*);
+template __global__ void km_assign_tc_kernel<4>(const SegDesc*, const float*, const float*, int32_t*);
+template __global__ void km_assign_tc_kernel<2>(const SegDesc*, const float*, const float*, int32_t*);
+
+// ---------------------------------------------------------------------------
 // phase 3: assignment = argmax(points @ centroids.T) (clustering.py:85,96).
 // Every score is the reference's sequential fp32 FMA chain over t; register
 // tiled 64 points x 64 centroids per CTA iteration, transposed smem tiles.
