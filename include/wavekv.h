@@ -69,6 +69,7 @@ typedef struct wk_build_scratch {
   float* md;          /* [2 * sum L] min-dist + cdf (k-means++ seeding)        */
   wk_segment* segs_dev; /* [n_segments] device copy of the descriptors         */
   int* status;        /* device status word                                    */
+  void* P16;          /* [sum L, d] fp16 copy of P: k-means++ first pass (may be NULL) */
 } wk_build_scratch;
 
 /* Steady zone: sinks + decode buffer per unit (engine.py:87-96). */

@@ -35,7 +35,7 @@ class SegmentC(ctypes.Structure):
 
 class BuildScratchC(ctypes.Structure):
     _fields_ = [("P", _P), ("C", _P), ("A", _P), ("perm", _P), ("sims", _P), ("md", _P),
-                ("segs_dev", _P), ("status", _P)]
+                ("segs_dev", _P), ("status", _P), ("P16", _P)]
 
 
 class SteadyViewC(ctypes.Structure):

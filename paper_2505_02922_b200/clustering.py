@@ -67,6 +67,7 @@ def spherical_kmeans(keys, k: int, iters: int, seed, device="cuda", threads=None
                          size.data_ptr(), c64.data_ptr(), c32.data_ptr(), cn.data_ptr(),
                          vs.data_ptr(), None, n, k)
     P = torch.empty((n, d), dtype=f32, device=dev)
+    P16 = torch.empty((n, d), dtype=torch.float16, device=dev)
     C = torch.empty((k, d), dtype=f32, device=dev)
     A = torch.zeros(n, dtype=i32, device=dev)
     perm = torch.empty(n, dtype=i32, device=dev)
@@ -81,7 +82,8 @@ def spherical_kmeans(keys, k: int, iters: int, seed, device="cuda", threads=None
     for t, w in enumerate(_seed_words(seed)):
         s.rng[t] = w
     scr = _lib.BuildScratchC(P.data_ptr(), C.data_ptr(), A.data_ptr(), perm.data_ptr(),
-                             sims.data_ptr(), md.data_ptr(), segs_dev.data_ptr(), status.data_ptr())
+                             sims.data_ptr(), md.data_ptr(), segs_dev.data_ptr(), status.data_ptr(),
+                             P16.data_ptr())
     rc = _lib.lib().wk_kmeans_segments(ctypes.byref(ix), seg, 1, ctypes.byref(scr), d, 0, iters,
                                        threads if threads is not None else _BLAS_THREADS, n, k,
                                        ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream))

@@ -9,9 +9,9 @@
 
 namespace wk {
 // kmeans.cu
-__global__ void km_prep_kernel(const SegDesc*, float*, int);
+__global__ void km_prep_kernel(const SegDesc*, float*, int, __half*);
 __global__ void km_seed_kernel(const SegDesc*, const float*, float*, float*, int, int, int);
-__global__ void km_seed_v2_kernel(const SegDesc*, const float*, float*, float*, int, int, int);
+__global__ void km_seed_v2_kernel(const SegDesc*, const float*, float*, float*, int, int, int, const __half*);
 __global__ void km_assign_kernel(const SegDesc*, const float*, const float*, int32_t*, int);
 template <int KS>
 __global__ void km_assign_tc_kernel(const SegDesc*, const float*, const float*, int32_t*);
@@ -205,14 +205,15 @@ int wk_kmeans_segments(const wk_index_view* ix, const wk_segment* segs, int n_se
   if (cudaMemcpyAsync(scr->segs_dev, segs, sizeof(wk_segment) * (size_t)n_segs, cudaMemcpyHostToDevice, s) != cudaSuccess)
     return WK_ECUDA;
   const SegDesc* sd = scr->segs_dev;
-  km_prep_kernel<<<n_segs, 256, d * sizeof(float), s>>>(sd, scr->P, d);
+  __half* p16 = (d % 16 == 0) ? (__half*)scr->P16 : nullptr;
+  km_prep_kernel<<<n_segs, 256, d * sizeof(float), s>>>(sd, scr->P, d, p16);
   WK_CHECK_LAUNCH();
   if ((d % 8) == 0) {
     // v2: 256 threads, <= 72 KB of smem so 3 segments share an SM
     const int smem_rows = ((72 * 1024) / 4 - d) / 2;
-    const size_t seed_smem = (size_t)(d + 2 * (max_L <= smem_rows ? max_L : 0)) * sizeof(float);
-    km_seed_v2_kernel<<<n_segs, 256, seed_smem, s>>>(sd, scr->P, scr->C, scr->md, d, blas_threads,
-                                                      max_L <= smem_rows ? smem_rows : 0);
+    const size_t seed_smem = (size_t)(d + 2 * (max_L <= smem_rows ? max_L + 3 : 0)) * sizeof(float);
+    km_seed_v2_kernel<<<n_segs, 256, seed_smem + 16, s>>>(sd, scr->P, scr->C, scr->md, d, blas_threads,
+                                                           max_L <= smem_rows ? smem_rows : 0, p16);
   } else {
     const int smem_rows = ((200 * 1024) / 4 - d) / 2;
     const size_t seed_smem = (size_t)(d + 2 * (max_L <= smem_rows ? max_L : 0)) * sizeof(float);

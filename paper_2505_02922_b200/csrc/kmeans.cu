@@ -14,7 +14,8 @@ namespace wk {
 // and normalize rows (clustering.py:82, :16-23).
 // grid = n_segments, block = 256
 // ---------------------------------------------------------------------------
-__global__ void km_prep_kernel(const SegDesc* __restrict__ segs, float* __restrict__ P_all, int d) {
+__global__ void km_prep_kernel(const SegDesc* __restrict__ segs, float* __restrict__ P_all, int d,
+                               __half* __restrict__ P16_all) {
   const SegDesc sg = segs[blockIdx.x];
   if (sg.k <= 1) return;
   extern __shared__ float sm_mean[];
@@ -39,6 +40,10 @@ __global__ void km_prep_kernel(const SegDesc* __restrict__ segs, float* __restri
     } else {
       for (int t = 0; t < d; t++) row[t] = 0.f;
       row[0] = 1.0f;
+    }
+    if (P16_all) {
+      __half* r16 = P16_all + ((size_t)sg.p_off + i) * d;
+      for (int t = 0; t < d; t++) r16[t] = __float2half_rn(row[t]);
     }
   }
 }
@@ -127,21 +132,24 @@ __global__ void km_seed_kernel(const SegDesc* __restrict__ segs, const float* __
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) km_seed_v2_kernel(const SegDesc* __restrict__ segs, const float* __restrict__ P_all,
                                                          float* __restrict__ C_all, float* __restrict__ scratch_all,
-                                                         int d, int blas_threads, int smem_rows) {
+                                                         int d, int blas_threads, int smem_rows,
+                                                         const __half* __restrict__ P16_all) {
   const SegDesc sg = segs[blockIdx.x];
   if (sg.k <= 1) return;
   extern __shared__ __align__(16) float sm2[];
   float* cent = sm2;  // d floats: current centroid
   const int L = sg.L;
   float *md, *cdf;
-  if (L <= smem_rows) {
+  const int L4 = (L + 3) & ~3;  // cdf 16-byte aligned
+  if (L + 3 <= smem_rows) {
     md = sm2 + d;
-    cdf = md + L;
+    cdf = md + L4;
   } else {
     md = scratch_all + (size_t)sg.p_off * 2;
     cdf = md + L;
   }
   const float* P = P_all + (size_t)sg.p_off * d;
+  const __half* P16 = P16_all ? P16_all + (size_t)sg.p_off * d : nullptr;
   float* C = C_all + (size_t)sg.c_off * d;
   __shared__ Pcg64 g;
   __shared__ long long s_idx;
@@ -166,7 +174,33 @@ __global__ void __launch_bounds__(256) km_seed_v2_kernel(const SegDesc* __restri
     if (c == sg.k - 1) break;
     for (int base = warp * 16; base < L; base += nwarp * 16) {
       const int i = base + rsub;
-      const bool act = i < L;
+      bool act = i < L;
+      if (act && c > 0 && P16) {
+        // first pass on the fp16 copy: |dot' - dot| <= 2^-11 + 2 gamma_d for
+        // unit rows, so v' - 1e-3 >= md[i] proves min(md, v) == md (no update)
+        const uint4* r16 = reinterpret_cast<const uint4*>(P16 + (size_t)i * d) + h * (nq / 2);
+        float a = 0.f;
+        uint4 wv[8];
+#pragma unroll
+        for (int q = 0; q < 8; q++) wv[q] = q < nq / 2 ? __ldcg(r16 + q) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+          if (q >= nq / 2) break;
+          const uint4 w = wv[q];
+          const __half2* hh = reinterpret_cast<const __half2*>(&w);
+          const float* cc = cent + h * (d / 2) + 8 * q;
+#pragma unroll
+          for (int e2 = 0; e2 < 4; e2++) {
+            const float2 f = __half22float2(hh[e2]);
+            a = fmaf(f.x, cc[2 * e2], a);
+            a = fmaf(f.y, cc[2 * e2 + 1], a);
+          }
+        }
+        const unsigned pm16 = __activemask() & (0x3u << (lane & ~1));
+        a += __shfl_xor_sync(pm16, a, 1);
+        const float vq = 1.0f - a;
+        if (vq - 1e-3f >= md[i]) act = false;
+      }
       const int cls = act ? gemv_row_class(i, L, d, blas_threads) : 0;
       float dot = 0.f;
       const unsigned both = __ballot_sync(0xffffffffu, act && cls == 0);
@@ -174,9 +208,13 @@ __global__ void __launch_bounds__(256) km_seed_v2_kernel(const SegDesc* __restri
         const float4* row = reinterpret_cast<const float4*>(P + (size_t)i * d) + h;
         const float4* cv = reinterpret_cast<const float4*>(cent) + h;
         float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-#pragma unroll 4
-        for (int q = 0; q < nq; q++) {
-          const float4 x = __ldcg(row + 2 * q), y = cv[2 * q];
+        float4 xv[16];
+#pragma unroll
+        for (int q = 0; q < 16; q++) xv[q] = q < nq ? __ldcg(row + 2 * q) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < 16; q++) {
+          if (q >= nq) break;
+          const float4 x = xv[q], y = cv[2 * q];
           a0 = __fmaf_rn(x.x, y.x, a0);
           a1 = __fmaf_rn(x.y, y.y, a1);
           a2 = __fmaf_rn(x.z, y.z, a2);
@@ -200,9 +238,27 @@ __global__ void __launch_bounds__(256) km_seed_v2_kernel(const SegDesc* __restri
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      float sacc = md[0];
-      cdf[0] = sacc;
-      for (int i = 1; i < L; i++) { sacc = __fadd_rn(sacc, md[i]); cdf[i] = sacc; }
+      // the reference's sequential fp32 cumsum; register-batched (float4 in,
+      // float4 out, no load/store aliasing) so it runs at the FADD latency
+      float sacc = 0.f;  // 0 + md[0] == md[0] (md >= +0)
+      if (L == L4 && cdf == md + L4) {
+        const float4* __restrict__ m4 = reinterpret_cast<const float4*>(md);
+        float4* __restrict__ c4 = reinterpret_cast<float4*>(cdf);
+#pragma unroll 4
+        for (int q = 0; q < L4 / 4; q++) {
+          const float4 v = m4[q];
+          float4 o;
+          sacc = __fadd_rn(sacc, v.x); o.x = sacc;
+          sacc = __fadd_rn(sacc, v.y); o.y = sacc;
+          sacc = __fadd_rn(sacc, v.z); o.z = sacc;
+          sacc = __fadd_rn(sacc, v.w); o.w = sacc;
+          c4[q] = o;
+        }
+      } else {
+        const float* __restrict__ m1 = md;
+        float* __restrict__ c1 = cdf;
+        for (int i = 0; i < L; i++) { sacc = __fadd_rn(sacc, m1[i]); c1[i] = sacc; }
+      }
       long long nidx;
       if (sacc <= 0.0f) {
         nidx = pcg_integers(g, L);

@@ -246,6 +246,7 @@ class WaveLayer:
             sumK = sum(max(1, s["k"]) for s in chunk)
             dev = self.dev
             P = torch.empty((sumL, d), dtype=torch.float32, device=dev)
+            P16 = torch.empty((sumL, d), dtype=torch.float16, device=dev)
             C = torch.empty((sumK, d), dtype=torch.float32, device=dev)
             A = torch.zeros(sumL, dtype=torch.int32, device=dev)
             perm = torch.empty(sumL, dtype=torch.int32, device=dev)
@@ -265,7 +266,7 @@ class WaveLayer:
                     a.rng[t] = s["rng"][t]
                 po += s["L"]; co += max(1, s["k"])
             scr = _lib.BuildScratchC(_ptr(P), _ptr(C), _ptr(A), _ptr(perm), _ptr(sims), _ptr(md),
-                                     _ptr(segs_dev), _ptr(self.status))
+                                     _ptr(segs_dev), _ptr(self.status), _ptr(P16))
             rc = self.L.wk_kmeans_segments(
                 ctypes.byref(self._ixv), arr, len(chunk), ctypes.byref(scr), d, self.store_bf16,
                 self.cfg.index.kmeans_iters, self.blas_threads, max(s["L"] for s in chunk),
@@ -273,7 +274,7 @@ class WaveLayer:
             _lib.check(rc, "wk_kmeans_segments")
             # keep scratch alive until the kernels ran
             torch.cuda.current_stream().synchronize()
-            del P, C, A, perm, sims, md, segs_dev
+            del P, P16, C, A, perm, sims, md, segs_dev
 
     # ------------------------------------------------------------------ prefill
     def prefill(self, keys: torch.Tensor, values: torch.Tensor, lengths=None):
