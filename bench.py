@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-flashinfer", action="store_true")
+    ap.add_argument("--split", type=int, default=1, help="unit groups pipelined on streams")
     ap.add_argument("--build", action="store_true",
                     help="configs[2]: segmented clustering index build at 120K and 256K, "
                          "throughput + sampled assignment parity vs the CPU oracle")
@@ -437,7 +438,8 @@ def main():
     t_build = 0.0
     for li in range(n_bufs):
         keys, vals, cen = gen_layer(torch, U, a.ctx, D, 1000 * rank + li, dev)
-        lay = WaveLayer(cfg, U, G, D, max_prefill=a.ctx, max_decode=64, store_dtype=torch.bfloat16)
+        lay = WaveLayer(cfg, U, G, D, max_prefill=a.ctx, max_decode=64, store_dtype=torch.bfloat16,
+                        split=a.split)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         lay.prefill(keys, vals)

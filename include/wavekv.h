@@ -249,6 +249,15 @@ int wk_decode_step(const wk_index_view* ix, const wk_steady_view* st, const wk_s
                    const wk_zone_params* zp, const float* k_new, const float* v_new, int U, int m_max, int S,
                    int store_bf16, void* stream);
 
+/* The two halves of wk_score_topk, for pipelining unit groups on streams:
+ * the centroid scan (HBM-bound) and the exact zone planning + unions
+ * (latency-bound; optionally with the fused token append). */
+int wk_centroid_scan(const wk_index_view* ix, const wk_step_view* sv, const wk_zone_params* zp, int U, int m_max,
+                     void* stream);
+int wk_plan_zones(const wk_index_view* ix, const wk_steady_view* st, const wk_step_view* sv,
+                  const wk_zone_params* zp, const float* k_new, const float* v_new, int U, int m_max,
+                  int store_bf16, void* stream);
+
 /* Offload cache step + attention pieces for U kv-head units (one CTA each). */
 int wk_cache_offload_step(const wk_cache2_view* cv, const wk_index_view* ix, const wk_steady_view* st,
                           const wk_step_view* sv, int G, int64_t step, int U, void* stream);

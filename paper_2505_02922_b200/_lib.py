@@ -86,7 +86,8 @@ _lib = None
 # every symbol include/wavekv.h declares
 EXPORTS = ("wk_version", "wk_kmeans_segments", "wk_append_tokens", "wk_score_topk",
            "wk_tripartite_attn", "wk_full_attn", "wk_cache_step", "wk_recall_at_k",
-           "wk_cache_offload_step", "wk_host_alloc", "wk_host_free", "wk_decode_step")
+           "wk_cache_offload_step", "wk_host_alloc", "wk_host_free", "wk_decode_step",
+           "wk_centroid_scan", "wk_plan_zones")
 
 
 def lib():
@@ -118,6 +119,9 @@ def lib():
                                         ctypes.c_int, _I64, ctypes.c_int, _P]
     L.wk_decode_step.argtypes = [R(IndexViewC), R(SteadyViewC), R(StepViewC), R(ZoneParamsC), _P, _P,
                                  ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _P]
+    L.wk_centroid_scan.argtypes = [R(IndexViewC), R(StepViewC), R(ZoneParamsC), ctypes.c_int, ctypes.c_int, _P]
+    L.wk_plan_zones.argtypes = [R(IndexViewC), R(SteadyViewC), R(StepViewC), R(ZoneParamsC), _P, _P,
+                                ctypes.c_int, ctypes.c_int, ctypes.c_int, _P]
     L.wk_host_alloc.argtypes = [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]
     L.wk_host_free.argtypes = [_P]
     for name in EXPORTS:

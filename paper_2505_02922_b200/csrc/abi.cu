@@ -98,6 +98,7 @@ static int sm_count() {
   return n;
 }
 static int g_sel_prof = 0;
+static thread_local int g_phases = 3;  // wk_score_topk phases: 1 = centroid scan, 2 = zone planning
 // wk_decode_step hands the token append to wk_score_topk's select kernel
 struct AppendArgs { int on; const float* k; const float* v; SteadyView st; int bf16; };
 static thread_local AppendArgs g_append = {0, nullptr, nullptr, {}, 0};
@@ -273,7 +274,7 @@ int wk_score_topk(const wk_index_view* ix, const wk_step_view* sv, const wk_zone
   if (v6_ok(ix, sv, zp->d)) {
     const bool tc = zp->score_mode == 2 && ix->C16 && ix->Cscale;
     int rc = 0;
-    if (m_max > 0) {
+    if (m_max > 0 && (g_phases & 1)) {
       const int nt = zp->G <= 4 ? 1 : 2;
       if (tc) {
         if (zp->d == 128) rc = nt == 1 ? launch_score_v4<8, 1>(*ix, *sv, zp->G, U, m_max, s)
@@ -299,7 +300,7 @@ int wk_score_topk(const wk_index_view* ix, const wk_step_view* sv, const wk_zone
     p.prof = g_sel_prof;
     p.k_new = nullptr; p.v_new = nullptr; p.store_bf16 = 0;
     if (g_append.on) { p.k_new = g_append.k; p.v_new = g_append.v; p.st = g_append.st; p.store_bf16 = g_append.bf16; }
-    return launch_select_v6(*ix, *sv, p, U, m_max, s);
+    return (g_phases & 2) ? launch_select_v6(*ix, *sv, p, U, m_max, s) : 0;
   }
   if (m_max > 0) {
     dim3 g1((m_max + 63) / 64, U);
@@ -415,6 +416,27 @@ int wk_decode_step(const wk_index_view* ix, const wk_steady_view* st, const wk_s
   g_append.on = 0;
   if (rc) return rc;
   return wk_tripartite_attn(ix, st, sv, zp, U, S, store_bf16, stream);
+}
+
+int wk_centroid_scan(const wk_index_view* ix, const wk_step_view* sv, const wk_zone_params* zp, int U, int m_max,
+                     void* stream) {
+  if (!ix || !sv || !zp || !v6_ok(ix, sv, zp->d)) return WK_ECONFIG;
+  g_phases = 1;
+  const int rc = wk_score_topk(ix, sv, zp, U, m_max, stream);
+  g_phases = 3;
+  return rc;
+}
+
+int wk_plan_zones(const wk_index_view* ix, const wk_steady_view* st, const wk_step_view* sv,
+                  const wk_zone_params* zp, const float* k_new, const float* v_new, int U, int m_max,
+                  int store_bf16, void* stream) {
+  if (!ix || !sv || !zp || !v6_ok(ix, sv, zp->d)) return WK_ECONFIG;
+  g_phases = 2;
+  if (k_new && v_new && st) g_append = {1, k_new, v_new, *st, store_bf16};
+  const int rc = wk_score_topk(ix, sv, zp, U, m_max, stream);
+  g_append.on = 0;
+  g_phases = 3;
+  return rc;
 }
 
 int wk_host_alloc(size_t bytes, void** ptr) {

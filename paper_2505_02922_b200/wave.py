@@ -75,7 +75,8 @@ class WaveLayer:
     def __init__(self, cfg: EngineConfig, U: int, G: int, d: int, *, max_prefill: int,
                  max_decode: int = 1024, store_dtype=torch.bfloat16, device="cuda",
                  blas_threads: int = 1, splits: int | None = None, keep_vs64: bool = False,
-                 with_elist: bool = False, score_mode: int | None = None, offload: bool = False):
+                 with_elist: bool = False, score_mode: int | None = None, offload: bool = False,
+                 split: int = 1):
         self.cfg = cfg.validate()
         ic = cfg.index
         if d <= 0 or d % 4 or d > 256:
@@ -213,9 +214,85 @@ class WaveLayer:
         if self.offload:
             from .block_cache import OffloadCache
             self.cache = OffloadCache(self)
+        # split > 1: the units are processed in groups on separate streams so the
+        # latency-bound zone planning of one group overlaps the HBM-bound
+        # centroid scan of the next (in-HBM fast path only)
+        self.split = int(split) if (self.fast and not self.offload and U >= 2 * int(split)) else 1
+        self._groups = []
+        if self.split > 1:
+            for gi in range(self.split):
+                u0, u1 = U * gi // self.split, U * (gi + 1) // self.split
+                n = u1 - u0
+                part = torch.zeros((self.S * self.attn_warps + n, 3, G, 4 + d), dtype=f32, device=dev)
+                woff = torch.zeros(n + 1, dtype=i32, device=dev)
+                self._groups.append(dict(u0=u0, n=n, part=part, woff=woff,
+                                         ixv=self._index_view(u0, u1), stv=self._steady_view(u0, u1)))
+            self._streams = [torch.cuda.Stream(device=dev) for _ in range(self.split)]
         self.prefilled = False
 
     # ------------------------------------------------------------------ views
+    def _index_view(self, u0, u1):
+        sl = lambda t: None if t is None else t[u0:u1]
+        return _lib.IndexViewC(
+            _ptr(sl(self.store_k)), _ptr(sl(self.store_v)), _ptr(sl(self.store_tok)), _ptr(sl(self.cl_off)),
+            _ptr(sl(self.cl_size)), _ptr(sl(self.C64)), _ptr(sl(self.C32)), _ptr(sl(self.Cnorm)),
+            _ptr(sl(self.VS32)), _ptr(sl(self.VS64)), self.s_cap, self.m_cap, _ptr(sl(self.Cmax)),
+            _ptr(sl(self.C16)), _ptr(sl(self.Cscale)))
+
+    def _steady_view(self, u0, u1):
+        return _lib.SteadyViewC(_ptr(self.st_k[u0:u1]), _ptr(self.st_v[u0:u1]), _ptr(self.st_tok[u0:u1]),
+                                _ptr(self.st_n[u0:u1]), _ptr(self.next_tok[u0:u1]), self.t_cap)
+
+    def _group_step_view(self, grp, q):
+        u0, u1 = grp["u0"], grp["u0"] + grp["n"]
+        sl = lambda t: None if t is None else t[u0:u1]
+        return _lib.StepViewC(
+            _ptr(q[u0:u1]), _ptr(sl(self.m_dev)), _ptr(sl(self.scores)), _ptr(sl(self.rlist)), _ptr(sl(self.elist)),
+            _ptr(sl(self.nr)), _ptr(sl(self.ne)), None, _ptr(sl(self.ru_ids)), _ptr(sl(self.ru_mask)),
+            None, _ptr(sl(self.eu_ids)), _ptr(sl(self.eu_mask)), _ptr(sl(self.cnt)),
+            _ptr(sl(self.tail)), _ptr(grp["part"]), _ptr(sl(self.out)), _ptr(sl(self.logden)), _ptr(sl(self.cov)),
+            _ptr(self.status), self.r_cap, self.e_cap, self.ru_cap, self.eu_cap,
+            None, None, _ptr(sl(self.sel_done)), 0, 0,
+            _ptr(sl(self.eu_x)), _ptr(sl(self.eu_sz)), _ptr(sl(self.rbits)), _ptr(sl(self.ebits)), _ptr(sl(self.pieces)),
+            _ptr(grp["woff"]), self.w_cap, self.pc_cap, None, None, None, None, 0, 0, 0, 2)
+
+    def _launch_split(self, q, k_new, v_new, m_max):
+        """Two-stream pipeline over unit groups: scan(g) -> plan(g) -> attention(g),
+        with scan(g+1) issued after scan(g) so it overlaps plan(g)."""
+        L = self.L
+        main = torch.cuda.current_stream()
+        if not hasattr(self, "_ev"):
+            self._ev = [torch.cuda.Event() for _ in range(2 * self.split + 1)]
+            self._hs = [ctypes.c_void_p(st.cuda_stream) for st in self._streams]
+        ev = self._ev
+        ev[0].record(main)
+        qp = q.data_ptr()
+        gsz = self.G * self.d * 4
+        for gi, grp in enumerate(self._groups):
+            st = self._streams[gi]
+            st.wait_event(ev[0])
+            if gi:
+                st.wait_event(ev[gi])
+            sv = grp.get("sv")
+            if sv is None:
+                sv = grp["sv"] = self._group_step_view(grp, q)
+            sv.q = qp + grp["u0"] * gsz
+            _lib.check(L.wk_centroid_scan(ctypes.byref(grp["ixv"]), ctypes.byref(sv), ctypes.byref(self._zp),
+                                          grp["n"], m_max, self._hs[gi]), "wk_centroid_scan")
+            ev[gi + 1].record(st)
+        kp, vp, dsz = k_new.data_ptr(), v_new.data_ptr(), self.d * 4
+        for gi, grp in enumerate(self._groups):
+            n, u0, h = grp["n"], grp["u0"], self._hs[gi]
+            _lib.check(L.wk_plan_zones(ctypes.byref(grp["ixv"]), ctypes.byref(grp["stv"]), ctypes.byref(grp["sv"]),
+                                       ctypes.byref(self._zp), kp + u0 * dsz, vp + u0 * dsz,
+                                       n, m_max, self.store_bf16, h), "wk_plan_zones")
+            _lib.check(L.wk_tripartite_attn(ctypes.byref(grp["ixv"]), ctypes.byref(grp["stv"]),
+                                            ctypes.byref(grp["sv"]), ctypes.byref(self._zp), n, self.S,
+                                            self.store_bf16, h), "wk_tripartite_attn")
+            ev[self.split + 1 + gi].record(self._streams[gi])
+        for gi in range(self.split):
+            main.wait_event(ev[self.split + 1 + gi])
+
     def _step_view(self, q: torch.Tensor) -> _lib.StepViewC:
         return _lib.StepViewC(
             _ptr(q), _ptr(self.m_dev), _ptr(self.scores), _ptr(self.rlist), _ptr(self.elist),
@@ -360,6 +437,11 @@ class WaveLayer:
         L = self.L
         sv = self._step_view(q)
         m_max = max(s.m for s in self.units)
+        if self.split > 1:
+            k_new = k_new if (k_new.dtype == torch.float32 and k_new.is_contiguous()) else k_new.float().contiguous()
+            v_new = v_new if (v_new.dtype == torch.float32 and v_new.is_contiguous()) else v_new.float().contiguous()
+            self._launch_split(q, k_new, v_new, m_max)
+            return
         if self.cache is None:  # one fused call: append + scan + zones + attention
             _lib.check(L.wk_decode_step(ctypes.byref(self._ixv), ctypes.byref(self._stv), ctypes.byref(sv),
                                         ctypes.byref(self._zp), _ptr(k_new), _ptr(v_new), self.U, m_max,

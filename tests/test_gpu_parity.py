@@ -137,3 +137,30 @@ def test_full_attention_matches_fp64():
             w = np.exp(s - s.max())
             ref = (w @ vals[u].astype(np.float64)) / w.sum()
             assert np.linalg.norm(out[u, g] - ref) <= 1e-5 * np.linalg.norm(ref)
+
+
+def test_split_pipeline_matches_single_launch():
+    """split=2 (unit groups on two streams, scan of one group overlapping the
+    zone planning of the other) gives the same zones and outputs."""
+    from paper_2505_02922_b200 import EngineConfig, WaveLayer
+    rng = np.random.default_rng(21)
+    U, Gh, d, n, steps = 6, 4, 128, 3000, 5
+    cen = rng.standard_normal((40, d)).astype(np.float32)
+    keys = G.bf16_round(cen[rng.integers(40, size=(U, n))] + 0.3 * rng.standard_normal((U, n, d)).astype(np.float32))
+    vals = G.bf16_round(rng.standard_normal((U, n, d)).astype(np.float32))
+    dev = torch.device("cuda")
+    lays = [WaveLayer(EngineConfig(), U, Gh, d, max_prefill=n, max_decode=64, split=sp) for sp in (1, 2)]
+    assert lays[1].split == 2
+    for lay in lays:
+        lay.prefill(torch.from_numpy(keys).to(dev), torch.from_numpy(vals).to(dev))
+    for t in range(steps):
+        q = torch.from_numpy(G.bf16_round(rng.standard_normal((U, Gh, d)).astype(np.float32))).to(dev)
+        k = torch.from_numpy(G.bf16_round(rng.standard_normal((U, d)).astype(np.float32))).to(dev)
+        v = torch.from_numpy(G.bf16_round(rng.standard_normal((U, d)).astype(np.float32))).to(dev)
+        outs = [lay.decode(q, k, v)[0].clone() for lay in lays]
+        torch.cuda.synchronize()
+        for lay in lays:
+            lay.check_status()
+        assert torch.equal(lays[0].rlist, lays[1].rlist)
+        a, b = outs[0].double(), outs[1].double()
+        assert float((a - b).norm() / b.norm()) <= 1e-6, t
