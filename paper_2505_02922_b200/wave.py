@@ -429,13 +429,21 @@ class WaveLayer:
             self.maybe_update()
         return self.out, self.logden, self.cov
 
-    def launch_step(self, q, k_new, v_new):
-        """Kernel launches of one decode step only (graph-capturable)."""
+    def launch_step(self, q, k_new, v_new, out=None):
+        """Kernel launches of one decode step only (graph-capturable).  ``out``:
+        optional [U, G, d] float32 device tensor the attention output is written
+        to instead of ``self.out``."""
         q = q if (q.dtype == torch.float32 and q.is_contiguous()) else q.float().contiguous()
         self._q = q
         stream = ctypes.c_void_p(_stream())
         L = self.L
         sv = self._step_view(q)
+        if out is not None:
+            if out.dtype != torch.float32 or not out.is_contiguous() or out.shape != self.out.shape:
+                raise ConfigError(f"out must be a contiguous float32 {tuple(self.out.shape)} tensor")
+            if self.split > 1:
+                raise ConfigError("out= is not supported with split > 1")
+            sv.out = _ptr(out)
         m_max = max(s.m for s in self.units)
         if self.split > 1:
             k_new = k_new if (k_new.dtype == torch.float32 and k_new.is_contiguous()) else k_new.float().contiguous()

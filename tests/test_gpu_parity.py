@@ -164,3 +164,29 @@ def test_split_pipeline_matches_single_launch():
         assert torch.equal(lays[0].rlist, lays[1].rlist)
         a, b = outs[0].double(), outs[1].double()
         assert float((a - b).norm() / b.norm()) <= 1e-6, t
+
+
+def test_launch_step_out_argument():
+    """launch_step(out=...) writes the attention output to the caller's tensor,
+    bit-identical to the layer's own output buffer (the pipelined e2e path)."""
+    from paper_2505_02922_b200 import EngineConfig, WaveLayer
+    from paper_2505_02922_b200.errors import ConfigError
+    rng = np.random.default_rng(5)
+    U, Gh, d, n = 4, 4, 128, 2500
+    keys = G.bf16_round(rng.standard_normal((U, n, d)).astype(np.float32))
+    vals = G.bf16_round(rng.standard_normal((U, n, d)).astype(np.float32))
+    dev = torch.device("cuda")
+    lays = [WaveLayer(EngineConfig(), U, Gh, d, max_prefill=n, max_decode=16) for _ in range(2)]
+    for lay in lays:
+        lay.prefill(torch.from_numpy(keys).to(dev), torch.from_numpy(vals).to(dev))
+    mine = torch.full((U, Gh, d), float("nan"), device=dev)
+    for t in range(3):
+        q = torch.from_numpy(G.bf16_round(rng.standard_normal((U, Gh, d)).astype(np.float32))).to(dev)
+        k = torch.from_numpy(G.bf16_round(rng.standard_normal((U, d)).astype(np.float32))).to(dev)
+        v = torch.from_numpy(G.bf16_round(rng.standard_normal((U, d)).astype(np.float32))).to(dev)
+        lays[0].launch_step(q, k, v)
+        lays[1].launch_step(q, k, v, out=mine)
+        torch.cuda.synchronize()
+        assert torch.equal(lays[0].out, mine), t
+    with pytest.raises(ConfigError):
+        lays[1].launch_step(q, k, v, out=mine[:2])
