@@ -149,15 +149,32 @@ static int launch_select_v6(const IndexView& ix, const StepView& sv, const SelPa
     cfg = 1;
   }
   if (m_max > 262144) return WK_ECONFIG;
-  if (m_max <= 16384 && r_max <= 480)
-    select_v6_kernel<512, true><<<blocks, 256, select_v6_dyn_smem(m_max, true, 512), s>>>(ix, sv, p);
-  else if (r_max <= 480)
-    select_v6_kernel<512, false><<<blocks, 256, select_v6_dyn_smem(m_max, false, 512), s>>>(ix, sv, p);
-  else if (r_max <= 1900)
-    select_v6_kernel<2048, false><<<blocks, 256, select_v6_dyn_smem(m_max, false, 2048), s>>>(ix, sv, p);
-  else
+  // the G CTAs of a unit form one thread-block cluster (the union runs over DSMEM)
+  cudaLaunchConfig_t lc = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = p.G;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.gridDim = dim3(blocks);
+  lc.blockDim = dim3(256);
+  lc.stream = s;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  cudaError_t e;
+  if (m_max <= 16384 && r_max <= 480) {
+    lc.dynamicSmemBytes = select_v6_dyn_smem(m_max, true, 512);
+    e = cudaLaunchKernelEx(&lc, select_v6_kernel<512, true>, ix, sv, p);
+  } else if (r_max <= 480) {
+    lc.dynamicSmemBytes = select_v6_dyn_smem(m_max, false, 512);
+    e = cudaLaunchKernelEx(&lc, select_v6_kernel<512, false>, ix, sv, p);
+  } else if (r_max <= 1900) {
+    lc.dynamicSmemBytes = select_v6_dyn_smem(m_max, false, 2048);
+    e = cudaLaunchKernelEx(&lc, select_v6_kernel<2048, false>, ix, sv, p);
+  } else {
     return WK_ECONFIG;
-  return cudaGetLastError() == cudaSuccess ? 0 : WK_ECUDA;
+  }
+  return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? 0 : WK_ECUDA;
 }
 
 template <typename T, int DPL, int HS, bool FULL, bool OFF>
@@ -338,8 +355,7 @@ int wk_tripartite_attn(const wk_index_view* ix, const wk_steady_view* st, const 
   p.denominator_eq2 = zp->denominator_eq2;
   dim3 grid(S, U);
   if (v6_ok(ix, sv, zp->d)) {
-    att4_est_prep_kernel<<<dim3((sv->eu_cap + 255) / 256, U), 256, 0, s>>>(*ix, *sv, zp->G, p.inv_sqrt_d);
-    WK_CHECK_LAUNCH();
+    // estimation rows (eu_x, eu_sz) were filled by select_v6's cluster union
     return store_bf16 ? dispatch_attend_v4<__nv_bfloat16, false>(*ix, *st, *sv, p, nullptr, U, S, s)
                       : dispatch_attend_v4<float, false>(*ix, *st, *sv, p, nullptr, U, S, s);
   }

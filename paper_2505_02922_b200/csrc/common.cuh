@@ -270,6 +270,21 @@ WK_DEVINL double score_error_bound_v2(double qnorm2, double cmax, int d, int mod
 // permuted layout so one warp ballot over 32 lanes x float4 covers a word:
 // cluster c <-> word ((c >> 7) << 2) | (c & 3), bit (c >> 2) & 31.
 // Words per unit: 4 * ceil(m / 128).
+// distributed shared memory (thread-block clusters): 32-bit shared::cluster
+// address of `p` (a shared-memory object of this CTA) in CTA `rank` of the
+// cluster -- all CTAs of a kernel share the layout -- and a 32-bit load.
+WK_DEVINL uint32_t dsmem_addr(const void* p, int rank) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
+  uint32_t r;
+  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+WK_DEVINL uint32_t dsmem_ld_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+
 __host__ __device__ __forceinline__ int zb_word(int c) { return ((c >> 7) << 2) | (c & 3); }
 __host__ __device__ __forceinline__ int zb_bit(int c) { return (c >> 2) & 31; }
 __host__ __device__ __forceinline__ int zb_cluster(int w, int b) { return ((w >> 2) << 7) | (b << 2) | (w & 3); }

@@ -22,6 +22,8 @@
 #include "common.cuh"
 #include "decode_internal.h"
 
+#include <cooperative_groups.h>
+
 namespace wk {
 
 __device__ long long g_sel_dbg[4096][16];  // per-CTA phase timestamps (globaltimer, ns), SelParams.prof
@@ -48,9 +50,10 @@ struct Sel6Smem {
   double be_ex[S6_BAND];
   unsigned char be_sel[S6_BAND];
   float red[3][S6_NW];
-  int wsum[4][S6_NW];
+  int wsum[4][S6_NW + 1];
   int ncand, n_in_r, nband_e, n_in_e, nx, ovf, last, b1, b2;
   int base[4];
+  int ctot[4];                      // union: this CTA's slice totals (read by peers)
   float fred[3];
 };
 
@@ -176,86 +179,251 @@ WK_DEVINL double s6_exact_quad(const double* __restrict__ row, const float* __re
 
 // ---------------------------------------------------------------------------
 // union of the unit's G zone bitmaps -> attend_v4 work lists
+//
+// The G CTAs of a unit form a thread-block cluster.  Once every head's R / E
+// bitmaps are final in its shared memory, CTA g takes the g-th slice of the
+// bitmap words (whole 128-cluster groups), per tile of S6_TWC clusters:
+//   * one coalesced round trip stages the tile's cluster sizes / store
+//     offsets, one DSMEM round trip copies all G heads' R / E words of the
+//     tile into local smem;
+//   * pass 1 counts (clusters, tokens, pieces, estimation rows) -- one warp
+//     per word, one lane per bit; the CTA totals are exchanged over DSMEM for
+//     the slice's output base;
+//   * pass 2 emits retrieval pieces (runs of <= piece_rows contiguous store
+//     rows of one cluster + head mask) and estimation rows (id, head mask,
+//     size), in (word, bit) order -- the order of a single-CTA union;
+//   * after a cluster barrier, CTA h writes head h's estimation logits
+//     s'(c) / sqrt(d) of every estimation row from its own staged scores.
 // ---------------------------------------------------------------------------
-template <int CAND>
-__device__ void s6_union(const IndexView& ix, const StepView& sv, const SelParams& p, int u, int m,
-                         Sel6Smem<CAND>& sm) {
-  const int G = p.G, T = S6_T, t = threadIdx.x;
-  const int W = zb_words(m);
-  const int w0 = (int)((long long)W * t / T), w1 = (int)((long long)W * (t + 1) / T);
-  const uint32_t* rb = sv.rbits + (size_t)u * G * sv.w_cap;
-  const uint32_t* eb = sv.ebits + (size_t)u * G * sv.w_cap;
+constexpr int S6_TWC = 2048;            // clusters per staging tile
+constexpr int S6_TWW = S6_TWC / 32;     // bitmap words per tile (16 groups)
+
+template <int CAND, bool SMS>
+__device__ void s6_union_cl(const IndexView& ix, const StepView& sv, const SelParams& p, int u, int g, int m,
+                            Sel6Smem<CAND>& sm, uint32_t* rbits, uint32_t* tre, float* scs) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int G = p.G, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int W = zb_words(m), NGR = W >> 2;
+  const int cw0 = (NGR * g / G) << 2, cw1 = (NGR * (g + 1) / G) << 2;
+  const int ntile = (cw1 - cw0 + S6_TWW - 1) / S6_TWW;
   const int* csize = ix.cl_size + (size_t)u * ix.m_cap;
   const int* coff = ix.cl_off + (size_t)u * ix.m_cap;
+  // staging (the select phases' dead smem): sizes | offsets | words [2][G][S6_TWW]
+  static_assert(offsetof(Sel6Smem<CAND>, red) - offsetof(Sel6Smem<CAND>, x) >=
+                    (2 * S6_TWC + 2 * 8 * S6_TWW) * sizeof(int), "union staging must fit the dead select smem");
+  int* csz = reinterpret_cast<int*>(&sm.x);
+  int* cof = csz + S6_TWC;
+  uint32_t* lw = reinterpret_cast<uint32_t*>(cof + S6_TWC);  // [R/E][h][word - tw0]
+  const uint32_t rb_loc = (uint32_t)__cvta_generic_to_shared(rbits);
+  const uint32_t tr_loc = (uint32_t)__cvta_generic_to_shared(tre);
+  auto peer = [&](uint32_t loc, int h) {
+    uint32_t r;
+    asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(loc), "r"(h));
+    return r;
+  };
   const int PR = p.piece_rows;
-  // pass 1: counts (clusters, tokens, pieces, estimation rows)
-  int v[4] = {0, 0, 0, 0};
-  for (int w = w0; w < w1; w++) {
-    uint32_t ur = 0u, ue = 0u;
-    for (int g = 0; g < G; g++) { ur |= __ldcg(rb + (size_t)g * sv.w_cap + w); ue |= __ldcg(eb + (size_t)g * sv.w_cap + w); }
-    v[0] += __popc(ur);
-    v[3] += __popc(ue);
-    while (ur) {
-      const int c = zb_cluster(w, __ffs(ur) - 1);
-      ur &= ur - 1;
-      const int s = __ldg(csize + c);
-      v[1] += s;
-      v[2] += (s + PR - 1) / PR;
+  auto stage = [&](int tw0, int tw1) {  // clusters [32 tw0, 32 tw1) + every head's words, one round trip
+    constexpr int K = S6_TWC / S6_T;
+    const int c0 = tw0 << 5, c1 = min(m, tw1 << 5), nw = tw1 - tw0;
+    int a[K], b[K];
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+      const int c = c0 + t + k * S6_T;
+      a[k] = c < c1 ? __ldg(csize + c) : 0;
+      b[k] = c < c1 ? __ldg(coff + c) : 0;
     }
+    uint32_t wv[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {  // 2 * G * nw <= 2 * 8 * 64 = 4 * S6_T
+      const int i = t + k * S6_T, e = i / (G * S6_TWW), h = (i / S6_TWW) % G, w = i % S6_TWW;
+      wv[k] = (i < 2 * G * S6_TWW && w < nw) ? dsmem_ld_u32(peer((e ? tr_loc : rb_loc) + 4u * (tw0 + w), h)) : 0u;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+      csz[t + k * S6_T] = a[k];
+      cof[t + k * S6_T] = b[k];
+    }
+#pragma unroll
+    for (int k = 0; k < 4; k++)
+      if (t + k * S6_T < 2 * G * S6_TWW) lw[t + k * S6_T] = wv[k];
+    __syncthreads();
+  };
+  // this warp's words of tile [tw0, tw1): contiguous block
+  auto wrange = [&](int tw0, int tw1, int& a, int& b) {
+    const int n = tw1 - tw0;
+    a = tw0 + n * warp / S6_NW;
+    b = tw0 + n * (warp + 1) / S6_NW;
+  };
+  auto load_words = [&](int wl, uint32_t (&rw)[8], uint32_t (&ew)[8], uint32_t& ur, uint32_t& ue) {
+    ur = 0u; ue = 0u;
+#pragma unroll
+    for (int h = 0; h < 8; h++) {
+      rw[h] = h < G ? lw[h * S6_TWW + wl] : 0u;
+      ew[h] = h < G ? lw[(G + h) * S6_TWW + wl] : 0u;
+      ur |= rw[h];
+      ue |= ew[h];
+    }
+  };
+  // per-warp counts over its words of a tile: (clusters, tokens, pieces, est rows)
+  auto count = [&](int tw0, int tw1, int (&c4)[4]) {
+    int a, b;
+    wrange(tw0, tw1, a, b);
+    int nr = 0, ne = 0, tok = 0, pcs = 0;
+    for (int w = a; w < b; w++) {
+      uint32_t rw[8], ew[8], ur, ue;
+      load_words(w - tw0, rw, ew, ur, ue);
+      nr += __popc(ur);
+      ne += __popc(ue);
+      if ((ur >> lane) & 1u) {
+        const int sz = csz[zb_cluster(w, lane) - (tw0 << 5)];
+        tok += sz;
+        pcs += (sz + PR - 1) / PR;
+      }
+    }
+    c4[0] = nr; c4[1] = tok; c4[2] = pcs; c4[3] = ne;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      c4[1] += __shfl_xor_sync(0xffffffffu, c4[1], o);
+      c4[2] += __shfl_xor_sync(0xffffffffu, c4[2], o);
+    }
+  };
+  // ---- pass 1: slice totals ----
+  int wc[4] = {0, 0, 0, 0};
+  if (t < 4) sm.ctot[t] = 0;
+  for (int k = 0; k < ntile; k++) {
+    const int tw0 = cw0 + k * S6_TWW, tw1 = min(cw1, tw0 + S6_TWW);
+    stage(tw0, tw1);
+    count(tw0, tw1, wc);
+    if (lane < 4) atomicAdd(&sm.ctot[lane], wc[lane]);
   }
-  int tot[4];
-  s6_scan4(v, tot, sm);
-  const int n_ru = tot[0], n_rt = tot[1], n_pc = tot[2], n_eu = tot[3];
+  // ---- slice bases from the peers' totals (DSMEM) ----
+  cl.sync();
+  if (t < 4) {
+    int base = 0, tot = 0;
+    const uint32_t loc = (uint32_t)__cvta_generic_to_shared(&sm.ctot[t]);
+    for (int h = 0; h < G; h++) {
+      const int v = (int)dsmem_ld_u32(peer(loc, h));
+      if (h < g) base += v;
+      tot += v;
+    }
+    sm.base[t] = base;
+    sm.wsum[t][0] = tot;
+  }
+  __syncthreads();
+  S6_MARK(15);
+  const int n_ru = sm.wsum[0][0], n_rt = sm.wsum[1][0], n_pc = sm.wsum[2][0], n_eu = sm.wsum[3][0];
   const bool fits = n_pc <= sv.pc_cap && n_eu <= sv.eu_cap && n_ru <= sv.ru_cap;
-  if (!fits) set_status(sv.status, kErrUnion);
-  // pass 2: emit
+  if (g == 0 && t == 0) {
+    if (!fits) set_status(sv.status, kErrUnion);
+    sv.cnt[u * 4 + 0] = fits ? n_ru : 0;
+    sv.cnt[u * 4 + 1] = fits ? n_rt : 0;
+    sv.cnt[u * 4 + 2] = fits ? n_eu : 0;
+    sv.cnt[u * 4 + 3] = fits ? n_pc : 0;
+  }
+  // ---- pass 2: emit ----
   int2* pcs = reinterpret_cast<int2*>(sv.pieces) + (size_t)u * sv.pc_cap;
   int32_t* ru = sv.ru_ids + (size_t)u * sv.ru_cap;
   uint8_t* rmk = sv.ru_mask + (size_t)u * sv.ru_cap;
   int32_t* eu = sv.eu_ids + (size_t)u * sv.eu_cap;
   uint8_t* emk = sv.eu_mask + (size_t)u * sv.eu_cap;
-  int ir = v[0], ipc = v[2], ie = v[3];
-  if (fits) {
-    for (int w = w0; w < w1; w++) {
-      uint32_t rw[8], ew[8];
-      uint32_t ur = 0u, ue = 0u;
+  float* eusz = sv.eu_sz + (size_t)u * sv.eu_cap;
+  int tb[4] = {sm.base[0], sm.base[1], sm.base[2], sm.base[3]};  // running tile base
+  const uint32_t lt = (1u << lane) - 1u;
+  for (int k = 0; fits && k < ntile; k++) {
+    const int tw0 = cw0 + k * S6_TWW, tw1 = min(cw1, tw0 + S6_TWW);
+    if (ntile > 1) {
+      stage(tw0, tw1);
+      count(tw0, tw1, wc);
+    }
+    __syncthreads();
+    if (lane < 4) sm.wsum[lane][warp + 1] = wc[lane];  // wsum[i][1..NW]: per-warp counts
+    __syncthreads();
+    int o[4], ttot[4];
 #pragma unroll
-      for (int g = 0; g < 8; g++) {
-        rw[g] = g < G ? __ldcg(rb + (size_t)g * sv.w_cap + w) : 0u;
-        ew[g] = g < G ? __ldcg(eb + (size_t)g * sv.w_cap + w) : 0u;
-        ur |= rw[g];
-        ue |= ew[g];
+    for (int i = 0; i < 4; i++) {
+      int ex = 0, all = 0;
+      for (int w2 = 0; w2 < S6_NW; w2++) {
+        const int v = sm.wsum[i][w2 + 1];
+        if (w2 < warp) ex += v;
+        all += v;
       }
-      while (ur) {
-        const int bit = __ffs(ur) - 1;
-        ur &= ur - 1;
-        const int c = zb_cluster(w, bit);
-        int mk = 0;
+      o[i] = tb[i] + ex;
+      ttot[i] = all;
+    }
+    int a, b;
+    wrange(tw0, tw1, a, b);
+    S6_MARK(13);
+    for (int w = a; w < b; w++) {
+      uint32_t rw[8], ew[8], ur, ue;
+      load_words(w - tw0, rw, ew, ur, ue);
+      const int c = zb_cluster(w, lane);
+      const int ci = c - (tw0 << 5);
+      if (ur) {
+        const bool in = (ur >> lane) & 1u;
+        const int sz = in ? csz[ci] : 0;
+        const int np = (sz + PR - 1) / PR;
+        int x = np;
 #pragma unroll
-        for (int g = 0; g < 8; g++) mk |= ((rw[g] >> bit) & 1u) << g;
-        const int s = __ldg(csize + c), o = __ldg(coff + c);
-        ru[ir] = c;
-        rmk[ir] = (uint8_t)mk;
-        ir++;
-        for (int j = 0; j < s; j += PR) pcs[ipc++] = make_int2(o + j, min(PR, s - j) | (mk << 8));
+        for (int off = 1; off < 32; off <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, x, off);
+          if (lane >= off) x += y;
+        }
+        if (in) {
+          int mk = 0;
+#pragma unroll
+          for (int h = 0; h < 8; h++) mk |= ((rw[h] >> lane) & 1u) << h;
+          const int ir = o[0] + __popc(ur & lt);
+          ru[ir] = c;
+          rmk[ir] = (uint8_t)mk;
+          const int r0 = cof[ci];
+          int ip = o[2] + x - np;
+          for (int j = 0; j < sz; j += PR) pcs[ip++] = make_int2(r0 + j, min(PR, sz - j) | (mk << 8));
+        }
+        o[0] += __popc(ur);
+        o[2] += __shfl_sync(0xffffffffu, x, 31);
       }
-      while (ue) {
-        const int bit = __ffs(ue) - 1;
-        ue &= ue - 1;
-        int mk = 0;
+      if (ue) {
+        if ((ue >> lane) & 1u) {
+          int mk = 0;
 #pragma unroll
-        for (int g = 0; g < 8; g++) mk |= ((ew[g] >> bit) & 1u) << g;
-        eu[ie] = zb_cluster(w, bit);
-        emk[ie] = (uint8_t)mk;
-        ie++;
+          for (int h = 0; h < 8; h++) mk |= ((ew[h] >> lane) & 1u) << h;
+          const int ie = o[3] + __popc(ue & lt);
+          eu[ie] = c;
+          emk[ie] = (uint8_t)mk;
+          eusz[ie] = (float)csz[ci];
+        }
+        o[3] += __popc(ue);
       }
     }
+    S6_MARK(14);
+#pragma unroll
+    for (int i = 0; i < 4; i++) tb[i] += ttot[i];
   }
-  if (t == 0) {
-    sv.cnt[u * 4 + 0] = fits ? n_ru : 0;
-    sv.cnt[u * 4 + 1] = fits ? n_rt : 0;
-    sv.cnt[u * 4 + 2] = fits ? n_eu : 0;
-    sv.cnt[u * 4 + 3] = fits ? n_pc : 0;
+  // ---- head g's estimation logits of every row (own staged scores) ----
+  cl.sync();  // all rows emitted (cluster-scope release / acquire); peers done with this CTA's smem
+  if (!fits) return;
+  float* eux = sv.eu_x + (size_t)u * sv.eu_cap * G + g;
+  const float isd = p.inv_sqrt_d;
+  const float* sg = sv.scores + ((size_t)u * G + g) * ix.m_cap;
+  constexpr int UN = 4;
+  for (int i0 = t; i0 < n_eu; i0 += UN * S6_T) {
+    int cc[UN], mm[UN];
+#pragma unroll
+    for (int k = 0; k < UN; k++) {
+      const int i = i0 + k * S6_T;
+      cc[k] = i < n_eu ? __ldcg(eu + i) : 0;
+      mm[k] = i < n_eu ? (int)__ldcg(emk + i) : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < UN; k++) {
+      const int i = i0 + k * S6_T;
+      if (i < n_eu) {
+        const float sc = (mm[k] >> g) & 1 ? (SMS ? scs[cc[k]] : __ldcg(sg + cc[k])) : 0.f;
+        eux[(size_t)i * G] = (mm[k] >> g) & 1 ? sc * isd : -INFINITY;
+      }
+    }
   }
 }
 
@@ -628,22 +796,16 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
   }
   if (m > 0 && !ok) {
     set_status(sv.status, kErrBandOverflow);
-    for (int w = t; w < W; w += T) { rb_out[w] = 0u; eb_out[w] = 0u; }
+    for (int w = t; w < W; w += T) { rb_out[w] = 0u; eb_out[w] = 0u; rbits[w] = 0u; tre[w] = 0u; }
   }
   if (!ok && t == 0) { tailp[0] = -INFINITY; tailp[1] = 0.f; tailp[2] = -INFINITY; tailp[3] = 0.f; }
   S6_MARK(9);
-  // ---- the last CTA of the unit builds the union ----
-  __threadfence();
-  __syncthreads();
-  if (t == 0) sm.last = (atomicAdd(sv.sel_done + u, 1) == G - 1);
-  __syncthreads();
-  if (!sm.last) return;
-  __threadfence();
-  if (t == 0) sv.sel_done[u] = 0;
+  // ---- the unit's G CTAs (one cluster) build the union together ----
+  cooperative_groups::this_cluster().sync();  // every head's R / E bitmaps final in its smem
   S6_MARK(10);
-  s6_union(ix, sv, p, u, m, sm);
+  s6_union_cl<CAND, SMS>(ix, sv, p, u, g, m, sm, rbits, tre, scs);
   S6_MARK(11);
-  if (p.prof && t == 0) { g_sel_dbg[blockIdx.x][12] = sm.ncand; g_sel_dbg[blockIdx.x][13] = sm.nx; g_sel_dbg[blockIdx.x][14] = sm.nband_e; }
+  if (p.prof && t == 0) { g_sel_dbg[blockIdx.x][12] = sm.ncand; }
 }
 
 size_t select_v6_dyn_smem(int m_max, bool sms, int cand) {

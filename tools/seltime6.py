@@ -40,6 +40,10 @@ for i in range(12):
     if len(v):
         print(f"{i:2d} {names[i]:18s} med {np.median(v - t0) / 1e3:8.1f} max {np.max(v - t0) / 1e3:8.1f} n={len(v)}")
 d = o[:, 1:10] - o[:, 0:9]
+for i, nm in ((15, "union pass1+xchg"), (13, "pass2 word loop start"), (14, "pass2 word loop end")):
+    v = o[:, i]
+    if (v > 1e9).any():
+        print(f"{i} {nm} med {np.median(v[v > 1e9] - t0) / 1e3:8.1f} max {np.max(v[v > 1e9] - t0) / 1e3:8.1f}")
 print("per-phase median durations (us):", np.round(np.median(d, axis=0) / 1e3, 2))
 print("ncand/nx/nband_e median", np.median(o[:, 12]), np.median(o[:, 13]), np.median(o[:, 14]),
       "max", o[:, 12].max(), o[:, 13].max(), o[:, 14].max())
