@@ -29,7 +29,8 @@ def up_to_date() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB
-    cmd = [NVCC, *FLAGS, os.path.join(CSRC, "wavekv.cu"), "-o", LIB + ".tmp"]
+    extra = os.environ.get("WK_EXTRA_NVCC_FLAGS", "").split()  # tuning experiments only
+    cmd = [NVCC, *FLAGS, *extra, os.path.join(CSRC, "wavekv.cu"), "-o", LIB + ".tmp"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     res = subprocess.run(cmd, capture_output=True, text=True)
