@@ -10,6 +10,9 @@ batched multi-request / GQA engine is ``WaveLayer``.
 from .config import EngineConfig, IndexConfig, round_half_up
 from .errors import ConfigError, IntegrityError, TierKVError, TraceFormatError
 from .clustering import spherical_kmeans
+from .engine import HeadEngine, StepMetrics, relative_l2
+from .runner import TraceEngine, oracle_trace, run_trace
+from .tracefile import TraceFile, read_trace, write_trace
 from .wave import WaveLayer
 
 __version__ = "0.1.0"
