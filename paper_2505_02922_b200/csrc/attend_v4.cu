@@ -576,94 +576,113 @@ __global__ void __launch_bounds__(128) att4_merge_kernel(SteadyView st, StepView
     w = wk0[k] + i - (k == 0 ? 0 : (k == 1 ? nk[0] : nk[0] + nk[1]));
   };
   auto rec = [&](int k, int w) { return sv.part + (((size_t)(w + u) * 3 + k) * G + g) * (size_t)D2; };
-  auto live_w = [&](int w) { return N * w / Wtot < N * (w + 1) / Wtot; };  // empty ranges wrote nothing
-  // pass 1: per-kind max over all items (thread-parallel)
-  float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY;
-  for (int i = t; i < S; i += 128) {
+  // empty ranges wrote nothing; with at least one chunk per warp every range is live (no division)
+  const bool all_live = N >= (long long)Wtot;
+  auto live_w = [&](int w) { return all_live || N * w / Wtot < N * (w + 1) / Wtot; };
+  // one pass: warp w folds its items i = w, w + 4, ... against per-warp, per-kind
+  // maxima (the value rows of the first 8 items are loaded together with the
+  // (M, D) words -- one round trip); warps are combined in shared memory.
+  const int Sw = (S - warp + 3) / 4;  // items of this warp
+  float mw[3] = {-INFINITY, -INFINITY, -INFINITY}, dw3[3] = {0.f, 0.f, 0.f};
+  float nacc[3][DL];
+#pragma unroll
+  for (int k = 0; k < 3; k++)
+#pragma unroll
+    for (int j = 0; j < DL; j++) nacc[k][j] = 0.f;
+  auto vload = [&](int i, float (&v)[DL]) {
     int k, w;
     item(i, k, w);
-    if (!live_w(w)) continue;
-    const float* r = rec(k, w);
-    if (__ldcg(r + 1) > 0.f) {
-      const float M = __ldcg(r);
-      if (k == 0) m0 = fmaxf(m0, M); else if (k == 1) m1 = fmaxf(m1, M); else m2 = fmaxf(m2, M);
+    const float* src = rec(k, w) + 4 + lane * DL;
+    if (DL == 4) {
+      const float4 x = __ldcg(reinterpret_cast<const float4*>(src));
+      v[0] = x.x; v[1] = x.y; v[2 % DL] = x.z; v[3 % DL] = x.w;
+    } else {
+      const float2 x = __ldcg(reinterpret_cast<const float2*>(src));
+      v[0] = x.x; v[1 % DL] = x.y;
     }
-  }
-  m0 = warp_max(m0); m1 = warp_max(m1); m2 = warp_max(m2);
-  if (lane == 0) { s_m[0][warp] = m0; s_m[1][warp] = m1; s_m[2][warp] = m2; }
-  __syncthreads();
-  m0 = fmaxf(fmaxf(s_m[0][0], s_m[0][1]), fmaxf(s_m[0][2], s_m[0][3]));
-  m1 = fmaxf(fmaxf(s_m[1][0], s_m[1][1]), fmaxf(s_m[1][2], s_m[1][3]));
-  m2 = fmaxf(fmaxf(s_m[2][0], s_m[2][1]), fmaxf(s_m[2][2], s_m[2][3]));
-  // pass 2: warp w folds items i = w, w + 4, ... (scales lane-parallel, loads unrolled)
-  float d0 = 0.f, d1 = 0.f, d2 = 0.f;
-  float n0[DL], n1[DL], n2[DL];
-#pragma unroll
-  for (int j = 0; j < DL; j++) n0[j] = n1[j] = n2[j] = 0.f;
-  const int Sw = (S - warp + 3) / 4;  // items of this warp
+  };
+  constexpr int PF = 8;
   for (int i0 = 0; i0 < Sw; i0 += 32) {
-    float sc = 0.f;
-    {
-      const int ii = i0 + lane;
-      if (ii < Sw) {
-        int k, w;
-        item(warp + 4 * ii, k, w);
-        if (live_w(w)) {
-          const float* r = rec(k, w);
-          const float dw = __ldcg(r + 1);
-          const float mk = k == 0 ? m0 : (k == 1 ? m1 : m2);
-          if (dw > 0.f) {
-            sc = __expf(__ldcg(r) - mk);
-            if (k == 0) d0 += dw * sc; else if (k == 1) d1 += dw * sc; else d2 += dw * sc;
-          }
-        }
+    const int nw = min(32, Sw - i0);
+    float pv[PF][DL];
+#pragma unroll
+    for (int j = 0; j < PF; j++)
+      if (j < nw) vload(warp + 4 * (i0 + j), pv[j]);
+    float M = -INFINITY, Dw = 0.f;
+    int kl = 0;
+    if (lane < nw) {
+      int w;
+      item(warp + 4 * (i0 + lane), kl, w);
+      if (live_w(w)) {
+        const float* r = rec(kl, w);
+        Dw = __ldcg(r + 1);
+        M = Dw > 0.f ? __ldcg(r) : -INFINITY;
       }
     }
-    const int nw = min(32, Sw - i0);
-#pragma unroll 8
-    for (int j = 0; j < nw; j++) {
-      const float swt = __shfl_sync(0xffffffffu, sc, j);
-      int k, w;
-      item(warp + 4 * (i0 + j), k, w);
-      const float* src = rec(k, w) + 4 + lane * DL;
-      float v[DL];
-      if (DL == 4) {
-        const float4 x = __ldcg(reinterpret_cast<const float4*>(src));
-        v[0] = x.x; v[1] = x.y; v[2 % DL] = x.z; v[3 % DL] = x.w;
-      } else {
-        const float2 x = __ldcg(reinterpret_cast<const float2*>(src));
-        v[0] = x.x; v[1 % DL] = x.y;
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+      const float bm = warp_max(kl == k ? M : -INFINITY);
+      if (bm > mw[k]) {  // raise the running maximum of kind k (first batch: from -inf)
+        const float alpha = mw[k] == -INFINITY ? 0.f : expf(mw[k] - bm);
+        dw3[k] *= alpha;
+#pragma unroll
+        for (int j = 0; j < DL; j++) nacc[k][j] *= alpha;
+        mw[k] = bm;
       }
+    }
+    const float mk = kl == 0 ? mw[0] : (kl == 1 ? mw[1] : mw[2]);
+    const float sc = Dw > 0.f ? __expf(M - mk) : 0.f;
+    if (kl == 0) dw3[0] += Dw * sc; else if (kl == 1) dw3[1] += Dw * sc; else dw3[2] += Dw * sc;
+    auto fold = [&](int j, const float (&v)[DL]) {
+      const float swt = __shfl_sync(0xffffffffu, sc, j);
+      const int kj = __shfl_sync(0xffffffffu, kl, j);
       // partials of empty-range warps may hold stale bits: weight 0 selects them out
 #pragma unroll
       for (int jj = 0; jj < DL; jj++) {
         const float add = swt != 0.f ? v[jj] * swt : 0.f;
-        n0[jj] += k == 0 ? add : 0.f;
-        n1[jj] += k == 1 ? add : 0.f;
-        n2[jj] += k == 2 ? add : 0.f;
+        nacc[0][jj] += kj == 0 ? add : 0.f;
+        nacc[1][jj] += kj == 1 ? add : 0.f;
+        nacc[2][jj] += kj == 2 ? add : 0.f;
       }
+    };
+#pragma unroll
+    for (int j = 0; j < PF; j++)
+      if (j < nw) fold(j, pv[j]);
+    for (int j = PF; j < nw; j++) {
+      float v[DL];
+      vload(warp + 4 * (i0 + j), v);
+      fold(j, v);
     }
   }
-  d0 = warp_sum(d0); d1 = warp_sum(d1); d2 = warp_sum(d2);
-  if (lane == 0) { s_d[0][warp] = d0; s_d[1][warp] = d1; s_d[2][warp] = d2; }
+#pragma unroll
+  for (int k = 0; k < 3; k++) dw3[k] = warp_sum(dw3[k]);
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < 3; k++) { s_m[k][warp] = mw[k]; s_d[k][warp] = dw3[k]; }
+  }
 #pragma unroll
   for (int jj = 0; jj < DL; jj++) {
-    s_n[0][warp][lane * DL + jj] = n0[jj];
-    s_n[1][warp][lane * DL + jj] = n1[jj];
-    s_n[2][warp][lane * DL + jj] = n2[jj];
+    s_n[0][warp][lane * DL + jj] = nacc[0][jj];
+    s_n[1][warp][lane * DL + jj] = nacc[1][jj];
+    s_n[2][warp][lane * DL + jj] = nacc[2][jj];
   }
   __syncthreads();
   if (warp != 0) return;
-  double kM[3] = {m0, m1, m2};
+  double kM[3];
   double kD[3];
   float num[3][DL];
 #pragma unroll
   for (int k = 0; k < 3; k++) {
-    kD[k] = (double)s_d[k][0] + s_d[k][1] + s_d[k][2] + s_d[k][3];
+    const float m = fmaxf(fmaxf(s_m[k][0], s_m[k][1]), fmaxf(s_m[k][2], s_m[k][3]));
+    kM[k] = m;
+    float f[4];
+#pragma unroll
+    for (int w = 0; w < 4; w++) f[w] = s_m[k][w] == -INFINITY ? 0.f : expf(s_m[k][w] - m);
+    kD[k] = (double)(s_d[k][0] * f[0]) + s_d[k][1] * f[1] + s_d[k][2] * f[2] + s_d[k][3] * f[3];
 #pragma unroll
     for (int jj = 0; jj < DL; jj++) {
       const int o = lane * DL + jj;
-      num[k][jj] = ((s_n[k][0][o] + s_n[k][1][o]) + (s_n[k][2][o] + s_n[k][3][o]));
+      num[k][jj] = ((s_n[k][0][o] * f[0] + s_n[k][1][o] * f[1]) + (s_n[k][2][o] * f[2] + s_n[k][3][o] * f[3]));
     }
   }
   const float zero4[4] = {-INFINITY, 0.f, -INFINITY, 0.f};
