@@ -29,8 +29,7 @@ HQ, HKV, D = 32, 8, 128
 # head shapes of the BASELINE configs (configs[1] Llama-3-8B, configs[4] Qwen2.5-7B)
 MODELS = {"llama3-8b": (32, 8, 128, 32), "qwen2.5-7b": (28, 4, 128, 28)}
 METRIC = "decode tokens/sec at 120K ctx (device-timed) and % HBM roofline vs full attn"
-# kernels per layer and step: score_v5, select_v6 (+ fused append), est_prep, attend_v4, merge
-LAUNCHES_PER_LAYER = 5
+LAUNCHES_PER_LAYER = 4  # score_v5, select_v6 (+ fused append, union, estimation prep), attend_v4, att4_merge
 
 
 def parse():
@@ -556,7 +555,7 @@ def main():
     achieved = attn_bytes / (t_attn / 1e3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
+    if os.path.exists(tp) and a.model == "llama3-8b":  # captured on the configs[1] workload only
         traffic = json.load(open(tp)).get("wk_tripartite_attn")
 
     # ---- full-attention comparators (same batch, heads, context, bf16 KV) ----
@@ -660,7 +659,7 @@ def main():
             "full_attention_own_kernel": fa_block,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "wk_tripartite_attn (est-prep + attend_v4 + merge)",
+                         "kernel": "wk_tripartite_attn (attend_v4 + att4_merge)",
                          "bytes_per_launch": attn_bytes, "ms_per_launch": t_attn},
             "step_roofline": {"bytes_per_step": step_bytes, "achieved": step_bytes / (ms / 1e3) / 1e9,
                               "frac": step_bytes / (ms / 1e3) / 1e9 / peak,
