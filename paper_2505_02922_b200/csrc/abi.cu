@@ -119,6 +119,45 @@ static int launch_score_v4(const IndexView& ix, const StepView& sv, int G, int U
   return cudaGetLastError() == cudaSuccess ? 0 : WK_ECUDA;
 }
 
+// Launch with programmatic dependent launch (the kernel may be scheduled while
+// the preceding kernel in the stream drains; it calls pdl_wait() before touching
+// anything that kernel wrote) and, optionally, a thread-block cluster.
+// WK_PDL=0 in the environment disables the attribute (A/B timing).
+static bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("WK_PDL");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on != 0;
+}
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                             int cluster, Args... args) {
+  cudaLaunchConfig_t lc = {};
+  cudaLaunchAttribute at[2];
+  int n = 0;
+  if (pdl_enabled()) {
+    at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[n].val.programmaticStreamSerializationAllowed = 1;
+    n++;
+  }
+  if (cluster > 1) {
+    at[n].id = cudaLaunchAttributeClusterDimension;
+    at[n].val.clusterDim.x = cluster;
+    at[n].val.clusterDim.y = 1;
+    at[n].val.clusterDim.z = 1;
+    n++;
+  }
+  lc.gridDim = grid;
+  lc.blockDim = block;
+  lc.dynamicSmemBytes = smem;
+  lc.stream = s;
+  lc.attrs = at;
+  lc.numAttrs = n;
+  return cudaLaunchKernelEx(&lc, kernel, args...);
+}
+
 template <int KG>
 static int launch_score_v5(const IndexView& ix, const StepView& sv, int G, int U, int m_max, cudaStream_t s) {
   const long long groups = (m_max + 7) / 8;
@@ -129,8 +168,8 @@ static int launch_score_v5(const IndexView& ix, const StepView& sv, int G, int U
   if (gpw < 1) gpw = 1;
   cpu = (groups + gpw * 4 - 1) / (gpw * 4);
   dim3 grid((unsigned)cpu, U);
-  score_v5_kernel<KG><<<grid, 128, 0, s>>>(ix, sv, G, (int)gpw);
-  return cudaGetLastError() == cudaSuccess ? 0 : WK_ECUDA;
+  const cudaError_t e = launch_ex(score_v5_kernel<KG>, grid, dim3(128), 0, s, 1, ix, sv, G, (int)gpw);
+  return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? 0 : WK_ECUDA;
 }
 
 static int launch_select_v6(const IndexView& ix, const StepView& sv, const SelParams& p, int U, int m_max,
@@ -150,30 +189,18 @@ static int launch_select_v6(const IndexView& ix, const StepView& sv, const SelPa
   }
   if (m_max > 262144) return WK_ECONFIG;
   // the G CTAs of a unit form one thread-block cluster (the union runs over DSMEM)
-  cudaLaunchConfig_t lc = {};
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = p.G;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  lc.gridDim = dim3(blocks);
-  lc.blockDim = dim3(256);
-  lc.stream = s;
-  lc.attrs = at;
-  lc.numAttrs = 1;
   cudaError_t e;
-  if (m_max <= 16384 && r_max <= 480) {
-    lc.dynamicSmemBytes = select_v6_dyn_smem(m_max, true, 512);
-    e = cudaLaunchKernelEx(&lc, select_v6_kernel<512, true>, ix, sv, p);
-  } else if (r_max <= 480) {
-    lc.dynamicSmemBytes = select_v6_dyn_smem(m_max, false, 512);
-    e = cudaLaunchKernelEx(&lc, select_v6_kernel<512, false>, ix, sv, p);
-  } else if (r_max <= 1900) {
-    lc.dynamicSmemBytes = select_v6_dyn_smem(m_max, false, 2048);
-    e = cudaLaunchKernelEx(&lc, select_v6_kernel<2048, false>, ix, sv, p);
-  } else {
+  if (m_max <= 16384 && r_max <= 480)
+    e = launch_ex(select_v6_kernel<512, true>, dim3(blocks), dim3(256), select_v6_dyn_smem(m_max, true, 512), s,
+                  p.G, ix, sv, p);
+  else if (r_max <= 480)
+    e = launch_ex(select_v6_kernel<512, false>, dim3(blocks), dim3(256), select_v6_dyn_smem(m_max, false, 512), s,
+                  p.G, ix, sv, p);
+  else if (r_max <= 1900)
+    e = launch_ex(select_v6_kernel<2048, false>, dim3(blocks), dim3(256), select_v6_dyn_smem(m_max, false, 2048),
+                  s, p.G, ix, sv, p);
+  else
     return WK_ECONFIG;
-  }
   return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? 0 : WK_ECUDA;
 }
 
@@ -190,11 +217,13 @@ static int launch_attend_v4(const IndexView& ix, const SteadyView& st, const Ste
     configured = true;
   }
   const int warps = attend_v4_warps<T, DPL, HS>();
-  attend_v4_kernel<T, DPL, HS, FULL, OFF><<<P, warps * 32, sm, s>>>(ix, st, sv, p, n_store, U);
-  if (cudaGetLastError() != cudaSuccess) return WK_ECUDA;
+  if (launch_ex(attend_v4_kernel<T, DPL, HS, FULL, OFF>, dim3(P), dim3(warps * 32), sm, s, 1, ix, st, sv, p,
+                n_store, U) != cudaSuccess || cudaGetLastError() != cudaSuccess)
+    return WK_ECUDA;
   const int RG = HS == 4 ? 16 : 8;  // Att4Cfg::RG
-  att4_merge_kernel<FULL, DPL / 2><<<U * p.G, 128, 0, s>>>(st, sv, p, n_store, U, P * warps, RG);
-  return cudaGetLastError() == cudaSuccess ? 0 : WK_ECUDA;
+  const cudaError_t e = launch_ex(att4_merge_kernel<FULL, DPL / 2>, dim3(U * p.G), dim3(128), 0, s, 1, st, sv, p,
+                                  n_store, U, P * warps, RG);
+  return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? 0 : WK_ECUDA;
 }
 
 template <typename T, bool FULL>

@@ -117,6 +117,7 @@ __global__ void __launch_bounds__(Att4Cfg<T, DPL, HS>::WARPS * 32, 1) attend_v4_
   using CF = Att4Cfg<T, DPL, HS>;
   constexpr int RG = CF::RG, NST = CF::NST, ROWT = CF::ROWT, ROWV = CF::ROWV, SB = CF::SB, NL = CF::NL;
   constexpr int D = CF::D, RH = RG / 2, DP2 = DPL / 2;
+  pdl_wait();
   const int G = p.G;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int half = lane >> 4, sub = lane & 15;
@@ -544,6 +545,7 @@ __global__ void __launch_bounds__(128) att4_merge_kernel(SteadyView st, StepView
                                                           int RG) {
   // one CTA (4 warps) per (unit, head): the partial records are split over
   // the warps so ~4x more loads are in flight than with one warp per head
+  pdl_wait();
   const int G = p.G, d = p.d, D2 = 4 + d;  // partial record: (M, D, -, -, num[d])
   const int u = blockIdx.x / G, g = blockIdx.x % G;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, t = threadIdx.x;

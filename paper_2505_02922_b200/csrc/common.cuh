@@ -270,6 +270,14 @@ WK_DEVINL double score_error_bound_v2(double qnorm2, double cmax, int d, int mod
 // permuted layout so one warp ballot over 32 lanes x float4 covers a word:
 // cluster c <-> word ((c >> 7) << 2) | (c & 3), bit (c >> 2) & 31.
 // Words per unit: 4 * ceil(m / 128).
+// programmatic dependent launch: the decode kernels are launched with the
+// programmatic-serialization attribute and wait here for the preceding grid
+// (completion and memory visibility; a no-op without the attribute).  They
+// never trigger early (griddepcontrol.launch_dependents): measured, early
+// triggers let waiting dependents take SM slots from the primary's tail
+// (-5%), while the implicit trigger at exit hides the launch latency (+4%).
+WK_DEVINL void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // distributed shared memory (thread-block clusters): 32-bit shared::cluster
 // address of `p` (a shared-memory object of this CTA) in CTA `rank` of the
 // cluster -- all CTAs of a kernel share the layout -- and a 32-bit load.

@@ -196,6 +196,7 @@ WK_DEVINL void dmma884(double (&c)[2], double a, double b) {
 template <int KG>  // KG = d / 16 load groups of 4 k-steps
 __global__ void __launch_bounds__(128, 8) score_v5_kernel(IndexView ix, StepView sv, int G, int groups_per_warp) {
   constexpr int D = KG * 16;
+  pdl_wait();
   const int u = blockIdx.y;
   const int m = sv.m[u];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

@@ -433,6 +433,7 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
   extern __shared__ __align__(16) unsigned char s6_raw[];  // Sel6Smem | SMS: scores [m] | bitmaps R, TRE [W]
   Sel6Smem<CAND>& sm = *reinterpret_cast<Sel6Smem<CAND>*>(s6_raw);
   float* s6_dyn = reinterpret_cast<float*>(s6_raw + ((sizeof(Sel6Smem<CAND>) + 15) & ~(size_t)15));
+  pdl_wait();
   const int G = p.G, d = p.d;
   const int u = blockIdx.x / G, g = blockIdx.x % G;
   const int m = sv.m[u];
