@@ -507,6 +507,7 @@ __global__ void __launch_bounds__(Att4Cfg<T, DPL, HS>::WARPS * 32, 1) attend_v4_
       }
       __syncwarp();
     }
+    pdl_trigger<4>();
     flush();
   }
 }
@@ -546,6 +547,7 @@ __global__ void __launch_bounds__(128) att4_merge_kernel(SteadyView st, StepView
   // one CTA (4 warps) per (unit, head): the partial records are split over
   // the warps so ~4x more loads are in flight than with one warp per head
   pdl_wait();
+  pdl_trigger<8>();
   const int G = p.G, d = p.d, D2 = 4 + d;  // partial record: (M, D, -, -, num[d])
   const int u = blockIdx.x / G, g = blockIdx.x % G;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, t = threadIdx.x;

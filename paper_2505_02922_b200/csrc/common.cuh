@@ -277,6 +277,13 @@ WK_DEVINL double score_error_bound_v2(double qnorm2, double cmax, int d, int mod
 // triggers let waiting dependents take SM slots from the primary's tail
 // (-5%), while the implicit trigger at exit hides the launch latency (+4%).
 WK_DEVINL void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+#ifndef WK_TRIG_MASK
+#define WK_TRIG_MASK 0  // tuning experiments: bit k = early trigger in kernel k (score, select, attend, merge)
+#endif
+template <int BIT>
+WK_DEVINL void pdl_trigger() {
+  if (WK_TRIG_MASK & BIT) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 // distributed shared memory (thread-block clusters): 32-bit shared::cluster
 // address of `p` (a shared-memory object of this CTA) in CTA `rank` of the

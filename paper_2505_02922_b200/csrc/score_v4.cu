@@ -253,6 +253,7 @@ __global__ void __launch_bounds__(128, 8) score_v5_kernel(IndexView ix, StepView
       if (h0 + 1 < G) out[(size_t)(h0 + 1) * ix.m_cap + row] = (float)c[1];
     }
   }
+  pdl_trigger<1>();
 }
 
 template __global__ void score_v5_kernel<8>(IndexView, StepView, int, int);

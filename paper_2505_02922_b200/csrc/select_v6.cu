@@ -801,6 +801,7 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
   }
   if (!ok && t == 0) { tailp[0] = -INFINITY; tailp[1] = 0.f; tailp[2] = -INFINITY; tailp[3] = 0.f; }
   S6_MARK(9);
+  pdl_trigger<2>();
   // ---- the unit's G CTAs (one cluster) build the union together ----
   cooperative_groups::this_cluster().sync();  // every head's R / E bitmaps final in its smem
   S6_MARK(10);
