@@ -222,7 +222,7 @@ __device__ void s6_union_cl(const IndexView& ix, const StepView& sv, const SelPa
     asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(loc), "r"(h));
     return r;
   };
-  const int PR = p.piece_rows;
+  const int PR = p.piece_rows, PRS = PR == 16 ? 4 : 3;  // pieces of <= PR = 2^PRS rows
   auto stage = [&](int tw0, int tw1) {  // clusters [32 tw0, 32 tw1) + every head's words, one round trip
     constexpr int K = S6_TWC / S6_T;
     const int c0 = tw0 << 5, c1 = min(m, tw1 << 5), nw = tw1 - tw0;
@@ -233,11 +233,13 @@ __device__ void s6_union_cl(const IndexView& ix, const StepView& sv, const SelPa
       a[k] = c < c1 ? __ldg(csize + c) : 0;
       b[k] = c < c1 ? __ldg(coff + c) : 0;
     }
+    // words: thread t takes word t % 64 of (R/E, head) pairs t / 64, t / 64 + 4, ... (2G <= 16 pairs)
     uint32_t wv[4];
+    const int w = t & (S6_TWW - 1), eh0 = t / S6_TWW;
 #pragma unroll
-    for (int k = 0; k < 4; k++) {  // 2 * G * nw <= 2 * 8 * 64 = 4 * S6_T
-      const int i = t + k * S6_T, e = i / (G * S6_TWW), h = (i / S6_TWW) % G, w = i % S6_TWW;
-      wv[k] = (i < 2 * G * S6_TWW && w < nw) ? dsmem_ld_u32(peer((e ? tr_loc : rb_loc) + 4u * (tw0 + w), h)) : 0u;
+    for (int k = 0; k < 4; k++) {
+      const int eh = eh0 + 4 * k, e = eh >= G, h = eh - (e ? G : 0);
+      wv[k] = (eh < 2 * G && w < nw) ? dsmem_ld_u32(peer((e ? tr_loc : rb_loc) + 4u * (tw0 + w), h)) : 0u;
     }
     __syncthreads();
 #pragma unroll
@@ -247,7 +249,7 @@ __device__ void s6_union_cl(const IndexView& ix, const StepView& sv, const SelPa
     }
 #pragma unroll
     for (int k = 0; k < 4; k++)
-      if (t + k * S6_T < 2 * G * S6_TWW) lw[t + k * S6_T] = wv[k];
+      if (eh0 + 4 * k < 2 * G) lw[(eh0 + 4 * k) * S6_TWW + w] = wv[k];
     __syncthreads();
   };
   // this warp's words of tile [tw0, tw1): contiguous block
@@ -279,7 +281,7 @@ __device__ void s6_union_cl(const IndexView& ix, const StepView& sv, const SelPa
       if ((ur >> lane) & 1u) {
         const int sz = csz[zb_cluster(w, lane) - (tw0 << 5)];
         tok += sz;
-        pcs += (sz + PR - 1) / PR;
+        pcs += (sz + PR - 1) >> PRS;
       }
     }
     c4[0] = nr; c4[1] = tok; c4[2] = pcs; c4[3] = ne;
@@ -363,7 +365,7 @@ __device__ void s6_union_cl(const IndexView& ix, const StepView& sv, const SelPa
       if (ur) {
         const bool in = (ur >> lane) & 1u;
         const int sz = in ? csz[ci] : 0;
-        const int np = (sz + PR - 1) / PR;
+        const int np = (sz + PR - 1) >> PRS;
         int x = np;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
@@ -407,7 +409,7 @@ __device__ void s6_union_cl(const IndexView& ix, const StepView& sv, const SelPa
   float* eux = sv.eu_x + (size_t)u * sv.eu_cap * G + g;
   const float isd = p.inv_sqrt_d;
   const float* sg = sv.scores + ((size_t)u * G + g) * ix.m_cap;
-  constexpr int UN = 4;
+  constexpr int UN = 8;
   for (int i0 = t; i0 < n_eu; i0 += UN * S6_T) {
     int cc[UN], mm[UN];
 #pragma unroll
