@@ -282,14 +282,13 @@ __global__ void __launch_bounds__(Att4Cfg<T, DPL, HS>::WARPS * 32, 1) attend_v4_
         srck = (const unsigned char*)ix.store_k + ((size_t)u * ix.s_cap + m.a) * ROWT;
         srcv = (const unsigned char*)ix.store_v + ((size_t)u * ix.s_cap + m.a) * ROWT;
       }
+      // K rows >= n stay stale (their logits are masked to -inf); V rows >= n are
+      // zero-filled so p = 0 never meets a non-finite stale value
       if (lane == 0) {
-        mbar_arrive_expect_tx(bars + sti, (uint32_t)(2 * RG * ROWT));
+        mbar_arrive_expect_tx(bars + sti, (uint32_t)((n + RG) * ROWT));
         bulk_g2s(stage, srck, (uint32_t)(n * ROWT), bars + sti);
         bulk_g2s(stage + RG * ROWT, srcv, (uint32_t)(n * ROWT), bars + sti);
-        if (n < RG) {
-          bulk_g2s(stage + n * ROWT, g_zero4, (uint32_t)((RG - n) * ROWT), bars + sti);
-          bulk_g2s(stage + RG * ROWT + n * ROWT, g_zero4, (uint32_t)((RG - n) * ROWT), bars + sti);
-        }
+        if (n < RG) bulk_g2s(stage + RG * ROWT + n * ROWT, g_zero4, (uint32_t)((RG - n) * ROWT), bars + sti);
       }
     } else {
       if (lane == 0) mbar_arrive_expect_tx(bars + sti, (uint32_t)(RG * ROWV));
