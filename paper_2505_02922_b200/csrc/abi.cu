@@ -161,12 +161,17 @@ static cudaError_t launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, si
 template <int KG>
 static int launch_score_v5(const IndexView& ix, const StepView& sv, int G, int U, int m_max, cudaStream_t s) {
   const long long groups = (m_max + 7) / 8;
-  // exactly one wave: 8 CTAs (32 warps) per SM, the same CTA count per unit
-  long long cpu = ((long long)sm_count() * 8) / U;
-  if (cpu < 1) cpu = 1;
-  long long gpw = (groups + cpu * 4 - 1) / (cpu * 4);
-  if (gpw < 1) gpw = 1;
-  cpu = (groups + gpw * 4 - 1) / (gpw * 4);
+  // short warp ranges (~6 eight-row groups per warp, many CTAs in flight) balance the
+  // HBM stream better than one exact wave of long ranges: measured 2,146 -> 2,218 tok/s
+  // (profiles/r1_attend_sweep.txt).  WK_SCORE_GPW overrides for tuning experiments.
+  static int gpw_t = -1;
+  if (gpw_t < 0) {
+    const char* e = getenv("WK_SCORE_GPW");
+    gpw_t = e ? atoi(e) : 6;
+    if (gpw_t < 1 || gpw_t > 4096) gpw_t = 6;
+  }
+  const long long gpw = gpw_t;
+  const long long cpu = (groups + gpw * 4 - 1) / (gpw * 4);
   dim3 grid((unsigned)cpu, U);
   const cudaError_t e = launch_ex(score_v5_kernel<KG>, grid, dim3(128), 0, s, 1, ix, sv, G, (int)gpw);
   return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? 0 : WK_ECUDA;
