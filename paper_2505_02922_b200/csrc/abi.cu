@@ -43,6 +43,8 @@ __global__ void att4_est_prep_kernel(IndexView, StepView, int, float);
 template <bool FULL, int DL>
 __global__ void att4_merge_kernel(SteadyView, StepView, AttnParams, const int32_t*, int, int, int);
 __global__ void km_pack16_kernel(const SegDesc*, IndexView, int);
+template <int EPL>
+__global__ void km_prep_v2_kernel(const SegDesc*, float*, __half*);
 // cache_v2.cu
 __global__ void cache2_step_kernel(wk_cache2_view, IndexView, SteadyView, StepView, int, int64_t);
 // metrics.cu
@@ -258,7 +260,13 @@ int wk_kmeans_segments(const wk_index_view* ix, const wk_segment* segs, int n_se
     return WK_ECUDA;
   const SegDesc* sd = scr->segs_dev;
   __half* p16 = (d % 16 == 0) ? (__half*)scr->P16 : nullptr;
-  km_prep_kernel<<<n_segs, 256, d * sizeof(float), s>>>(sd, scr->P, d, p16);
+  if (d == 32 || d == 64 || d == 128) {
+    if (d == 128) km_prep_v2_kernel<4><<<n_segs, 512, 0, s>>>(sd, scr->P, p16);
+    else if (d == 64) km_prep_v2_kernel<2><<<n_segs, 512, 0, s>>>(sd, scr->P, p16);
+    else km_prep_v2_kernel<1><<<n_segs, 512, 0, s>>>(sd, scr->P, p16);
+  } else {
+    km_prep_kernel<<<n_segs, 256, d * sizeof(float), s>>>(sd, scr->P, d, p16);
+  }
   WK_CHECK_LAUNCH();
   if ((d % 8) == 0) {
     // v2: 256 threads, <= 72 KB of smem so 3 segments share an SM

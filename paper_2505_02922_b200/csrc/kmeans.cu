@@ -48,6 +48,89 @@ __global__ void km_prep_kernel(const SegDesc* __restrict__ segs, float* __restri
   }
 }
 
+// v2 of the prep for d = 32 EPL (32 / 64 / 128): the column means keep the
+// sequential fp32 chain of np.mean(axis=0) with 8 loads in flight per column;
+// then one warp per row (lane = EPL contiguous dims, coalesced): centre, square
+// into smem, the 8 pairwise-sum chains of np.linalg.norm on lanes 0-7 (one
+// block of 8 per step, then ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) by shuffles),
+// divide, write P and P16 in the same pass.  Bit-identical to km_prep_kernel.
+template <int EPL>
+__global__ void __launch_bounds__(512) km_prep_v2_kernel(const SegDesc* __restrict__ segs, float* __restrict__ P_all,
+                                                         __half* __restrict__ P16_all) {
+  constexpr int D = 32 * EPL;
+  const SegDesc sg = segs[blockIdx.x];
+  if (sg.k <= 1) return;
+  __shared__ float mean[D];
+  __shared__ float sq[16][D];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, NW = blockDim.x >> 5;
+  const float* keys = sg.keys;
+  if (t < D) {
+    float sum = 0.f;
+    int i = 0;
+    for (; i + 8 <= sg.L; i += 8) {
+      float v[8];
+#pragma unroll
+      for (int k = 0; k < 8; k++) v[k] = __ldg(keys + (size_t)(i + k) * sg.key_stride + t);
+#pragma unroll
+      for (int k = 0; k < 8; k++) sum = __fadd_rn(sum, v[k]);
+    }
+    for (; i < sg.L; i++) sum = __fadd_rn(sum, __ldg(keys + (size_t)i * sg.key_stride + t));
+    mean[t] = __fdiv_rn(sum, (float)sg.L);
+  }
+  __syncthreads();
+  float mu[EPL];
+#pragma unroll
+  for (int e = 0; e < EPL; e++) mu[e] = mean[lane * EPL + e];
+  float* P = P_all + (size_t)sg.p_off * D;
+  __half* P16 = P16_all ? P16_all + (size_t)sg.p_off * D : nullptr;
+  float* sw = sq[warp];
+  for (int i = warp; i < sg.L; i += NW) {
+    const float* kr = keys + (size_t)i * sg.key_stride + lane * EPL;
+    float x[EPL];
+    if (EPL == 4) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(kr));
+      x[0] = v.x; x[1 % EPL] = v.y; x[2 % EPL] = v.z; x[3 % EPL] = v.w;
+    } else if (EPL == 2) {
+      const float2 v = __ldg(reinterpret_cast<const float2*>(kr));
+      x[0] = v.x; x[1 % EPL] = v.y;
+    } else {
+      x[0] = __ldg(kr);
+    }
+#pragma unroll
+    for (int e = 0; e < EPL; e++) {
+      x[e] = __fsub_rn(x[e], mu[e]);
+      sw[lane * EPL + e] = __fmul_rn(x[e], x[e]);
+    }
+    __syncwarp();
+    float r = 0.f;
+    if (lane < 8) {
+      r = sw[lane];
+#pragma unroll
+      for (int j = 8; j < D; j += 8) r = __fadd_rn(r, sw[j + lane]);
+    }
+    r = __fadd_rn(r, __shfl_down_sync(0xffffffffu, r, 1));
+    r = __fadd_rn(r, __shfl_down_sync(0xffffffffu, r, 2));
+    r = __fadd_rn(r, __shfl_down_sync(0xffffffffu, r, 4));
+    const float nr = __fsqrt_rn(__shfl_sync(0xffffffffu, r, 0));
+    __syncwarp();
+    float y[EPL];
+#pragma unroll
+    for (int e = 0; e < EPL; e++) y[e] = nr != 0.f ? __fdiv_rn(x[e], nr) : (lane * EPL + e == 0 ? 1.f : 0.f);
+    float* pr = P + (size_t)i * D + lane * EPL;
+    if (EPL == 4) *reinterpret_cast<float4*>(pr) = make_float4(y[0], y[1 % EPL], y[2 % EPL], y[3 % EPL]);
+    else if (EPL == 2) *reinterpret_cast<float2*>(pr) = make_float2(y[0], y[1 % EPL]);
+    else pr[0] = y[0];
+    if (P16) {
+      __half* hr = P16 + (size_t)i * D + lane * EPL;
+#pragma unroll
+      for (int e = 0; e < EPL; e++) hr[e] = __float2half_rn(y[e]);
+    }
+  }
+}
+template __global__ void km_prep_v2_kernel<1>(const SegDesc*, float*, __half*);
+template __global__ void km_prep_v2_kernel<2>(const SegDesc*, float*, __half*);
+template __global__ void km_prep_v2_kernel<4>(const SegDesc*, float*, __half*);
+
 // ---------------------------------------------------------------------------
 // phase 2: k-means++ seeding under cosine distance (clustering.py:26-43).
 // One CTA per segment runs the k-1 sequential steps; the sgemv of each step
