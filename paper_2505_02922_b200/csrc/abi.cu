@@ -11,7 +11,7 @@ namespace wk {
 // kmeans.cu
 __global__ void km_prep_kernel(const SegDesc*, float*, int, __half*);
 __global__ void km_seed_kernel(const SegDesc*, const float*, float*, float*, int, int, int);
-__global__ void km_seed_v2_kernel(const SegDesc*, const float*, float*, float*, int, int, int, const __half*);
+__global__ void km_seed_v2_kernel(const SegDesc*, const float*, float*, float*, int, int, int, const __half*, int);
 __global__ void km_assign_kernel(const SegDesc*, const float*, const float*, int32_t*, int);
 template <int KS>
 __global__ void km_assign_tc_kernel(const SegDesc*, const float*, const float*, int32_t*);
@@ -269,11 +269,15 @@ int wk_kmeans_segments(const wk_index_view* ix, const wk_segment* segs, int n_se
   }
   WK_CHECK_LAUNCH();
   if ((d % 8) == 0) {
-    // v2: 256 threads, <= 72 KB of smem so 3 segments share an SM
-    const int smem_rows = ((72 * 1024) / 4 - d) / 2;
-    const size_t seed_smem = (size_t)(d + 2 * (max_L <= smem_rows ? max_L + 3 : 0)) * sizeof(float);
-    km_seed_v2_kernel<<<n_segs, 256, seed_smem + 16, s>>>(sd, scr->P, scr->C, scr->md, d, blas_threads,
-                                                           max_L <= smem_rows ? smem_rows : 0, p16);
+    // v2: 256 threads; centre + centre-distance bounds + (md, best) rows in smem
+    // when they fit 72 KB (4 segments per SM at 120K: 52 KB)
+    const int L4 = (max_L + 3) & ~3, K4 = (max_k + 3) & ~3;
+    const size_t base = (size_t)(d + K4) * sizeof(float);
+    const size_t rows = (size_t)L4 * sizeof(float) + (size_t)L4 * sizeof(unsigned short);
+    const bool in_smem = base + rows + 16 <= 72 * 1024;
+    km_seed_v2_kernel<<<n_segs, 256, base + (in_smem ? rows : 0) + 16, s>>>(sd, scr->P, scr->C, scr->md, d,
+                                                                             blas_threads, in_smem ? 1 : 0, p16,
+                                                                             max_k);
   } else {
     const int smem_rows = ((200 * 1024) / 4 - d) / 2;
     const size_t seed_smem = (size_t)(d + 2 * (max_L <= smem_rows ? max_L : 0)) * sizeof(float);

@@ -210,26 +210,36 @@ __global__ void km_seed_kernel(const SegDesc* __restrict__ segs, const float* __
 // halves are combined in the recipe order ((a_l + a_{l+4}), then
 // (s0+s1)+(s2+s3)).  A warp covers 16 rows per 16-byte load instruction
 // (512 contiguous-row bytes).  Chunk-tail rows (classes 1, 2) keep the
-// per-thread recipe.  The fp32 cumsum stays the reference's sequential chain.
+// per-thread recipe.  The fp32 cumsum stays the reference's sequential chain
+// (recomputed in a second pass up to the drawn index instead of being stored).
+// Rows the new centre provably cannot improve are skipped before any load
+// (triangle inequality on the unit sphere, rigorous margin KS_EPS covering the
+// fp32 evaluation): with b = the row's current best centre,
+//   ||p - c|| >= ||c_b - c|| - ||p - c_b||,  ||p - c_b||^2 <= 2 (md + eps),
+// so if (D_lo - r_hi)^2 / 2 >= md + eps the computed 1 - p.c is >= md and
+// min(md, .) keeps md -- the same bits as evaluating the row.
 // grid = n_segments, block = 256
 // ---------------------------------------------------------------------------
+constexpr float KS_EPS = 1e-4f;
 __global__ void __launch_bounds__(256) km_seed_v2_kernel(const SegDesc* __restrict__ segs, const float* __restrict__ P_all,
                                                          float* __restrict__ C_all, float* __restrict__ scratch_all,
-                                                         int d, int blas_threads, int smem_rows,
-                                                         const __half* __restrict__ P16_all) {
+                                                         int d, int blas_threads, int in_smem,
+                                                         const __half* __restrict__ P16_all, int max_k) {
   const SegDesc sg = segs[blockIdx.x];
   if (sg.k <= 1) return;
   extern __shared__ __align__(16) float sm2[];
-  float* cent = sm2;  // d floats: current centroid
+  float* cent = sm2;          // d floats: current centroid
+  float* ccd = sm2 + d;       // max_k floats: lower bounds of ||C[a] - cent||
   const int L = sg.L;
-  float *md, *cdf;
-  const int L4 = (L + 3) & ~3;  // cdf 16-byte aligned
-  if (L + 3 <= smem_rows) {
-    md = sm2 + d;
-    cdf = md + L4;
+  float* md;
+  unsigned short* best;       // the centre each row's md was last set by
+  const int L4 = (L + 3) & ~3;
+  if (in_smem) {
+    md = ccd + ((max_k + 3) & ~3);
+    best = reinterpret_cast<unsigned short*>(md + L4);
   } else {
     md = scratch_all + (size_t)sg.p_off * 2;
-    cdf = md + L;
+    best = reinterpret_cast<unsigned short*>(md + L);
   }
   const float* P = P_all + (size_t)sg.p_off * d;
   const __half* P16 = P16_all ? P16_all + (size_t)sg.p_off * d : nullptr;
@@ -255,9 +265,22 @@ __global__ void __launch_bounds__(256) km_seed_v2_kernel(const SegDesc* __restri
     }
     __syncthreads();
     if (c == sg.k - 1) break;
+    // lower bounds of the distances from the earlier centres to the new one
+    for (int a = warp; a < c; a += nwarp) {
+      float dp = 0.f;
+      for (int t = lane; t < d; t += 32) dp = fmaf(C[(size_t)a * d + t], cent[t], dp);
+      dp = warp_sum(dp);
+      if (lane == 0) ccd[a] = sqrtf(fmaxf(0.f, 2.f * (1.f - dp - KS_EPS)));
+    }
+    __syncthreads();
     for (int base = warp * 16; base < L; base += nwarp * 16) {
       const int i = base + rsub;
       bool act = i < L;
+      if (act && c > 0) {
+        const float m = md[i];
+        const float rh = sqrtf(2.f * (m + KS_EPS)), dl = ccd[best[i]];
+        if (dl > rh && 0.5f * (dl - rh) * (dl - rh) >= m + KS_EPS) act = false;
+      }
       if (act && c > 0 && P16) {
         // first pass on the fp16 copy: |dot' - dot| <= 2^-11 + 2 gamma_d for
         // unit rows, so v' - 1e-3 >= md[i] proves min(md, v) == md (no update)
@@ -315,32 +338,28 @@ __global__ void __launch_bounds__(256) km_seed_v2_kernel(const SegDesc* __restri
       if (act && h == 0) {
         float v = __fsub_rn(1.0f, dot);
         v = v < 0.f ? 0.f : v;
-        if (c == 0) md[i] = v;
-        else if (!(md[i] <= v)) md[i] = v;
+        if (c == 0 || !(md[i] <= v)) { md[i] = v; best[i] = (unsigned short)c; }
       }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      // the reference's sequential fp32 cumsum; register-batched (float4 in,
-      // float4 out, no load/store aliasing) so it runs at the FADD latency
+      // the reference's sequential fp32 cumsum (register-batched, runs at the
+      // FADD latency); pass 1 gives cdf[-1], pass 2 re-walks the same chain up
+      // to the first cdf > threshold (searchsorted 'right')
       float sacc = 0.f;  // 0 + md[0] == md[0] (md >= +0)
-      if (L == L4 && cdf == md + L4) {
+      const bool v4 = in_smem && L == L4;
+      if (v4) {
         const float4* __restrict__ m4 = reinterpret_cast<const float4*>(md);
-        float4* __restrict__ c4 = reinterpret_cast<float4*>(cdf);
 #pragma unroll 4
         for (int q = 0; q < L4 / 4; q++) {
           const float4 v = m4[q];
-          float4 o;
-          sacc = __fadd_rn(sacc, v.x); o.x = sacc;
-          sacc = __fadd_rn(sacc, v.y); o.y = sacc;
-          sacc = __fadd_rn(sacc, v.z); o.z = sacc;
-          sacc = __fadd_rn(sacc, v.w); o.w = sacc;
-          c4[q] = o;
+          sacc = __fadd_rn(sacc, v.x);
+          sacc = __fadd_rn(sacc, v.y);
+          sacc = __fadd_rn(sacc, v.z);
+          sacc = __fadd_rn(sacc, v.w);
         }
       } else {
-        const float* __restrict__ m1 = md;
-        float* __restrict__ c1 = cdf;
-        for (int i = 0; i < L; i++) { sacc = __fadd_rn(sacc, m1[i]); c1[i] = sacc; }
+        for (int i = 0; i < L; i++) sacc = __fadd_rn(sacc, md[i]);
       }
       long long nidx;
       if (sacc <= 0.0f) {
@@ -348,9 +367,26 @@ __global__ void __launch_bounds__(256) km_seed_v2_kernel(const SegDesc* __restri
       } else {
         const float u = (float)pcg_next_double(g);
         const float thr = __fmul_rn(u, sacc);
-        int lo = 0, hi = L;
-        while (lo < hi) { const int mid = (lo + hi) >> 1; if (cdf[mid] <= thr) lo = mid + 1; else hi = mid; }
-        nidx = lo > L - 1 ? L - 1 : lo;
+        float s2 = 0.f;
+        int i = 0;
+        if (v4) {
+          const float4* __restrict__ m4 = reinterpret_cast<const float4*>(md);
+          for (; i < L; i += 4) {
+            const float4 v = m4[i >> 2];
+            float o0, o1, o2, o3;
+            s2 = __fadd_rn(s2, v.x); o0 = s2;
+            s2 = __fadd_rn(s2, v.y); o1 = s2;
+            s2 = __fadd_rn(s2, v.z); o2 = s2;
+            s2 = __fadd_rn(s2, v.w); o3 = s2;
+            if (o3 > thr) { i += o0 > thr ? 0 : (o1 > thr ? 1 : (o2 > thr ? 2 : 3)); break; }
+          }
+        } else {
+          for (; i < L; i++) {
+            s2 = __fadd_rn(s2, md[i]);
+            if (s2 > thr) break;
+          }
+        }
+        nidx = i > L - 1 ? L - 1 : i;
       }
       s_idx = nidx;
     }
