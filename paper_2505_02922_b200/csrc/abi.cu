@@ -39,7 +39,6 @@ template <typename T, int DPL, int HS, bool FULL>
 size_t attend_v4_smem();
 template <typename T, int DPL, int HS>
 int attend_v4_warps();
-__global__ void att4_est_prep_kernel(IndexView, StepView, int, float);
 template <bool FULL, int DL>
 __global__ void att4_merge_kernel(SteadyView, StepView, AttnParams, const int32_t*, int, int, int);
 __global__ void km_pack16_kernel(const SegDesc*, IndexView, int);

@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(Att4Cfg<T, DPL, HS>::WARPS * 32, 1) attend_v4_
       n = min(RG, sv.cnt[u * 4 + 2] - e0);
       if (lane < n) m.a = __ldcg(sv.eu_ids + (size_t)u * sv.eu_cap + e0 + lane);
       // lane slot (row jl, head h_own): logit sigma * q.C and cluster size
-      // (att4_est_prep_kernel)
+      // (select_v6's cluster union)
 #pragma unroll
       for (int l = 0; l < NL; l++)
         if (jl(l) < n && h_own < G) {
@@ -509,31 +509,6 @@ __global__ void __launch_bounds__(Att4Cfg<T, DPL, HS>::WARPS * 32, 1) attend_v4_
     pdl_trigger<4>();
     flush();
   }
-}
-
-// ---------------------------------------------------------------------------
-// estimation-row inputs of the union estimation list (attention.py:98-104):
-// per row the logit sigma * q.C of each head whose estimation zone holds the
-// cluster (-inf otherwise; reusing the ranking score, engine.py:186-189) and
-// the cluster size.  Grid-wide so attend_v4's chunk metadata is one level of
-// independent loads.
-// ---------------------------------------------------------------------------
-__global__ void att4_est_prep_kernel(IndexView ix, StepView sv, int G, float isd) {
-  const int u = blockIdx.y;
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= sv.cnt[u * 4 + 2]) return;
-  const size_t row = (size_t)u * sv.eu_cap + e;
-  const int c = __ldcg(sv.eu_ids + row), mk = __ldcg(sv.eu_mask + row);
-  // all loads first (one round trip), then the stores
-  const float sz = (float)__ldg(ix.cl_size + (size_t)u * ix.m_cap + c);
-  float x[8];
-#pragma unroll
-  for (int h = 0; h < 8; h++)
-    x[h] = (h < G && ((mk >> h) & 1)) ? __ldcg(sv.scores + ((size_t)u * G + h) * ix.m_cap + c) * isd : -INFINITY;
-  sv.eu_sz[row] = sz;
-#pragma unroll
-  for (int h = 0; h < 8; h++)
-    if (h < G) sv.eu_x[row * G + h] = x[h];
 }
 
 // ---------------------------------------------------------------------------
