@@ -42,6 +42,8 @@ int attend_v4_warps();
 template <bool FULL, int DL>
 __global__ void att4_merge_kernel(SteadyView, StepView, AttnParams, const int32_t*, int, int, int);
 __global__ void km_pack16_kernel(const SegDesc*, IndexView, int);
+__global__ void km_assign_tc5_kernel(const SegDesc*, const float*, const float*, int32_t*);
+constexpr size_t K5_SMEM_BYTES = 2 * 128 * 128 * 2 + 2 * 256 * 128 * 2 + 64;
 template <int EPL>
 __global__ void km_prep_v2_kernel(const SegDesc*, float*, __half*);
 // cache_v2.cu
@@ -70,6 +72,7 @@ static int configure_smem() {
   // opt in to large dynamic shared memory where the kernels need it
   if (cudaFuncSetAttribute(km_seed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess) return WK_ECUDA;
   if (cudaFuncSetAttribute(km_seed_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 72 * 1024) != cudaSuccess) return WK_ECUDA;
+  if (cudaFuncSetAttribute(km_assign_tc5_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K5_SMEM_BYTES) != cudaSuccess) return WK_ECUDA;
   if (cudaFuncSetAttribute(km_assign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024) != cudaSuccess) return WK_ECUDA;
   if (cudaFuncSetAttribute(km_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess) return WK_ECUDA;
   if (cudaFuncSetAttribute(km_finalize_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess) return WK_ECUDA;
@@ -287,8 +290,14 @@ int wk_kmeans_segments(const wk_index_view* ix, const wk_segment* segs, int n_se
   const dim3 ag((max_L + 63) / 64, n_segs);
   // Lloyd assignment: tensor-core first pass + exact verification when the
   // head dim tiles by 16 (<= 128), else the exact FFMA kernel
+  const dim3 ag5((max_L + 127) / 128, n_segs);
+  // d = 128 (k <= 512): tcgen05 contraction with the scores in TMEM; WK_KM_TC5=0 selects the
+  // mma.sync kernel (A/B timing)
+  const char* tc5e = getenv("WK_KM_TC5");
+  const bool tc5 = d == 128 && max_k <= 512 && !(tc5e && tc5e[0] == '0');
   auto assign = [&]() {
-    if (d == 128) km_assign_tc_kernel<8><<<ag, 128, 0, s>>>(sd, scr->P, scr->C, scr->A);
+    if (tc5) km_assign_tc5_kernel<<<ag5, 256, K5_SMEM_BYTES, s>>>(sd, scr->P, scr->C, scr->A);
+    else if (d == 128) km_assign_tc_kernel<8><<<ag, 128, 0, s>>>(sd, scr->P, scr->C, scr->A);
     else if (d == 64) km_assign_tc_kernel<4><<<ag, 128, 0, s>>>(sd, scr->P, scr->C, scr->A);
     else if (d == 32) km_assign_tc_kernel<2><<<ag, 128, 0, s>>>(sd, scr->P, scr->C, scr->A);
     else km_assign_kernel<<<ag, 256, (size_t)2 * d * 65 * sizeof(float), s>>>(sd, scr->P, scr->C, scr->A, d);

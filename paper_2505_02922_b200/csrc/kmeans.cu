@@ -561,6 +561,209 @@ template __global__ void km_assign_tc_kernel<4>(const SegDesc*, const float*, co
 template __global__ void km_assign_tc_kernel<2>(const SegDesc*, const float*, const float*, int32_t*);
 
 // ---------------------------------------------------------------------------
+// phase 3 on the 5th-generation tensor cores (d = 128): the same bf16x3 first
+// pass + exact verification as km_assign_tc_kernel, with the contraction on
+// tcgen05.mma and the scores in TMEM.
+//   * one CTA = 128 points of a segment, 4 warps; points (hi / lo bf16) and a
+//     chunk of 256 centroids (hi / lo) are staged in smem in the K-major,
+//     no-swizzle UMMA layout (8-row x 16-byte core matrices; LBO = 128 B along
+//     K, SBO = 2 KB along M/N);
+//   * thread 0 issues M128 x N256 x K16 MMAs: 3 split products x 8 K-steps per
+//     centroid chunk into TMEM columns [256 j, 256 j + 256), then commits to an
+//     mbarrier; the chunk buffer is refilled once the MMAs have read it;
+//   * thread r owns TMEM lane r (= point r): tcgen05.ld 32 columns at a time,
+//     top-4 insertion, then the exact fp32 chain for the candidates within 2B.
+// grid = (ceil(Lmax / 128), n_segments), block = 128, dyn smem = 192 KB + 64.
+// ---------------------------------------------------------------------------
+constexpr int K5_M = 128, K5_N = 256, K5_D = 128;
+constexpr uint32_t K5_A_BYTES = K5_M * K5_D * 2, K5_B_BYTES = K5_N * K5_D * 2;
+constexpr size_t K5_SMEM = 2 * (size_t)K5_A_BYTES + 2 * (size_t)K5_B_BYTES + 64;  // + top-4 exchange aliases B
+
+WK_DEVINL uint32_t k5_off(int r, int k) {  // byte offset of (row r, dim k) in a K-major no-swizzle operand
+  return (uint32_t)((((r >> 3) * (K5_D / 8) + (k >> 3)) << 7) + ((r & 7) << 4) + ((k & 7) << 1));
+}
+WK_DEVINL uint64_t k5_desc(uint32_t saddr) {  // UMMA shared-memory descriptor, SWIZZLE_NONE
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);             // start address
+  d |= (uint64_t)((128u >> 4) & 0x3FFF) << 16;        // LBO: next core matrix along K
+  d |= (uint64_t)((2048u >> 4) & 0x3FFF) << 32;       // SBO: next 8-row group
+  d |= (uint64_t)1 << 46;                              // descriptor version (sm_100)
+  return d;                                            // base offset 0, layout type 0
+}
+// instruction descriptor: f32 accumulate, bf16 x bf16, both K-major, M = 128, N = 256
+constexpr uint32_t K5_IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(K5_N >> 3) << 17) |
+                              ((uint32_t)(K5_M >> 4) << 24);
+
+WK_DEVINL void k5_mma(uint32_t tmem, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+      "l"(a), "l"(b), "r"(K5_IDESC), "r"(acc));
+}
+WK_DEVINL void k5_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
+               : "memory");
+}
+WK_DEVINL void k5_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; i++) v[i] = __uint_as_float(r[i]);
+}
+
+__global__ void __launch_bounds__(256, 1) km_assign_tc5_kernel(const SegDesc* __restrict__ segs,
+                                                                const float* __restrict__ P_all,
+                                                                const float* __restrict__ C_all,
+                                                                int32_t* __restrict__ A_all) {
+  constexpr int d = K5_D;
+  const SegDesc sg = segs[blockIdx.y];
+  if (sg.k <= 1) return;
+  if ((long long)sg.L * sg.k <= 1200) return;  // OpenBLAS small-kernel shapes: km_assign_small_kernel
+  const int p0 = blockIdx.x * K5_M;
+  if (p0 >= sg.L) return;
+  extern __shared__ __align__(1024) unsigned char k5s[];
+  unsigned char* Ah = k5s;
+  unsigned char* Al = Ah + K5_A_BYTES;
+  unsigned char* Bh = Al + K5_A_BYTES;
+  unsigned char* Bl = Bh + K5_B_BYTES;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(Bl + K5_B_BYTES);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
+  const float* P = P_all + (size_t)sg.p_off * d;
+  const float* C = C_all + (size_t)sg.c_off * d;
+  const int t = threadIdx.x, warp = t >> 5;
+  const int nchunk = (sg.k + K5_N - 1) / K5_N;  // <= 2 (k <= 512)
+  const uint32_t ncols = nchunk > 1 ? 512u : 256u;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tslot)),
+                 "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  if (t == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  // points -> A (hi / lo): row t % 128, dims of half t / 128
+  {
+    const int row = t & (K5_M - 1), kh = t >> 7;
+    const float* pr = P + (size_t)min(p0 + row, sg.L - 1) * d;
+#pragma unroll 4
+    for (int kg = kh * (d / 16); kg < (kh + 1) * (d / 16); kg++) {
+      const float4 a = *reinterpret_cast<const float4*>(pr + 8 * kg), b = *reinterpret_cast<const float4*>(pr + 8 * kg + 4);
+      uint4 h, l;
+      ktc_split(a.x, a.y, h.x, l.x);
+      ktc_split(a.z, a.w, h.y, l.y);
+      ktc_split(b.x, b.y, h.z, l.z);
+      ktc_split(b.z, b.w, h.w, l.w);
+      *reinterpret_cast<uint4*>(Ah + k5_off(row, 8 * kg)) = h;
+      *reinterpret_cast<uint4*>(Al + k5_off(row, 8 * kg)) = l;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = *tslot;
+  for (int j = 0; j < nchunk; j++) {
+    // centroids [256 j, 256 j + 256) -> B (hi / lo); zero rows past k
+    if (j > 0) {
+      mbar_wait(bar, (uint32_t)((j - 1) & 1));  // the previous chunk's MMAs have read B
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    }
+    for (int idx = t; idx < K5_N * (d / 8); idx += blockDim.x) {
+      const int c = idx / (d / 8), kg = idx % (d / 8), cg = j * K5_N + c;
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+      if (cg < sg.k) {
+        a = *reinterpret_cast<const float4*>(C + (size_t)cg * d + 8 * kg);
+        b = *reinterpret_cast<const float4*>(C + (size_t)cg * d + 8 * kg + 4);
+      }
+      uint4 h, l;
+      ktc_split(a.x, a.y, h.x, l.x);
+      ktc_split(a.z, a.w, h.y, l.y);
+      ktc_split(b.x, b.y, h.z, l.z);
+      ktc_split(b.z, b.w, h.w, l.w);
+      *reinterpret_cast<uint4*>(Bh + k5_off(c, 8 * kg)) = h;
+      *reinterpret_cast<uint4*>(Bl + k5_off(c, 8 * kg)) = l;
+    }
+    fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor core
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    if (t == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const uint32_t tc = tmem + (uint32_t)(j * K5_N);
+      const uint32_t ah = smem_u32(Ah), al = smem_u32(Al), bh = smem_u32(Bh), bl = smem_u32(Bl);
+      uint32_t acc = 0;
+#pragma unroll
+      for (int kk = 0; kk < d / 16; kk++) {  // K step: 2 core matrices along K = 256 B
+        const uint32_t ko = (uint32_t)kk * 256u;
+        k5_mma(tc, k5_desc(ah + ko), k5_desc(bh + ko), acc); acc = 1;
+        k5_mma(tc, k5_desc(ah + ko), k5_desc(bl + ko), 1);
+        k5_mma(tc, k5_desc(al + ko), k5_desc(bh + ko), 1);
+      }
+      k5_commit(bar);
+    }
+  }
+  mbar_wait(bar, (uint32_t)((nchunk - 1) & 1));
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  // epilogue: warps w and w + 4 read TMEM lanes 32 (w % 4) .. + 31 (their points),
+  // columns [0, 256) and [256, 512) respectively, 32 at a time; the two top-4
+  // lists of a point meet in smem (aliasing the consumed B buffer)
+  float tv[4];
+  int ti[4];
+#pragma unroll
+  for (int i = 0; i < 4; i++) { tv[i] = -INFINITY; ti[i] = 0x7fffffff; }
+  const int half = warp >> 2, row = t & (K5_M - 1);
+  const uint32_t lane_base = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+  const int cend = min(sg.k, (half + 1) * K5_N);
+  for (int c0 = half * K5_N; c0 < cend; c0 += 32) {
+    float v[32];
+    k5_ld32(lane_base + (uint32_t)c0, v);
+#pragma unroll
+    for (int i = 0; i < 32; i++)
+      if (c0 + i < sg.k) ktc_ins(tv, ti, v[i], c0 + i);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  float* xv = reinterpret_cast<float*>(Bh);          // [128][4] values of the upper half
+  int* xi = reinterpret_cast<int*>(Bh + 128 * 16);   // [128][4] indices
+  if (half == 1)
+#pragma unroll
+    for (int i = 0; i < 4; i++) { xv[row * 4 + i] = tv[i]; xi[row * 4 + i] = ti[i]; }
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(ncols));
+  if (half == 1) return;
+#pragma unroll
+  for (int i = 0; i < 4; i++) ktc_ins(tv, ti, xv[row * 4 + i], xi[row * 4 + i]);
+  const int r = p0 + row;
+  if (r >= sg.L) return;
+  const float* pr = P + (size_t)r * d;
+  const float lim = tv[0] - 2.f * KTC_B;
+  float best = -INFINITY;
+  int bi = 0x7fffffff;
+  if (tv[3] >= lim) {
+    for (int c = 0; c < sg.k; c++) {
+      const float v = ktc_exact(pr, C + (size_t)c * d, d);
+      if (v > best) { best = v; bi = c; }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      if (!(tv[i] >= lim)) break;
+      const float v = ktc_exact(pr, C + (size_t)ti[i] * d, d);
+      if (v > best || (v == best && ti[i] < bi)) { best = v; bi = ti[i]; }
+    }
+    if (bi == 0x7fffffff) bi = ti[0];
+  }
+  A_all[sg.p_off + r] = bi;
+}
+
+// ---------------------------------------------------------------------------
 // phase 3: assignment = argmax(points @ centroids.T) (clustering.py:85,96).
 // Every score is the reference's sequential fp32 FMA chain over t; register
 // tiled 64 points x 64 centroids per CTA iteration, transposed smem tiles.
