@@ -42,7 +42,8 @@ int attend_v4_warps();
 template <bool FULL, int DL>
 __global__ void att4_merge_kernel(SteadyView, StepView, AttnParams, const int32_t*, int, int, int);
 __global__ void km_pack16_kernel(const SegDesc*, IndexView, int);
-__global__ void km_assign_tc5_kernel(const SegDesc*, const float*, const float*, int32_t*);
+__global__ void km_assign_tc5_kernel(const SegDesc*, const float*, const float*, int32_t*, const __nv_bfloat16*);
+__global__ void km_pack_c5_kernel(const SegDesc*, const float*, __nv_bfloat16*);
 constexpr size_t K5_SMEM_BYTES = 2 * 128 * 128 * 2 + 2 * 256 * 128 * 2 + 64;
 template <int EPL>
 __global__ void km_prep_v2_kernel(const SegDesc*, float*, __half*);
@@ -294,9 +295,17 @@ int wk_kmeans_segments(const wk_index_view* ix, const wk_segment* segs, int n_se
   // d = 128 (k <= 512): tcgen05 contraction with the scores in TMEM; WK_KM_TC5=0 selects the
   // mma.sync kernel (A/B timing)
   const char* tc5e = getenv("WK_KM_TC5");
-  const bool tc5 = d == 128 && max_k <= 512 && !(tc5e && tc5e[0] == '0');
+  // the pre-split centroids reuse the fp16 point copy (dead after seeding): (sum k + 8 n) * 2 rows
+  long long sum_l = 0, sum_k = 0;
+  for (int i = 0; i < n_segs; i++) { sum_l += segs[i].L; sum_k += segs[i].k; }
+  const bool tc5 = d == 128 && max_k <= 512 && p16 != nullptr && (sum_k + 8LL * n_segs) * 2 <= sum_l &&
+                   !(tc5e && tc5e[0] == '0');
+  __nv_bfloat16* pk = reinterpret_cast<__nv_bfloat16*>(p16);
   auto assign = [&]() {
-    if (tc5) km_assign_tc5_kernel<<<ag5, 256, K5_SMEM_BYTES, s>>>(sd, scr->P, scr->C, scr->A);
+    if (tc5) {
+      km_pack_c5_kernel<<<n_segs, 256, 0, s>>>(sd, scr->C, pk);
+      km_assign_tc5_kernel<<<ag5, 256, K5_SMEM_BYTES, s>>>(sd, scr->P, scr->C, scr->A, pk);
+    }
     else if (d == 128) km_assign_tc_kernel<8><<<ag, 128, 0, s>>>(sd, scr->P, scr->C, scr->A);
     else if (d == 64) km_assign_tc_kernel<4><<<ag, 128, 0, s>>>(sd, scr->P, scr->C, scr->A);
     else if (d == 32) km_assign_tc_kernel<2><<<ag, 128, 0, s>>>(sd, scr->P, scr->C, scr->A);

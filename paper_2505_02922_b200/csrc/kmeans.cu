@@ -619,10 +619,41 @@ WK_DEVINL void k5_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; i++) v[i] = __uint_as_float(r[i]);
 }
 
+// centroids of every segment split to bf16 hi / lo once per Lloyd round, in the
+// UMMA operand layout (rows beyond k zero, k rounded up to 8): segment s at
+// element offset (c_off + 8 s) * 2 * d of `pk`, hi rows then lo rows, so a chunk
+// of 256 rows is one contiguous 64 KB run for a bulk copy.
+__global__ void km_pack_c5_kernel(const SegDesc* __restrict__ segs, const float* __restrict__ C_all,
+                                  __nv_bfloat16* __restrict__ pk) {
+  constexpr int d = K5_D;
+  const SegDesc sg = segs[blockIdx.x];
+  if (sg.k <= 1 || (long long)sg.L * sg.k <= 1200) return;
+  const int k8 = (sg.k + 7) & ~7;
+  unsigned char* hi = reinterpret_cast<unsigned char*>(pk + ((size_t)sg.c_off + 8 * (size_t)blockIdx.x) * 2 * d);
+  unsigned char* lo = hi + (size_t)k8 * d * 2;
+  const float* C = C_all + (size_t)sg.c_off * d;
+  for (int idx = threadIdx.x; idx < k8 * (d / 8); idx += blockDim.x) {
+    const int c = idx / (d / 8), kg = idx % (d / 8);
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+    if (c < sg.k) {
+      a = *reinterpret_cast<const float4*>(C + (size_t)c * d + 8 * kg);
+      b = *reinterpret_cast<const float4*>(C + (size_t)c * d + 8 * kg + 4);
+    }
+    uint4 h, l;
+    ktc_split(a.x, a.y, h.x, l.x);
+    ktc_split(a.z, a.w, h.y, l.y);
+    ktc_split(b.x, b.y, h.z, l.z);
+    ktc_split(b.z, b.w, h.w, l.w);
+    *reinterpret_cast<uint4*>(hi + k5_off(c, 8 * kg)) = h;
+    *reinterpret_cast<uint4*>(lo + k5_off(c, 8 * kg)) = l;
+  }
+}
+
 __global__ void __launch_bounds__(256, 1) km_assign_tc5_kernel(const SegDesc* __restrict__ segs,
                                                                 const float* __restrict__ P_all,
                                                                 const float* __restrict__ C_all,
-                                                                int32_t* __restrict__ A_all) {
+                                                                int32_t* __restrict__ A_all,
+                                                                const __nv_bfloat16* __restrict__ pk) {
   constexpr int d = K5_D;
   const SegDesc sg = segs[blockIdx.y];
   if (sg.k <= 1) return;
@@ -634,8 +665,8 @@ __global__ void __launch_bounds__(256, 1) km_assign_tc5_kernel(const SegDesc* __
   unsigned char* Al = Ah + K5_A_BYTES;
   unsigned char* Bh = Al + K5_A_BYTES;
   unsigned char* Bl = Bh + K5_B_BYTES;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(Bl + K5_B_BYTES);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(Bl + K5_B_BYTES);  // [0] MMA commits, [1] B bulk copies
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
   const float* P = P_all + (size_t)sg.p_off * d;
   const float* C = C_all + (size_t)sg.c_off * d;
   const int t = threadIdx.x, warp = t >> 5;
@@ -649,6 +680,7 @@ __global__ void __launch_bounds__(256, 1) km_assign_tc5_kernel(const SegDesc* __
   }
   if (t == 0) {
     mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
     fence_mbar_init();
   }
   // points -> A (hi / lo): row t % 128, dims of half t / 128
@@ -667,38 +699,27 @@ __global__ void __launch_bounds__(256, 1) km_assign_tc5_kernel(const SegDesc* __
       *reinterpret_cast<uint4*>(Al + k5_off(row, 8 * kg)) = l;
     }
   }
+  fence_proxy_async();  // A (generic-proxy smem writes) -> visible to the tensor core
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = *tslot;
-  for (int j = 0; j < nchunk; j++) {
-    // centroids [256 j, 256 j + 256) -> B (hi / lo); zero rows past k
-    if (j > 0) {
-      mbar_wait(bar, (uint32_t)((j - 1) & 1));  // the previous chunk's MMAs have read B
-      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    }
-    for (int idx = t; idx < K5_N * (d / 8); idx += blockDim.x) {
-      const int c = idx / (d / 8), kg = idx % (d / 8), cg = j * K5_N + c;
-      float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
-      if (cg < sg.k) {
-        a = *reinterpret_cast<const float4*>(C + (size_t)cg * d + 8 * kg);
-        b = *reinterpret_cast<const float4*>(C + (size_t)cg * d + 8 * kg + 4);
-      }
-      uint4 h, l;
-      ktc_split(a.x, a.y, h.x, l.x);
-      ktc_split(a.z, a.w, h.y, l.y);
-      ktc_split(b.x, b.y, h.z, l.z);
-      ktc_split(b.z, b.w, h.w, l.w);
-      *reinterpret_cast<uint4*>(Bh + k5_off(c, 8 * kg)) = h;
-      *reinterpret_cast<uint4*>(Bl + k5_off(c, 8 * kg)) = l;
-    }
-    fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor core
-    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-    __syncthreads();
-    if (t == 0) {
+  if (t == 0) {
+    // B chunks: one bulk copy each of the pre-split hi / lo rows, MMAs once they land
+    const int k8 = (sg.k + 7) & ~7;
+    const unsigned char* hi = reinterpret_cast<const unsigned char*>(pk + ((size_t)sg.c_off + 8 * (size_t)blockIdx.y) * 2 * d);
+    const unsigned char* lo = hi + (size_t)k8 * d * 2;
+    const uint32_t ah = smem_u32(Ah), al = smem_u32(Al), bh = smem_u32(Bh), bl = smem_u32(Bl);
+    for (int j = 0; j < nchunk; j++) {
+      if (j > 0) mbar_wait(bar, (uint32_t)((j - 1) & 1));  // the previous chunk's MMAs have read B
+      const int rows = min(K5_N, k8 - j * K5_N);
+      const uint32_t bytes = (uint32_t)rows * d * 2;
+      mbar_arrive_expect_tx(bar + 1, 2 * bytes);
+      bulk_g2s(Bh, hi + (size_t)j * K5_N * d * 2, bytes, bar + 1);
+      bulk_g2s(Bl, lo + (size_t)j * K5_N * d * 2, bytes, bar + 1);
+      mbar_wait(bar + 1, (uint32_t)(j & 1));
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       const uint32_t tc = tmem + (uint32_t)(j * K5_N);
-      const uint32_t ah = smem_u32(Ah), al = smem_u32(Al), bh = smem_u32(Bh), bl = smem_u32(Bl);
       uint32_t acc = 0;
 #pragma unroll
       for (int kk = 0; kk < d / 16; kk++) {  // K step: 2 core matrices along K = 256 B
@@ -710,6 +731,8 @@ __global__ void __launch_bounds__(256, 1) km_assign_tc5_kernel(const SegDesc* __
       k5_commit(bar);
     }
   }
+  if (t != 0)  // thread 0 passed these phases in its chunk loop
+    for (int j = 0; j + 1 < nchunk; j++) mbar_wait(bar, (uint32_t)(j & 1));  // phases in order
   mbar_wait(bar, (uint32_t)((nchunk - 1) & 1));
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   // epilogue: warps w and w + 4 read TMEM lanes 32 (w % 4) .. + 31 (their points),
