@@ -590,32 +590,38 @@ def main():
         hkv.copy_(kpool[0][: a.layers].cpu() if kpool[0].shape[0] >= a.layers else hkv.normal_())
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         k_e2e = max(1, min(a.steps, 5))
-        # Pipelined host I/O: layer l's q/k/v go up on an H2D stream while earlier
-        # layers compute; layer l's output comes down on a D2H stream once layer l
-        # is done (its copy overlaps layer l+1).  Both copy engines run beside the
-        # compute stream; the timed region ends when the last output has landed.
+        # Pipelined host I/O: the q/k/v of a group of GR layers go up on an H2D stream
+        # while earlier layers compute; a group's outputs come down on a D2H stream
+        # once its last layer is done (overlapping the next group).  Stream waits /
+        # event records only at group boundaries, so the kernels of a group stay
+        # back to back (programmatic dependent launch).  The timed region ends when
+        # the last output has landed.
+        GR = int(os.environ.get("WK_E2E_GROUP", "4"))
         main = torch.cuda.current_stream()
         up, down = torch.cuda.Stream(), torch.cuda.Stream()
-        ev_in = [torch.cuda.Event() for _ in range(a.layers)]
-        ev_out = [torch.cuda.Event() for _ in range(a.layers)]
+        ngr = -(-a.layers // GR)
+        ev_in = [torch.cuda.Event() for _ in range(ngr)]
+        ev_out = [torch.cuda.Event() for _ in range(ngr)]
         dout = torch.empty((a.layers, U, G, D), device=dev)
         torch.cuda.synchronize()
         e0.record()
         for i in range(k_e2e):
             up.wait_stream(main)
             with torch.cuda.stream(up):
-                for l in range(a.layers):
-                    dq[l].copy_(hq[l], non_blocking=True)
-                    dkv[l].copy_(hkv[l], non_blocking=True)
-                    ev_in[l].record(up)
-            for l in range(a.layers):
-                lay_l = layers[l % n_bufs]
-                main.wait_event(ev_in[l])
-                lay_l.launch_step(dq[l], dkv[l, 0], dkv[l, 1], out=dout[l])
-                ev_out[l].record(main)
-                down.wait_event(ev_out[l])
+                for gi in range(ngr):
+                    l0, l1 = gi * GR, min(a.layers, gi * GR + GR)
+                    dq[l0:l1].copy_(hq[l0:l1], non_blocking=True)
+                    dkv[l0:l1].copy_(hkv[l0:l1], non_blocking=True)
+                    ev_in[gi].record(up)
+            for gi in range(ngr):
+                l0, l1 = gi * GR, min(a.layers, gi * GR + GR)
+                main.wait_event(ev_in[gi])
+                for l in range(l0, l1):
+                    layers[l % n_bufs].launch_step(dq[l], dkv[l, 0], dkv[l, 1], out=dout[l])
+                ev_out[gi].record(main)
+                down.wait_event(ev_out[gi])
                 with torch.cuda.stream(down):
-                    hout[l].copy_(dout[l], non_blocking=True)
+                    hout[l0:l1].copy_(dout[l0:l1], non_blocking=True)
             main.wait_stream(down)
         e1.record()
         torch.cuda.synchronize()
