@@ -313,16 +313,17 @@ int wk_kmeans_segments(const wk_index_view* ix, const wk_segment* segs, int n_se
   };
   const size_t asmem = (size_t)2 * d * 65 * sizeof(float);
   const size_t usmem = (size_t)(2 * max_k + 1) * sizeof(int);
+  const size_t upsmem = usmem + (size_t)16 * d * sizeof(float);  // + per-warp row scratch (512 threads)
   assign();
   km_assign_small_kernel<<<n_segs, 256, 0, s>>>(sd, scr->P, scr->C, scr->A, d);
   WK_CHECK_LAUNCH();
   for (int it = 0; it < kmeans_iters; it++) {
-    km_update_kernel<<<n_segs, 512, usmem, s>>>(sd, scr->P, scr->C, scr->A, scr->perm, scr->sims, d, 0);
+    km_update_kernel<<<n_segs, 512, upsmem, s>>>(sd, scr->P, scr->C, scr->A, scr->perm, scr->sims, d, 0);
     assign();
     km_assign_small_kernel<<<n_segs, 256, 0, s>>>(sd, scr->P, scr->C, scr->A, d);
     WK_CHECK_LAUNCH();
   }
-  km_update_kernel<<<n_segs, 512, usmem, s>>>(sd, scr->P, scr->C, scr->A, scr->perm, scr->sims, d, 1);
+  km_update_kernel<<<n_segs, 512, upsmem, s>>>(sd, scr->P, scr->C, scr->A, scr->perm, scr->sims, d, 1);
   if (store_bf16)
     km_finalize_kernel<__nv_bfloat16><<<n_segs, 256, usmem, s>>>(sd, scr->A, scr->perm, *ix, d, scr->status);
   else

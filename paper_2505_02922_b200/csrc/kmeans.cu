@@ -1023,14 +1023,42 @@ __global__ void km_update_kernel(const SegDesc* __restrict__ segs, const float* 
       }
     }
     __syncthreads();
-    for (int c = threadIdx.x; c < sg.k; c += blockDim.x) {
-      float* row = C + (size_t)c * d;
-      float nr = row_norm_f32(row, d);
-      if (nr != 0.0f) {
-        for (int t = 0; t < d; t++) row[t] = __fdiv_rn(row[t], nr);
-      } else {
-        for (int t = 0; t < d; t++) row[t] = 0.f;
-        row[0] = 1.0f;
+    if (d == 32 || d == 64 || d == 128) {
+      // warp per centroid row, coalesced; the 8 pairwise-norm chains on lanes 0-7
+      // (same bits as row_norm_f32, see km_prep_v2_kernel)
+      float* sq = reinterpret_cast<float*>(cursor + sg.k) + (threadIdx.x >> 5) * d;
+      const int lane = threadIdx.x & 31, epl = d >> 5;
+      for (int c = threadIdx.x >> 5; c < sg.k; c += blockDim.x >> 5) {
+        float* row = C + (size_t)c * d;
+        float x[4];
+#pragma unroll
+        for (int e = 0; e < 4; e++)
+          if (e < epl) { x[e] = row[lane * epl + e]; sq[lane * epl + e] = __fmul_rn(x[e], x[e]); }
+        __syncwarp();
+        float r = 0.f;
+        if (lane < 8) {
+          r = sq[lane];
+          for (int j = 8; j < d; j += 8) r = __fadd_rn(r, sq[j + lane]);
+        }
+        r = __fadd_rn(r, __shfl_down_sync(0xffffffffu, r, 1));
+        r = __fadd_rn(r, __shfl_down_sync(0xffffffffu, r, 2));
+        r = __fadd_rn(r, __shfl_down_sync(0xffffffffu, r, 4));
+        const float nr = __fsqrt_rn(__shfl_sync(0xffffffffu, r, 0));
+        __syncwarp();
+#pragma unroll
+        for (int e = 0; e < 4; e++)
+          if (e < epl) row[lane * epl + e] = nr != 0.f ? __fdiv_rn(x[e], nr) : (lane * epl + e == 0 ? 1.f : 0.f);
+      }
+    } else {
+      for (int c = threadIdx.x; c < sg.k; c += blockDim.x) {
+        float* row = C + (size_t)c * d;
+        float nr = row_norm_f32(row, d);
+        if (nr != 0.0f) {
+          for (int t = 0; t < d; t++) row[t] = __fdiv_rn(row[t], nr);
+        } else {
+          for (int t = 0; t < d; t++) row[t] = 0.f;
+          row[0] = 1.0f;
+        }
       }
     }
     __syncthreads();
