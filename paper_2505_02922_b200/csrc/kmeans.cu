@@ -221,7 +221,10 @@ __global__ void km_seed_kernel(const SegDesc* __restrict__ segs, const float* __
 // grid = n_segments, block = 256
 // ---------------------------------------------------------------------------
 constexpr float KS_EPS = 1e-4f;
-__global__ void __launch_bounds__(256) km_seed_v2_kernel(const SegDesc* __restrict__ segs, const float* __restrict__ P_all,
+#ifndef KS_MINB
+#define KS_MINB 4  // 4 segments per SM (64 registers): the seeding is latency-bound
+#endif
+__global__ void __launch_bounds__(256, KS_MINB) km_seed_v2_kernel(const SegDesc* __restrict__ segs, const float* __restrict__ P_all,
                                                          float* __restrict__ C_all, float* __restrict__ scratch_all,
                                                          int d, int blas_threads, int in_smem,
                                                          const __half* __restrict__ P16_all, int max_k) {
