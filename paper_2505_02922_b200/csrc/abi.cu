@@ -30,7 +30,7 @@ __global__ void attend_kernel(IndexView, SteadyView, StepView, AttnParams, const
 __global__ void merge_kernel(StepView, AttnParams, int);
 size_t select_smem_bytes();
 // select_v6.cu / attend_v4.cu / score_v4.cu
-template <int CAND, bool SMS>
+template <int CAND, bool SMS, int GM>
 __global__ void select_v6_kernel(IndexView, StepView, SelParams);
 size_t select_v6_dyn_smem(int m_max, bool sms, int cand);
 template <typename T, int DPL, int HS, bool FULL, bool OFF>
@@ -182,17 +182,18 @@ static int launch_score_v5(const IndexView& ix, const StepView& sv, int G, int U
   return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? 0 : WK_ECUDA;
 }
 
-static int launch_select_v6(const IndexView& ix, const StepView& sv, const SelParams& p, int U, int m_max,
+template <int GM>
+static int launch_select_v6_g(const IndexView& ix, const StepView& sv, const SelParams& p, int U, int m_max,
                             cudaStream_t s) {
   const double r_max = floor(p.retrieval_fraction * (double)m_max + 0.5) + 1;
   const int blocks = U * p.G;
   static int cfg = 0;
   if (!cfg) {
-    if (cudaFuncSetAttribute(select_v6_kernel<512, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(select_v6_kernel<512, true, GM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)select_v6_dyn_smem(16384, true, 512)) != cudaSuccess ||
-        cudaFuncSetAttribute(select_v6_kernel<512, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(select_v6_kernel<512, false, GM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)select_v6_dyn_smem(262144, false, 512)) != cudaSuccess ||
-        cudaFuncSetAttribute(select_v6_kernel<2048, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(select_v6_kernel<2048, false, GM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)select_v6_dyn_smem(262144, false, 2048)) != cudaSuccess)
       return WK_ECUDA;
     cfg = 1;
@@ -201,17 +202,22 @@ static int launch_select_v6(const IndexView& ix, const StepView& sv, const SelPa
   // the G CTAs of a unit form one thread-block cluster (the union runs over DSMEM)
   cudaError_t e;
   if (m_max <= 16384 && r_max <= 480)
-    e = launch_ex(select_v6_kernel<512, true>, dim3(blocks), dim3(256), select_v6_dyn_smem(m_max, true, 512), s,
+    e = launch_ex(select_v6_kernel<512, true, GM>, dim3(blocks), dim3(256), select_v6_dyn_smem(m_max, true, 512), s,
                   p.G, ix, sv, p);
   else if (r_max <= 480)
-    e = launch_ex(select_v6_kernel<512, false>, dim3(blocks), dim3(256), select_v6_dyn_smem(m_max, false, 512), s,
+    e = launch_ex(select_v6_kernel<512, false, GM>, dim3(blocks), dim3(256), select_v6_dyn_smem(m_max, false, 512), s,
                   p.G, ix, sv, p);
   else if (r_max <= 1900)
-    e = launch_ex(select_v6_kernel<2048, false>, dim3(blocks), dim3(256), select_v6_dyn_smem(m_max, false, 2048),
+    e = launch_ex(select_v6_kernel<2048, false, GM>, dim3(blocks), dim3(256), select_v6_dyn_smem(m_max, false, 2048),
                   s, p.G, ix, sv, p);
   else
     return WK_ECONFIG;
   return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? 0 : WK_ECUDA;
+}
+
+static int launch_select_v6(const IndexView& ix, const StepView& sv, const SelParams& p, int U, int m_max,
+                            cudaStream_t s) {
+  return p.G <= 4 ? launch_select_v6_g<4>(ix, sv, p, U, m_max, s) : launch_select_v6_g<8>(ix, sv, p, U, m_max, s);
 }
 
 template <typename T, int DPL, int HS, bool FULL, bool OFF>

@@ -198,7 +198,7 @@ WK_DEVINL double s6_exact_quad(const double* __restrict__ row, const float* __re
 constexpr int S6_TWC = 2048;            // clusters per staging tile
 constexpr int S6_TWW = S6_TWC / 32;     // bitmap words per tile (16 groups)
 
-template <int CAND, bool SMS>
+template <int CAND, bool SMS, int GM>
 __device__ void s6_union_cl(const IndexView& ix, const StepView& sv, const SelParams& p, int u, int g, int m,
                             Sel6Smem<CAND>& sm, uint32_t* rbits, uint32_t* tre, float* scs) {
   namespace cg = cooperative_groups;
@@ -258,10 +258,10 @@ __device__ void s6_union_cl(const IndexView& ix, const StepView& sv, const SelPa
     a = tw0 + n * warp / S6_NW;
     b = tw0 + n * (warp + 1) / S6_NW;
   };
-  auto load_words = [&](int wl, uint32_t (&rw)[8], uint32_t (&ew)[8], uint32_t& ur, uint32_t& ue) {
+  auto load_words = [&](int wl, uint32_t (&rw)[GM], uint32_t (&ew)[GM], uint32_t& ur, uint32_t& ue) {
     ur = 0u; ue = 0u;
 #pragma unroll
-    for (int h = 0; h < 8; h++) {
+    for (int h = 0; h < GM; h++) {
       rw[h] = h < G ? lw[h * S6_TWW + wl] : 0u;
       ew[h] = h < G ? lw[(G + h) * S6_TWW + wl] : 0u;
       ur |= rw[h];
@@ -274,7 +274,7 @@ __device__ void s6_union_cl(const IndexView& ix, const StepView& sv, const SelPa
     wrange(tw0, tw1, a, b);
     int nr = 0, ne = 0, tok = 0, pcs = 0;
     for (int w = a; w < b; w++) {
-      uint32_t rw[8], ew[8], ur, ue;
+      uint32_t rw[GM], ew[GM], ur, ue;
       load_words(w - tw0, rw, ew, ur, ue);
       nr += __popc(ur);
       ne += __popc(ue);
@@ -358,7 +358,7 @@ __device__ void s6_union_cl(const IndexView& ix, const StepView& sv, const SelPa
     wrange(tw0, tw1, a, b);
     S6_MARK(13);
     for (int w = a; w < b; w++) {
-      uint32_t rw[8], ew[8], ur, ue;
+      uint32_t rw[GM], ew[GM], ur, ue;
       load_words(w - tw0, rw, ew, ur, ue);
       const int c = zb_cluster(w, lane);
       const int ci = c - (tw0 << 5);
@@ -375,7 +375,7 @@ __device__ void s6_union_cl(const IndexView& ix, const StepView& sv, const SelPa
         if (in) {
           int mk = 0;
 #pragma unroll
-          for (int h = 0; h < 8; h++) mk |= ((rw[h] >> lane) & 1u) << h;
+          for (int h = 0; h < GM; h++) mk |= ((rw[h] >> lane) & 1u) << h;
           const int ir = o[0] + __popc(ur & lt);
           ru[ir] = c;
           rmk[ir] = (uint8_t)mk;
@@ -390,7 +390,7 @@ __device__ void s6_union_cl(const IndexView& ix, const StepView& sv, const SelPa
         if ((ue >> lane) & 1u) {
           int mk = 0;
 #pragma unroll
-          for (int h = 0; h < 8; h++) mk |= ((ew[h] >> lane) & 1u) << h;
+          for (int h = 0; h < GM; h++) mk |= ((ew[h] >> lane) & 1u) << h;
           const int ie = o[3] + __popc(ue & lt);
           eu[ie] = c;
           emk[ie] = (uint8_t)mk;
@@ -430,7 +430,7 @@ __device__ void s6_union_cl(const IndexView& ix, const StepView& sv, const SelPa
 }
 
 // ---------------------------------------------------------------------------
-template <int CAND, bool SMS>
+template <int CAND, bool SMS, int GM>
 __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepView sv, SelParams p) {
   extern __shared__ __align__(16) unsigned char s6_raw[];  // Sel6Smem | SMS: scores [m] | bitmaps R, TRE [W]
   Sel6Smem<CAND>& sm = *reinterpret_cast<Sel6Smem<CAND>*>(s6_raw);
@@ -807,7 +807,7 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
   // ---- the unit's G CTAs (one cluster) build the union together ----
   cooperative_groups::this_cluster().sync();  // every head's R / E bitmaps final in its smem
   S6_MARK(10);
-  s6_union_cl<CAND, SMS>(ix, sv, p, u, g, m, sm, rbits, tre, scs);
+  s6_union_cl<CAND, SMS, GM>(ix, sv, p, u, g, m, sm, rbits, tre, scs);
   S6_MARK(11);
   if (p.prof && t == 0) { g_sel_dbg[blockIdx.x][12] = sm.ncand; }
 }
@@ -818,9 +818,13 @@ size_t select_v6_dyn_smem(int m_max, bool sms, int cand) {
   return ((hdr + 15) & ~(size_t)15) + (size_t)(sms ? ((m_max + 3) & ~3) : 0) * 4 + (size_t)2 * W * 4;
 }
 
-template __global__ void select_v6_kernel<512, true>(IndexView, StepView, SelParams);
-template __global__ void select_v6_kernel<512, false>(IndexView, StepView, SelParams);
-template __global__ void select_v6_kernel<2048, false>(IndexView, StepView, SelParams);
+// GM: head slots of the unit union (4 for G <= 4, else 8)
+template __global__ void select_v6_kernel<512, true, 4>(IndexView, StepView, SelParams);
+template __global__ void select_v6_kernel<512, false, 4>(IndexView, StepView, SelParams);
+template __global__ void select_v6_kernel<2048, false, 4>(IndexView, StepView, SelParams);
+template __global__ void select_v6_kernel<512, true, 8>(IndexView, StepView, SelParams);
+template __global__ void select_v6_kernel<512, false, 8>(IndexView, StepView, SelParams);
+template __global__ void select_v6_kernel<2048, false, 8>(IndexView, StepView, SelParams);
 
 }  // namespace wk
 
