@@ -512,7 +512,7 @@ def main():
         stream = ctypes.c_void_p(_stream())
         ev[l][0].record()
         _lib.check(lay.L.wk_append_tokens(ctypes.byref(lay._stv), _ptr(kpool[b_][j, 0]), _ptr(kpool[b_][j, 1]),
-                                          lay.U, lay.d, lay.store_bf16, stream), "append")
+                                          lay.U, lay.d, lay.store_bf16, _ptr(lay.status), stream), "append")
         ev[l][1].record()
         sv = lay._step_view(q)
         _lib.check(lay.L.wk_score_topk(ctypes.byref(lay._ixv), ctypes.byref(sv), ctypes.byref(lay._zp), lay.U,

@@ -123,6 +123,13 @@ typedef struct wk_step_view {
   const int32_t* slot_off; /* [U, m_cap] first block of each cluster            */
   int64_t arena_rows, slot_cap;
   int32_t block_tokens, pstride; /* pieces: 2 ints (in HBM) or 4 (offload)      */
+  /* exact selection (index.py:74-75): fp64 queries for the exact re-scoring
+   * (optional; NULL = the fp32 q, exact when q is fp32-representable) and the
+   * scratch of the tie-safe fallback (exact scores of every row + radix select,
+   * csrc/exact_select.cuh) taken when the error band overflows */
+  const double* q64;  /* [U, G, d] or NULL                                      */
+  double* xscr;       /* [U, G, m_cap] (NULL: overflow -> status, no fallback)  */
+  int32_t* xcount;    /* [1] number of (unit, head) fallbacks, or NULL          */
 } wk_step_view;
 
 typedef struct wk_zone_params {
@@ -198,9 +205,10 @@ int wk_kmeans_segments(const wk_index_view* ix, const wk_segment* segs, int n_se
                        void* stream);
 
 /* Append one decode token per unit to the steady buffer
- * (HeadEngine._append_tokens + buffer.append, engine.py:178-182). */
+ * (HeadEngine._append_tokens + buffer.append, engine.py:178-182).  A full
+ * steady buffer writes nothing and sets *status (may be NULL) to 7. */
 int wk_append_tokens(const wk_steady_view* st, const float* k_new, const float* v_new, int U,
-                     int d, int store_bf16, void* stream);
+                     int d, int store_bf16, int* status, void* stream);
 
 /* Centroid scoring over GQA groups + exact zone planning + per-unit unions.
  * Replaces ClusterIndex.rank -> rank_clusters and plan_zones

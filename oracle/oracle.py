@@ -41,6 +41,8 @@ def lib():
         L.wko_engine_new.restype = _P
         L.wko_engine_new.argtypes = [_P, _P]
         L.wko_engine_free.argtypes = [_P]
+        L.wko_engine_clone.restype = _P
+        L.wko_engine_clone.argtypes = [_P]
         L.wko_engine_prefill.argtypes = [_P, _P, _P, ctypes.c_int, ctypes.c_int]
         L.wko_engine_decode.argtypes = [_P, _P, _P, _P, ctypes.c_int, ctypes.c_int, _P, _P]
         L.wko_engine_m.argtypes = [_P]
@@ -250,6 +252,14 @@ class OracleEngine:
         if getattr(self, "_h", None):
             lib().wko_engine_free(self._h)
             self._h = None
+
+    def clone(self):
+        """Independent copy of the engine state (one prefill serves the G
+        heads of a GQA group: the index does not depend on the head)."""
+        x = object.__new__(OracleEngine)
+        x.cfg, x._cfg, x.d = dict(self.cfg), self._cfg, self.d
+        x._h = lib().wko_engine_clone(self._h)
+        return x
 
     def prefill(self, keys, values):
         keys = np.ascontiguousarray(keys, np.float32)

@@ -7,6 +7,8 @@
 #include "wk_oracle.h"
 
 #include <math.h>
+#include <pthread.h>
+#include <unistd.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -686,16 +688,11 @@ static void ensure_clusters(wko_engine* e, int need) {
   e->m_cap = cap;
 }
 
-/* _cluster_batch + finalize_cluster (index.py:43-58, 143-151): tokens are
- * the contiguous token-id range [t0, t0+L) */
-static int cluster_batch(wko_engine* e, int64_t t0, int L, int k, int kind, int64_t idx) {
+/* finalize_cluster for every cluster of one clustered batch (index.py:43-58,
+ * 143-151): tokens are the contiguous token-id range [t0, t0+L), `a` their
+ * assignment (freed here) */
+static int finalize_batch(wko_engine* e, int64_t t0, int L, int k, int64_t* a) {
   int d = e->d;
-  uint64_t words[4];
-  e->seed_fn(e->cfg.rng_seed, kind, idx, words);
-  int64_t* a = (int64_t*)malloc(sizeof(int64_t) * (size_t)L);
-  int rc = wko_spherical_kmeans(e->keys + t0 * d, L, d, k, e->cfg.kmeans_iters, words,
-                                e->cfg.blas_threads, a);
-  if (rc) { free(a); return rc; }
   ensure_clusters(e, e->m + k);
   if (e->mem_len + L > e->mem_cap) {
     while (e->mem_len + L > e->mem_cap) e->mem_cap = e->mem_cap ? 2 * e->mem_cap : 65536;
@@ -736,10 +733,54 @@ static int cluster_batch(wko_engine* e, int64_t t0, int L, int k, int kind, int6
   return 0;
 }
 
+/* _cluster_batch (index.py:143-151): spherical k-means, then finalize */
+static int cluster_batch(wko_engine* e, int64_t t0, int L, int k, int kind, int64_t idx) {
+  uint64_t words[4];
+  e->seed_fn(e->cfg.rng_seed, kind, idx, words);
+  int64_t* a = (int64_t*)malloc(sizeof(int64_t) * (size_t)L);
+  int rc = wko_spherical_kmeans(e->keys + t0 * e->d, L, e->d, k, e->cfg.kmeans_iters, words,
+                                e->cfg.blas_threads, a);
+  if (rc) { free(a); return rc; }
+  return finalize_batch(e, t0, L, k, a);
+}
+
 /* engine._update_capacity (engine.py:98-101) */
 static void update_capacity(wko_engine* e) {
   int64_t want = (int64_t)ceil(e->cfg.cache_fraction * (double)e->n_blocks);
   if (want > e->cache->capacity) e->cache->capacity = want;
+}
+
+/* segment k-means workers of the segmented build (one segment per pull) */
+typedef struct {
+  wko_engine* e;
+  int64_t L;
+  int nseg;
+  const uint64_t* words;
+  int64_t** asg;
+  int next, rc;
+  pthread_mutex_t mu;
+} seg_job;
+
+static void* seg_worker(void* arg) {
+  seg_job* j = (seg_job*)arg;
+  wko_engine* e = j->e;
+  for (;;) {
+    pthread_mutex_lock(&j->mu);
+    const int seg = j->next++;
+    pthread_mutex_unlock(&j->mu);
+    if (seg >= j->nseg) return NULL;
+    int64_t s0 = (int64_t)seg * e->cfg.segment_size;
+    int64_t len = j->L - s0 < e->cfg.segment_size ? j->L - s0 : e->cfg.segment_size;
+    int k = (int)ceil_div(len, e->cfg.centroid_ratio);
+    j->asg[seg] = (int64_t*)malloc(sizeof(int64_t) * (size_t)len);
+    int rc = wko_spherical_kmeans(e->keys + (e->n_sink + s0) * e->d, (int)len, e->d, k, e->cfg.kmeans_iters,
+                                  j->words + 4 * seg, e->cfg.blas_threads, j->asg[seg]);
+    if (rc) {
+      pthread_mutex_lock(&j->mu);
+      j->rc = rc;
+      pthread_mutex_unlock(&j->mu);
+    }
+  }
 }
 
 /* HeadEngine.prefill (engine.py:110-138) */
@@ -762,14 +803,39 @@ int wko_engine_prefill(wko_engine* e, const float* keys, const float* values, in
   if (e->n_sink) pack_blocks(e, e->n_sink);
   ensure_clusters(e, 1);
   e->mem_off[0] = 0;
+  /* segmented_build (index.py:153-166): segments are independent (seed
+   * [rng_seed, 1, seg]), so their k-means runs on all host cores; finalize
+   * and packing stay sequential in segment order (dense ids). */
   int64_t L = index_end - e->n_sink;
-  int seg = 0;
-  for (int64_t s0 = 0; s0 < L; s0 += e->cfg.segment_size, seg++) {
+  int nseg = (int)ceil_div(L, e->cfg.segment_size);
+  uint64_t* words = (uint64_t*)malloc(sizeof(uint64_t) * 4 * (size_t)(nseg > 0 ? nseg : 1));
+  int64_t** asg = (int64_t**)calloc((size_t)(nseg > 0 ? nseg : 1), sizeof(int64_t*));
+  for (int seg = 0; seg < nseg; seg++) e->seed_fn(e->cfg.rng_seed, 1, seg, words + 4 * seg);
+  seg_job job = {e, L, nseg, words, asg, 0, 0};
+  pthread_mutex_init(&job.mu, NULL);
+  long ncpu = sysconf(_SC_NPROCESSORS_ONLN);
+  int nth = (int)(ncpu < 1 ? 1 : ncpu);
+  if (nth > nseg) nth = nseg;
+  pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)(nth > 0 ? nth : 1));
+  int started = 0;
+  for (int i = 1; i < nth; i++)
+    if (pthread_create(&th[started], NULL, seg_worker, &job) == 0) started++;
+  seg_worker(&job);
+  for (int i = 0; i < started; i++) pthread_join(th[i], NULL);
+  free(th);
+  pthread_mutex_destroy(&job.mu);
+  int rc = job.rc ? -1 : 0;
+  for (int seg = 0; seg < nseg; seg++) {
+    int64_t s0 = (int64_t)seg * e->cfg.segment_size;
     int64_t len = L - s0 < e->cfg.segment_size ? L - s0 : e->cfg.segment_size;
     int k = (int)ceil_div(len, e->cfg.centroid_ratio);
-    int rc = cluster_batch(e, e->n_sink + s0, (int)len, k, 1, seg);
-    if (rc) return rc;
+    if (!rc) rc = finalize_batch(e, e->n_sink + s0, (int)len, k, asg[seg]);
+    else free(asg[seg]);
+    asg[seg] = NULL;
   }
+  free(asg);
+  free(words);
+  if (rc) return rc;
   update_capacity(e);
   e->prefilled = 1;
   return 0;
@@ -1009,6 +1075,51 @@ int wko_engine_decode(wko_engine* e, const double* q, const float* knew, const f
 done:
   free(order); free(scores); free(nbuf); free(K); free(V); free(retrieved); free(scratch); free(dropped);
   return rc;
+}
+
+static void* dup_mem(const void* src, size_t bytes) {
+  if (!src || !bytes) return NULL;
+  void* d = malloc(bytes);
+  memcpy(d, src, bytes);
+  return d;
+}
+
+static wko_cache* cache_clone(const wko_cache* c) {
+  if (!c) return NULL;
+  wko_cache* x = (wko_cache*)malloc(sizeof(wko_cache));
+  *x = *c;
+  size_t n = (size_t)c->cap_cl;
+  x->nblocks = (int32_t*)dup_mem(c->nblocks, 4 * n);
+  x->cached = (int32_t*)dup_mem(c->cached, 4 * n);
+  x->slot_off = (int64_t*)dup_mem(c->slot_off, 8 * n);
+  x->last_access = (int64_t*)dup_mem(c->last_access, 8 * n);
+  x->prev = (int32_t*)dup_mem(c->prev, 4 * n);
+  x->next = (int32_t*)dup_mem(c->next, 4 * n);
+  x->touched = (uint8_t*)dup_mem(c->touched, n);
+  x->slot_ids = (int32_t*)dup_mem(c->slot_ids, 4 * (size_t)c->slot_ids_cap);
+  x->heap = (int32_t*)dup_mem(c->heap, 4 * (size_t)c->heap_cap);
+  x->ev = (ev_t*)dup_mem(c->ev, sizeof(ev_t) * (size_t)c->ev_cap);
+  return x;
+}
+
+/* Deep copy of an engine: the G heads of a GQA group build the identical
+ * index (the seeds do not depend on the head, index.py:162), so tests prefill
+ * once and clone per head (test infrastructure). */
+wko_engine* wko_engine_clone(const wko_engine* e) {
+  wko_engine* x = (wko_engine*)malloc(sizeof(wko_engine));
+  *x = *e;
+  size_t d = (size_t)(e->d > 0 ? e->d : 0), mc = (size_t)e->m_cap;
+  x->keys = (float*)dup_mem(e->keys, sizeof(float) * (size_t)e->cap_tokens * d);
+  x->values = (float*)dup_mem(e->values, sizeof(float) * (size_t)e->cap_tokens * d);
+  x->C = (double*)dup_mem(e->C, sizeof(double) * mc * d);
+  x->VS = (double*)dup_mem(e->VS, sizeof(double) * mc * d);
+  x->sizes = (int64_t*)dup_mem(e->sizes, sizeof(int64_t) * mc);
+  x->mem_off = (int64_t*)dup_mem(e->mem_off, sizeof(int64_t) * (mc + 1));
+  x->members = (int32_t*)dup_mem(e->members, sizeof(int32_t) * (size_t)e->mem_cap);
+  x->last_r = x->last_e = NULL;
+  x->n_last_r = x->n_last_e = 0;
+  x->cache = cache_clone(e->cache);
+  return x;
 }
 
 int wko_engine_m(const wko_engine* e) { return e->m; }

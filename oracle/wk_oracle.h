@@ -81,6 +81,7 @@ typedef struct {
 typedef void (*wko_seed_fn)(int64_t rng_seed, int kind, int64_t idx, uint64_t out[4]);
 
 wko_engine* wko_engine_new(const wko_config* cfg, wko_seed_fn seed_fn);
+wko_engine* wko_engine_clone(const wko_engine* e);
 void wko_engine_free(wko_engine* e);
 int wko_engine_prefill(wko_engine* e, const float* keys, const float* values, int n, int d);
 int wko_engine_decode(wko_engine* e, const double* q, const float* k, const float* v,

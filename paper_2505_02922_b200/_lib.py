@@ -52,7 +52,7 @@ class StepViewC(ctypes.Structure):
                 ("eu_x", _P), ("eu_sz", _P), ("rbits", _P), ("ebits", _P), ("pieces", _P),
                 ("woff", _P), ("w_cap", _I32), ("pc_cap", _I32), ("arena_k", _P), ("arena_v", _P),
                 ("slot_ids", _P), ("slot_off", _P), ("arena_rows", _I64), ("slot_cap", _I64),
-                ("block_tokens", _I32), ("pstride", _I32)]
+                ("block_tokens", _I32), ("pstride", _I32), ("q64", _P), ("xscr", _P), ("xcount", _P)]
 
 
 class CacheViewC(ctypes.Structure):
@@ -103,7 +103,7 @@ def lib():
     L.wk_kmeans_segments.argtypes = [R(IndexViewC), R(SegmentC), ctypes.c_int, R(BuildScratchC),
                                      ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                      ctypes.c_int, ctypes.c_int, _P]
-    L.wk_append_tokens.argtypes = [R(SteadyViewC), _P, _P, ctypes.c_int, ctypes.c_int, ctypes.c_int, _P]
+    L.wk_append_tokens.argtypes = [R(SteadyViewC), _P, _P, ctypes.c_int, ctypes.c_int, ctypes.c_int, _P, _P]
     L.wk_score_topk.argtypes = [R(IndexViewC), R(StepViewC), R(ZoneParamsC), ctypes.c_int,
                                 ctypes.c_int, _P]
     L.wk_tripartite_attn.argtypes = [R(IndexViewC), R(SteadyViewC), R(StepViewC), R(ZoneParamsC),
@@ -145,6 +145,7 @@ STATUS_TEXT = {
     4: "zone union overflow",
     5: "unknown cluster id",
     6: "merge requires at least one non-empty partial",
+    7: "steady buffer full (decode capacity)",
 }
 
 

@@ -21,7 +21,7 @@ template <typename T>
 __global__ void km_finalize_kernel(const SegDesc*, const int32_t*, int32_t*, IndexView, int, int*);
 // decode.cu
 template <typename T>
-__global__ void append_kernel(SteadyView, const float*, const float*, int);
+__global__ void append_kernel(SteadyView, const float*, const float*, int, int*);
 __global__ void score_kernel(IndexView, StepView, int, int);
 __global__ void select_kernel(IndexView, StepView, SelParams);
 __global__ void union_kernel(IndexView, StepView);
@@ -343,11 +343,11 @@ int wk_kmeans_segments(const wk_index_view* ix, const wk_segment* segs, int n_se
 }
 
 int wk_append_tokens(const wk_steady_view* st, const float* k_new, const float* v_new, int U, int d,
-                     int store_bf16, void* stream) {
+                     int store_bf16, int* status, void* stream) {
   if (!st || U <= 0 || d <= 0) return WK_ECONFIG;
   cudaStream_t s = (cudaStream_t)stream;
-  if (store_bf16) append_kernel<__nv_bfloat16><<<U, 128, 0, s>>>(*st, k_new, v_new, d);
-  else append_kernel<float><<<U, 128, 0, s>>>(*st, k_new, v_new, d);
+  if (store_bf16) append_kernel<__nv_bfloat16><<<U, 128, 0, s>>>(*st, k_new, v_new, d, status);
+  else append_kernel<float><<<U, 128, 0, s>>>(*st, k_new, v_new, d, status);
   WK_CHECK_LAUNCH();
   return 0;
 }
@@ -491,7 +491,7 @@ int wk_decode_step(const wk_index_view* ix, const wk_steady_view* st, const wk_s
   if (!ix || !st || !sv || !zp || !k_new || !v_new || U <= 0) return WK_ECONFIG;
   if (!v6_ok(ix, sv, zp->d) || sv->pstride != 2 || m_max <= 0) {
     // generic path: separate append
-    int rc = wk_append_tokens(st, k_new, v_new, U, zp->d, store_bf16, stream);
+    int rc = wk_append_tokens(st, k_new, v_new, U, zp->d, store_bf16, sv->status, stream);
     if (rc) return rc;
     rc = wk_score_topk(ix, sv, zp, U, m_max, stream);
     if (rc) return rc;

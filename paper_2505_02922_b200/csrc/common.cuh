@@ -22,6 +22,7 @@ enum : int {
   kErrUnion = 4,          // union list overflow
   kErrUnknownCluster = 5, // cache access to an unregistered cluster
   kErrEmptyMerge = 6,     // all partials empty (attention.py:117-119)
+  kErrSteadyFull = 7,     // decode append beyond the steady buffer capacity
 };
 
 WK_DEVINL void set_status(int* status, int code) {

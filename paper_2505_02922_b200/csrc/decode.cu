@@ -16,6 +16,7 @@
 //             engine.py:150-172), merged and eq2 denominator modes
 #include "common.cuh"
 #include "decode_internal.h"
+#include "exact_select.cuh"
 
 namespace wk {
 
@@ -25,23 +26,28 @@ namespace wk {
 // ---------------------------------------------------------------------------
 template <typename T>
 __global__ void append_kernel(SteadyView st, const float* __restrict__ k_new,
-                              const float* __restrict__ v_new, int d) {
+                              const float* __restrict__ v_new, int d, int* status) {
   const int u = blockIdx.x;
   const int row = st.n[u];
+  if (row >= st.t_cap) {  // capacity: the host checks first; never write past the buffer
+    if (threadIdx.x == 0 && status) atomicCAS(status, 0, (int)kErrSteadyFull);
+    return;
+  }
   T* kd = (T*)st.k + ((size_t)u * st.t_cap + row) * d;
   T* vd = (T*)st.v + ((size_t)u * st.t_cap + row) * d;
   for (int t = threadIdx.x; t < d; t += blockDim.x) {
     kd[t] = KV<T>::from_f(k_new[(size_t)u * d + t]);
     vd[t] = KV<T>::from_f(v_new[(size_t)u * d + t]);
   }
+  __syncthreads();  // every thread read n[u] before it advances
   if (threadIdx.x == 0) {
     st.tok[(size_t)u * st.t_cap + row] = st.next_tok[u];
     st.next_tok[u] += 1;
     st.n[u] = row + 1;
   }
 }
-template __global__ void append_kernel<float>(SteadyView, const float*, const float*, int);
-template __global__ void append_kernel<__nv_bfloat16>(SteadyView, const float*, const float*, int);
+template __global__ void append_kernel<float>(SteadyView, const float*, const float*, int, int*);
+template __global__ void append_kernel<__nv_bfloat16>(SteadyView, const float*, const float*, int, int*);
 
 // ---------------------------------------------------------------------------
 // score: warp per C row, lanes split d (float4), G heads per row read.
@@ -222,7 +228,8 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(IndexView ix, StepV
   const float* s = sv.scores + ((size_t)u * G + g) * ix.m_cap;
   const float* q = sv.q + ((size_t)u * G + g) * d;
   const int* csize = ix.cl_size + (size_t)u * ix.m_cap;
-  for (int t = threadIdx.x; t < d; t += blockDim.x) sm.q64[t] = (double)q[t];
+  const double* q64 = sv.q64 ? sv.q64 + ((size_t)u * G + g) * d : nullptr;
+  for (int t = threadIdx.x; t < d; t += blockDim.x) sm.q64[t] = q64 ? q64[t] : (double)q[t];
   if (r > RL_CAP) { set_status(sv.status, kErrBandOverflow); return; }
   // ---- error bound B >= |s'_c - s_c| for every row -------------------------
   float qq = 0.f;
@@ -233,7 +240,8 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(IndexView ix, StepV
   float cmax = block_reduce(cm, true, sm);
   const double uu = 5.9604644775390625e-08;  // 2^-24
   const double gam = (double)d * uu / (1.0 - (double)d * uu);
-  const double B = score_error_bound((double)qn2, (double)cmax, d, p.score_fp64 != 0);
+  // with fp64 queries the scan's fp32 q adds 2^-24 |q| |C|
+  const double B = score_error_bound((double)qn2, (double)cmax, d, p.score_fp64 != 0) * (q64 ? 1.6 : 1.0);
   const double B2 = 2.0 * B;
   // ---- thresholds -------------------------------------------------------------
   const float tau_r = u2f_ord(radix_kth_largest(s, m, r, sm));
@@ -263,11 +271,50 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(IndexView ix, StepV
   }
   __syncthreads();
   const int nbr = sm.n_band_r, nbe = sm.n_band_e, nin_r = sm.n_in_r, nin_e = sm.n_in_e;
+  int32_t* rl_out = sv.rlist + ((size_t)u * G + g) * sv.r_cap;
+  uint32_t* zm = sv.zmask + (size_t)u * ix.m_cap;
+  int32_t* el_out = sv.elist ? sv.elist + ((size_t)u * G + g) * sv.e_cap : nullptr;
   if (nbr > BAND_CAP || nbe > BAND_CAP || nin_r > r || nin_r + nbr < r ||
       (e > 0 && (nin_e > r + e || nin_e + nbe < r + e))) {
-    set_status(sv.status, kErrBandOverflow);
-    return;
-  }
+    // dense ties / band overflow: exact scores of every row + radix select
+    // (exact_select.cuh), R ordered by counting
+    if (!sv.xscr) {
+      set_status(sv.status, kErrBandOverflow);
+      return;
+    }
+    double* xs = sv.xscr + ((size_t)u * G + g) * ix.m_cap;
+    xs_score_rows(ix.C64 + (size_t)u * ix.m_cap * d, sm.q64, m, d, p.blas_threads, xs);
+    if (threadIdx.x == 0) { sm.n_rl = 0; sm.n_in_e = 0; }
+    __syncthreads();
+    auto key = [&](int c) { return xs_key(__ldcg(xs + c)); };
+    auto idf = [&](int c) { return (unsigned)c; };
+    unsigned long long k1, k2 = 0ull;
+    unsigned i1, i2 = 0u;
+    xs_select(m, r, key, idf, sm.bid_r, k1, i1);
+    if (e > 0) xs_select(m, r + e, key, idf, sm.bid_r, k2, i2);
+    for (int c = threadIdx.x; c < m; c += blockDim.x) {
+      const unsigned long long kk = key(c);
+      if (xs_in(kk, (unsigned)c, k1, i1)) {
+        const int pos = atomicAdd(&sm.n_rl, 1);
+        sm.rl[pos] = (unsigned long long)(unsigned)c;
+        sm.ex[pos] = __ldcg(xs + c);
+      } else if (e > 0 && xs_in(kk, (unsigned)c, k2, i2)) {
+        atomicOr(zm + c, 1u << (8 + g));
+        if (el_out) el_out[atomicAdd(&sm.n_in_e, 1)] = c;
+      }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < r; i += blockDim.x) {
+      const double ei = sm.ex[i];
+      const int ii = key_id(sm.rl[i]);
+      int rk = 0;
+      for (int j = 0; j < r; j++) rk += exact_better(sm.ex[j], key_id(sm.rl[j]), ei, ii) ? 1 : 0;
+      rl_out[rk] = ii;
+      atomicOr(zm + ii, 1u << g);
+    }
+    if (threadIdx.x == 0 && sv.xcount) atomicAdd(sv.xcount, 1);
+    __syncthreads();
+  } else {
   // ---- exact fp64 re-scoring of the bands (reference dgemv recipe) ------------
   for (int i = threadIdx.x; i < nbr; i += blockDim.x)
     sm.bex_r[i] = exact_score(ix, u, sm.bid_r[i], m, d, p.blas_threads, sm.q64);
@@ -343,8 +390,6 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(IndexView ix, StepV
   }
   __syncthreads();
   // ---- outputs: ordered retrieval list, zone masks ---------------------------
-  int32_t* rl_out = sv.rlist + ((size_t)u * G + g) * sv.r_cap;
-  uint32_t* zm = sv.zmask + (size_t)u * ix.m_cap;
   for (int i = threadIdx.x; i < r; i += blockDim.x) {
     int c = key_id(sm.rl[i]);
     rl_out[i] = c;
@@ -352,7 +397,6 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(IndexView ix, StepV
   }
   __threadfence_block();
   __syncthreads();
-  int32_t* el_out = sv.elist ? sv.elist + ((size_t)u * G + g) * sv.e_cap : nullptr;
   if (threadIdx.x == 0) sm.n_in_e = 0;  // reuse as E cursor
   __syncthreads();
   if (e > 0) {
@@ -371,6 +415,7 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(IndexView ix, StepV
     }
   }
   __syncthreads();
+  }  // exact band path
   // ---- tail / all-cluster denominator terms (engine.py:153-172) ---------------
   if (p.need_tail || p.need_allc) {
     const float isd = p.inv_sqrt_d;

@@ -1133,6 +1133,8 @@ __global__ void km_finalize_kernel(const SegDesc* __restrict__ segs, const int32
     float s = 0.f;
     for (int t = 0; t < d; t++) s = fmaf(cr[t], cr[t], s);
     ix.Cnorm[row] = sqrtf(s);
+    // the unit's max centroid norm: the scan's error bound (score_error_bound_v2)
+    if (ix.Cmax) atomicMax(reinterpret_cast<int*>(ix.Cmax + u), __float_as_int(sqrtf(s)));  // >= 0
   }
 }
 

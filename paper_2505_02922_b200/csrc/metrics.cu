@@ -9,6 +9,7 @@
 // batched engine leaves it off).
 #include "common.cuh"
 #include "decode_internal.h"
+#include "exact_select.cuh"
 
 namespace wk {
 
@@ -50,7 +51,8 @@ __global__ void __launch_bounds__(512) recall_kernel(IndexView ix, SteadyView st
   const T* stk = (const T*)st.k + (int64_t)u * st.t_cap * d;
   const int32_t* stok = ix.store_tok + (int64_t)u * ix.s_cap;
   const int32_t* sttok = st.tok + (int64_t)u * st.t_cap;
-  for (int t = threadIdx.x; t < d; t += blockDim.x) sm.q64[t] = (double)q[t];
+  const double* q64 = sv.q64 ? sv.q64 + ((int64_t)u * G + g) * d : nullptr;
+  for (int t = threadIdx.x; t < d; t += blockDim.x) sm.q64[t] = q64 ? q64[t] : (double)q[t];
   // retrieved store rows: clusters of this head's retrieval list
   for (int i = threadIdx.x; i < ns; i += blockDim.x) rf[i] = 0;
   __syncthreads();
@@ -82,7 +84,7 @@ __global__ void __launch_bounds__(512) recall_kernel(IndexView ix, SteadyView st
   const double uu = 5.9604644775390625e-08;
   const double gam = (double)d * uu / (1.0 - (double)d * uu);
   const double B = 2.0 * (gam + 1e-13) * (1.0 + 1e-5) * sqrt((double)qn2) * sqrt((double)kn2) * (1.0 + 1e-5);
-  const double B2 = 2.0 * B;
+  const double B2 = 2.0 * B * (q64 ? 1.5 : 1.0);  // fp64 queries: + the fp32 q rounding
   const float tau = u2f_ord(radix_kth_largest(s, n, K, ssm));
   if (threadIdx.x == 0) { sm.n_in = 0; sm.n_band = 0; sm.n_hit = 0; }
   __syncthreads();
@@ -99,7 +101,28 @@ __global__ void __launch_bounds__(512) recall_kernel(IndexView ix, SteadyView st
   __syncthreads();
   const int nb = sm.n_band, nin = sm.n_in;
   if (nb > BAND_CAP || nin > K || nin + nb < K) {
-    set_status(sv.status, kErrBandOverflow);
+    // dense ties (e.g. identical keys): exact selection over every token,
+    // scores recomputed per radix pass (exact_select.cuh), ties to the lower
+    // token id as lexsort (metrics.py:15)
+    auto tok_of = [&](int i) { return i < ns ? stok[i] : sttok[i - ns]; };
+    auto key = [&](int i) {
+      const T* kr = i < ns ? sk + (int64_t)i * d : stk + (int64_t)(i - ns) * d;
+      double kd[256];
+      load_row_f64(kr, kd, d);
+      return xs_key(dgemv_row(kd, sm.q64, d, gemv_row_class(tok_of(i), n, d, blas_threads)));
+    };
+    auto idf = [&](int i) { return (unsigned)tok_of(i); };
+    unsigned long long tk;
+    unsigned ti;
+    xs_select(n, K, key, idf, sm.bid, tk, ti);
+    if (threadIdx.x == 0) sm.n_hit = 0;
+    __syncthreads();
+    int hit = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+      if ((i >= ns || rf[i]) && xs_in(key(i), idf(i), tk, ti)) hit++;
+    atomicAdd(&sm.n_hit, hit);
+    __syncthreads();
+    if (threadIdx.x == 0) recall_out[ug] = K == 0 ? 1.f : (float)sm.n_hit / (float)K;
     return;
   }
   // exact fp64 scores in the reference's row recipe (row = token id in keys[:n])

@@ -21,12 +21,12 @@
 //      work lists of attend_v4.
 #include "common.cuh"
 #include "decode_internal.h"
+#include "exact_select.cuh"
 
 #include <cooperative_groups.h>
 
 namespace wk {
 
-__device__ long long g_sel_dbg[4096][16];  // per-CTA phase timestamps (globaltimer, ns), SelParams.prof
 
 constexpr int S6_T = 256;
 constexpr int S6_NW = S6_T / 32;
@@ -57,15 +57,6 @@ struct Sel6Smem {
   float fred[3];
 };
 
-// phase timestamps (globaltimer) for tools/seltime6.py when p.prof != 0
-#define S6_MARK(i)                                                                     \
-  do {                                                                                 \
-    if (p.prof && threadIdx.x == 0 && blockIdx.x < 4096) {                             \
-      long long _t;                                                                    \
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                           \
-      g_sel_dbg[blockIdx.x][i] = _t;                                                   \
-    }                                                                                  \
-  } while (0)
 
 WK_DEVINL unsigned long long s6_key(float s, int id) {
   return ((unsigned long long)(~f2u_ord(s)) << 32) | (unsigned int)id;
@@ -147,34 +138,6 @@ WK_DEVINL void s6_scan4(int (&v)[4], int (&tot)[4], Sel6Smem<CAND>& sm) {
     v[i] = ex;
   }
   __syncthreads();
-}
-
-// exact dgemv-recipe scores (index.py:74 via OpenBLAS dgemv_t, DESIGN.md
-// "Numerics recipes"): item `it` of the warp's 8 rows is served by lanes
-// 4*(it%8) .. +3; lane j accumulates chain j.  Returns the score on every lane
-// of the quad.
-WK_DEVINL double s6_exact_quad(const double* __restrict__ row, const float* __restrict__ q, int d, int cls, bool act) {
-  const int j = threadIdx.x & 3;
-  double acc = 0.0;
-  if (act) {
-    if (cls == 0) {
-#pragma unroll 16
-      for (int t = j; t < d; t += 4) acc = __fma_rn(__ldcg(row + t), (double)__ldg(q + t), acc);
-    } else if (cls == 1) {
-      if (j < 2) {
-#pragma unroll 8
-        for (int t = j; t < d; t += 2) acc = __dadd_rn(acc, __dmul_rn(__ldcg(row + t), (double)__ldg(q + t)));
-      }
-    } else {
-#pragma unroll 8
-      for (int t = j; t < d; t += 4) acc = __dadd_rn(acc, __dmul_rn(__ldcg(row + t), (double)__ldg(q + t)));
-    }
-  }
-  const int base = (threadIdx.x & 31) & ~3;
-  const double a0 = __shfl_sync(0xffffffffu, acc, base), a1 = __shfl_sync(0xffffffffu, acc, base + 1),
-               a2 = __shfl_sync(0xffffffffu, acc, base + 2), a3 = __shfl_sync(0xffffffffu, acc, base + 3);
-  if (cls == 1) return __dadd_rn(0.0, __dadd_rn(a0, a1));
-  return __dadd_rn(0.0, __dadd_rn(__dadd_rn(a0, a2), __dadd_rn(a1, a3)));
 }
 
 // ---------------------------------------------------------------------------
@@ -314,7 +277,6 @@ __device__ void s6_union_cl(const IndexView& ix, const StepView& sv, const SelPa
     sm.wsum[t][0] = tot;
   }
   __syncthreads();
-  S6_MARK(15);
   const int n_ru = sm.wsum[0][0], n_rt = sm.wsum[1][0], n_pc = sm.wsum[2][0], n_eu = sm.wsum[3][0];
   const bool fits = n_pc <= sv.pc_cap && n_eu <= sv.eu_cap && n_ru <= sv.ru_cap;
   if (g == 0 && t == 0) {
@@ -356,7 +318,6 @@ __device__ void s6_union_cl(const IndexView& ix, const StepView& sv, const SelPa
     }
     int a, b;
     wrange(tw0, tw1, a, b);
-    S6_MARK(13);
     for (int w = a; w < b; w++) {
       uint32_t rw[GM], ew[GM], ur, ue;
       load_words(w - tw0, rw, ew, ur, ue);
@@ -399,7 +360,6 @@ __device__ void s6_union_cl(const IndexView& ix, const StepView& sv, const SelPa
         o[3] += __popc(ue);
       }
     }
-    S6_MARK(14);
 #pragma unroll
     for (int i = 0; i < 4; i++) tb[i] += ttot[i];
   }
@@ -444,8 +404,9 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
   if (p.k_new && g == 0) {
     // append this step's token to the unit's steady buffer (engine.py:178-182)
     const int row = p.st.n[u];
+    const bool fits = row < p.st.t_cap;
     const size_t o = ((size_t)u * p.st.t_cap + row) * d;
-    for (int i = t; i < d; i += T) {
+    for (int i = t; fits && i < d; i += T) {
       const float kv = p.k_new[(size_t)u * d + i], vv = p.v_new[(size_t)u * d + i];
       if (p.store_bf16) {
         reinterpret_cast<__nv_bfloat16*>(p.st.k)[o + i] = __float2bfloat16_rn(kv);
@@ -455,10 +416,15 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
         reinterpret_cast<float*>(p.st.v)[o + i] = vv;
       }
     }
+    __syncthreads();  // every thread read n[u] before it advances
     if (t == 0) {
-      p.st.tok[(size_t)u * p.st.t_cap + row] = p.st.next_tok[u];
-      p.st.next_tok[u] += 1;
-      p.st.n[u] = row + 1;
+      if (fits) {
+        p.st.tok[(size_t)u * p.st.t_cap + row] = p.st.next_tok[u];
+        p.st.next_tok[u] += 1;
+        p.st.n[u] = row + 1;
+      } else {
+        set_status(sv.status, kErrSteadyFull);
+      }
     }
   }
   float* scs = s6_dyn;
@@ -476,12 +442,15 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
   if (t == 0 && g == 0) { sv.nr[u] = r; sv.ne[u] = e; }
   const float* s = sv.scores + ((size_t)u * G + g) * ix.m_cap;
   const float* q = sv.q + ((size_t)u * G + g) * d;
+  const double* q64 = sv.q64 ? sv.q64 + ((size_t)u * G + g) * d : nullptr;
   const double* C64 = ix.C64 + (size_t)u * ix.m_cap * d;
   uint32_t* rb_out = sv.rbits + ((size_t)u * G + g) * sv.w_cap;
   uint32_t* eb_out = sv.ebits + ((size_t)u * G + g) * sv.w_cap;
   auto S_ = [&](int c) -> float { return SMS ? scs[c] : __ldcg(s + c); };
-  bool ok = m > 0 && r <= CAND && r <= sv.r_cap;
-  if (m > 0 && !ok) set_status(sv.status, kErrBandOverflow);
+  // capacity (r fits the candidate and output lists): a configuration error
+  const bool cap_ok = m > 0 && r <= CAND && r <= sv.r_cap;
+  if (m > 0 && !cap_ok) set_status(sv.status, kErrBandOverflow);
+  bool ok = cap_ok;
   for (int w = t; w < W; w += T) { rbits[w] = 0u; tre[w] = 0u; }
   double B2 = 0.0;
   float bk_mn = 0.f, bk_scale = 0.f;
@@ -500,9 +469,8 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
                           : (double)bk_mn + (double)(b + 1) / ((double)bk_scale * (1.0 - 1.1920928955078125e-07));
   };
   double hr = 0, lr = 0, he = 0, le = 0;
-  if (ok) {
-  S6_MARK(0);
-    // ---- pass A: stage scores, min / max, |q|^2 ----
+  if (m > 0) {
+    // ---- pass A: stage scores, min / max, |q|^2 (always: the union reads them) ----
     float mn = INFINITY, mx = -INFINITY;
     const int m4 = m >> 2;
 #pragma unroll 4
@@ -524,12 +492,17 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
     float nmn = -mn;
     s6_reduce3(qq, mx, nmn, sm);
     mn = -nmn;
-    const double B = score_error_bound_v2((double)qq, (double)ix.Cmax[u], d, p.score_mode);
+    // |s' - s| <= B; with fp64 queries the scan's fp32 q adds 2^-24 |q| |C|
+    const double B = score_error_bound_v2((double)qq, (double)ix.Cmax[u], d, p.score_mode) * (q64 ? 1.6 : 1.0);
     B2 = 2.0 * B;
     const float span = mx - mn;
     bk_mn = mn;
     bk_scale = span > 0.f ? (float)S6_NB / span : 0.f;
-  S6_MARK(1);
+    // a zero span (every score tied: q = 0, q orthogonal to every centroid,
+    // a single cluster) or a non-finite one goes to the exact path
+    if (!(span > 0.f) || !(bk_scale < INFINITY)) ok = false;
+  }
+  if (ok) {
     // ---- pass B: histogram ----
 #pragma unroll 4
     for (int c = t; c < m; c += T) atomicAdd(&sm.x.hist[bucket(S_(c))], 1);
@@ -571,7 +544,6 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
       }
     }
     __syncthreads();
-  S6_MARK(2);
     // tau_r (the r-th largest s') lies in bucket b1, tau_e in b2: rows above
     // edge_hi + 2B are certainly in, rows below edge_lo - 2B certainly out
     const int b1 = sm.b1, b2 = sm.b2;
@@ -579,7 +551,6 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
     hr = edge_hi(b1) + B2; lr = edge_lo(b1) - B2;
     if (e > 0) { he = edge_hi(b2) + B2; le = edge_lo(b2) - B2; }
   }
-  S6_MARK(3);
   if (ok) {
     // ---- pass D: candidates for R (certain-in + band), band around tau_e,
     //      certain members of the top r+e (bitmap, one ballot per word).
@@ -643,7 +614,6 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
     if (sm.ovf || nin_r > r || nc < r || (e > 0 && (nin_e > r + e || nin_e + nbe < r + e))) {
       ok = false;
     } else {
-  S6_MARK(4);
       // ---- order candidates by (approx desc, id asc): rank by counting ----
       for (int i = t; i < nc; i += T) {
         const unsigned long long k = sm.y.cand[i];
@@ -668,7 +638,6 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
         s6_append(need, i, sm.xpos, &sm.nx, CAND, &sm.ovf);
       }
       __syncthreads();
-  S6_MARK(5);
       // ---- one exact round: 8 rows per warp, 4 lanes per row ----
       const int nx = sm.nx, nall = nx + nbe;
       for (int b0 = warp * 8; b0 < nall; b0 += S6_NW * 8) {
@@ -676,14 +645,14 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
         const bool act = it < nall;
         const int c = !act ? 0 : (it < nx ? s6_id(sm.cs[sm.xpos[it]]) : sm.be_id[it - nx]);
         const int cls = gemv_row_class(c, m, d, p.blas_threads);
-        const double ex = s6_exact_quad(C64 + (size_t)c * d, q, d, cls, act);
+        const double ex = q64 ? xs_exact_quad(C64 + (size_t)c * d, q64, d, cls, act)
+                              : xs_exact_quad(C64 + (size_t)c * d, q, d, cls, act);
         if (act && (lane & 3) == 0) {
           if (it < nx) sm.y.cex[sm.xpos[it]] = ex;
           else sm.be_ex[it - nx] = ex;
         }
       }
       __syncthreads();
-  S6_MARK(6);
       // ---- band winners for R: best (r - nin_r) band rows by exact score ----
       const int need_r = r - nin_r;
       for (int i = nin_r + t; i < nc; i += T) {
@@ -713,7 +682,6 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
       for (int i = t; i < nbe; i += T)
         if (sm.be_sel[i]) atomicOr(tre + zb_word(sm.be_id[i]), 1u << zb_bit(sm.be_id[i]));
       __syncthreads();
-  S6_MARK(7);
       // every maximal run of approx-order neighbours closer than 2B was
       // exact-scored: sort each run exactly (insertion sort by its first thread)
       for (int i = t; i < r; i += T) {
@@ -738,63 +706,107 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
         }
       }
       __syncthreads();
-  S6_MARK(8);
-      // ---- outputs: ordered retrieval list, R bitmap ----
-      int32_t* rl_out = sv.rlist + ((size_t)u * G + g) * sv.r_cap;
-      for (int i = t; i < r; i += T) {
-        const int c = s6_id(sm.x.f.fin[i]);
-        rl_out[i] = c;
-        atomicOr(rbits + zb_word(c), 1u << zb_bit(c));
+    }
+  }
+  if (cap_ok && !ok && sv.xscr) {
+    // ---- tie-safe exact path (exact_select.cuh): exact scores of every row,
+    //      96-bit radix select of ranks r and r+e in lexsort order, R ordered
+    //      by counting.  Taken on band / candidate overflow and zero spans. ----
+    double* xs = sv.xscr + ((size_t)u * G + g) * ix.m_cap;
+    if (q64) xs_score_rows(C64, q64, m, d, p.blas_threads, xs);
+    else xs_score_rows(C64, q, m, d, p.blas_threads, xs);
+    for (int w = t; w < W; w += T) { rbits[w] = 0u; tre[w] = 0u; }
+    if (t == 0) sm.ncand = 0;
+    __syncthreads();
+    auto key = [&](int c) { return xs_key(__ldcg(xs + c)); };
+    auto idf = [&](int c) { return (unsigned)c; };
+    unsigned long long k1, k2 = 0ull;
+    unsigned i1, i2 = 0u;
+    int* hist = reinterpret_cast<int*>(&sm.y);  // 258 ints of the dead candidate list
+    static_assert(sizeof(sm.y) >= 258 * sizeof(int), "radix histogram must fit");
+    xs_select(m, r, key, idf, hist, k1, i1);
+    if (e > 0) xs_select(m, r + e, key, idf, hist, k2, i2);
+    for (int c = t; c < m; c += T) {
+      const unsigned long long kk = key(c);
+      if (xs_in(kk, (unsigned)c, k1, i1)) {
+        const int pos = atomicAdd(&sm.ncand, 1);
+        sm.x.f.fin[pos] = (unsigned long long)(unsigned)c;
+        sm.x.f.fex[pos] = __ldcg(xs + c);
+      } else if (e > 0 && xs_in(kk, (unsigned)c, k2, i2)) {
+        atomicOr(tre + zb_word(c), 1u << zb_bit(c));
       }
-      __syncthreads();
-      // E = top(r+e) minus R
-      int32_t* el_out = sv.elist ? sv.elist + ((size_t)u * G + g) * sv.e_cap : nullptr;
-      int ecnt = 0;
+    }
+    __syncthreads();
+    // R in (exact desc, id asc) order: rank by counting into cs / cex
+    for (int i = t; i < r; i += T) {
+      const double ei = sm.x.f.fex[i];
+      const int ii = s6_id(sm.x.f.fin[i]);
+      int rk = 0;
+      for (int j = 0; j < r; j++) rk += s6_better(sm.x.f.fex[j], s6_id(sm.x.f.fin[j]), ei, ii) ? 1 : 0;
+      sm.cs[rk] = sm.x.f.fin[i];
+    }
+    __syncthreads();
+    for (int i = t; i < r; i += T) sm.x.f.fin[i] = sm.cs[i];
+    __syncthreads();
+    if (t == 0 && sv.xcount) atomicAdd(sv.xcount, 1);
+    ok = true;
+  }
+  if (ok) {
+    // ---- outputs: ordered retrieval list, R bitmap ----
+    int32_t* rl_out = sv.rlist + ((size_t)u * G + g) * sv.r_cap;
+    for (int i = t; i < r; i += T) {
+      const int c = s6_id(sm.x.f.fin[i]);
+      rl_out[i] = c;
+      atomicOr(rbits + zb_word(c), 1u << zb_bit(c));
+    }
+    __syncthreads();
+    // E = top(r+e) minus R
+    int32_t* el_out = sv.elist ? sv.elist + ((size_t)u * G + g) * sv.e_cap : nullptr;
+    int ecnt = 0;
+    for (int w = t; w < W; w += T) {
+      const uint32_t ew = tre[w] & ~rbits[w];
+      rb_out[w] = rbits[w];
+      eb_out[w] = ew;
+      tre[w] = ew;
+      ecnt += __popc(ew);
+    }
+    if (el_out) {
+      int v4[4] = {ecnt, 0, 0, 0}, tot[4];
+      s6_scan4(v4, tot, sm);
+      int pos = v4[0];
       for (int w = t; w < W; w += T) {
-        const uint32_t ew = tre[w] & ~rbits[w];
-        rb_out[w] = rbits[w];
-        eb_out[w] = ew;
-        tre[w] = ew;
-        ecnt += __popc(ew);
-      }
-      if (el_out) {
-        int v4[4] = {ecnt, 0, 0, 0}, tot[4];
-        s6_scan4(v4, tot, sm);
-        int pos = v4[0];
-        for (int w = t; w < W; w += T) {
-          uint32_t ew = tre[w];
-          while (ew) {
-            el_out[pos++] = zb_cluster(w, __ffs(ew) - 1);
-            ew &= ew - 1;
-          }
+        uint32_t ew = tre[w];
+        while (ew) {
+          el_out[pos++] = zb_cluster(w, __ffs(ew) - 1);
+          ew &= ew - 1;
         }
       }
-      if (p.need_tail || p.need_allc) {
-        __syncthreads();
-        const float isd = p.inv_sqrt_d;
-        const int* csize = ix.cl_size + (size_t)u * ix.m_cap;
-        float mx_t = -INFINITY, mx_a = -INFINITY;
-        for (int c = t; c < m; c += T) {
-          const float xv = S_(c) * isd;
-          mx_a = fmaxf(mx_a, xv);
-          const bool z = ((rbits[zb_word(c)] | tre[zb_word(c)]) >> zb_bit(c)) & 1u;
-          if (!z) mx_t = fmaxf(mx_t, xv);
-        }
-        float dummy = 0.f;
-        s6_reduce3(dummy, mx_t, mx_a, sm);
-        float dt = 0.f, da = 0.f, dz = -INFINITY;
-        for (int c = t; c < m; c += T) {
-          const float xv = S_(c) * isd;
-          const float sz = (float)csize[c];
-          da += sz * expf(xv - mx_a);
-          const bool z = ((rbits[zb_word(c)] | tre[zb_word(c)]) >> zb_bit(c)) & 1u;
-          if (!z) dt += sz * expf(xv - mx_t);
-        }
-        float dz2 = -INFINITY;
-        s6_reduce3(dt, dz, dz2, sm);
-        s6_reduce3(da, dz, dz2, sm);
-        if (t == 0) { tailp[0] = mx_t; tailp[1] = dt; tailp[2] = mx_a; tailp[3] = da; }
+    }
+    if (p.need_tail || p.need_allc) {
+      __syncthreads();
+      const float isd = p.inv_sqrt_d;
+      const int* csize = ix.cl_size + (size_t)u * ix.m_cap;
+      float mx_t = -INFINITY, mx_a = -INFINITY;
+      for (int c = t; c < m; c += T) {
+        const float xv = S_(c) * isd;
+        mx_a = fmaxf(mx_a, xv);
+        const bool z = ((rbits[zb_word(c)] | tre[zb_word(c)]) >> zb_bit(c)) & 1u;
+        if (!z) mx_t = fmaxf(mx_t, xv);
       }
+      float dummy = 0.f;
+      s6_reduce3(dummy, mx_t, mx_a, sm);
+      float dt = 0.f, da = 0.f, dz = -INFINITY;
+      for (int c = t; c < m; c += T) {
+        const float xv = S_(c) * isd;
+        const float sz = (float)csize[c];
+        da += sz * expf(xv - mx_a);
+        const bool z = ((rbits[zb_word(c)] | tre[zb_word(c)]) >> zb_bit(c)) & 1u;
+        if (!z) dt += sz * expf(xv - mx_t);
+      }
+      float dz2 = -INFINITY;
+      s6_reduce3(dt, dz, dz2, sm);
+      s6_reduce3(da, dz, dz2, sm);
+      if (t == 0) { tailp[0] = mx_t; tailp[1] = dt; tailp[2] = mx_a; tailp[3] = da; }
     }
   }
   if (m > 0 && !ok) {
@@ -802,14 +814,10 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
     for (int w = t; w < W; w += T) { rb_out[w] = 0u; eb_out[w] = 0u; rbits[w] = 0u; tre[w] = 0u; }
   }
   if (!ok && t == 0) { tailp[0] = -INFINITY; tailp[1] = 0.f; tailp[2] = -INFINITY; tailp[3] = 0.f; }
-  S6_MARK(9);
   pdl_trigger<2>();
   // ---- the unit's G CTAs (one cluster) build the union together ----
   cooperative_groups::this_cluster().sync();  // every head's R / E bitmaps final in its smem
-  S6_MARK(10);
   s6_union_cl<CAND, SMS, GM>(ix, sv, p, u, g, m, sm, rbits, tre, scs);
-  S6_MARK(11);
-  if (p.prof && t == 0) { g_sel_dbg[blockIdx.x][12] = sm.ncand; }
 }
 
 size_t select_v6_dyn_smem(int m_max, bool sms, int cand) {
@@ -827,7 +835,3 @@ template __global__ void select_v6_kernel<512, false, 8>(IndexView, StepView, Se
 template __global__ void select_v6_kernel<2048, false, 8>(IndexView, StepView, SelParams);
 
 }  // namespace wk
-
-extern "C" int wk_debug_select_timing(long long* out, int n) {
-  return cudaMemcpyFromSymbol(out, wk::g_sel_dbg, sizeof(long long) * 16 * (size_t)n) == cudaSuccess ? 0 : -2;
-}

@@ -195,6 +195,8 @@ class HeadEngine:
         self._recall_f = torch.empty((1, lay.s_cap), dtype=torch.uint8, device=self.device)
         self._recall = torch.zeros(1, dtype=torch.float32, device=self.device)
         self._oracle_out = torch.zeros((1, 1, d), dtype=torch.float32, device=self.device)
+        # ranking uses the caller's fp64 query (index.py:74): exact re-scoring reads it
+        lay.q64 = torch.zeros((1, 1, d), dtype=torch.float64, device=self.device)
         del n_all
         return self
 
@@ -210,6 +212,7 @@ class HeadEngine:
         if s.n_steady + 1 > lay.t_cap or self.step >= self.max_decode:
             raise ConfigError("decode capacity exceeded (raise max_decode)")
         qt = torch.from_numpy(q.astype(np.float32)).to(dev).view(1, 1, d)
+        lay.q64.copy_(torch.from_numpy(q).view(1, 1, d))
         kt = torch.from_numpy(np.asarray(new_k, np.float32).reshape(1, d)).to(dev)
         vt = torch.from_numpy(np.asarray(new_v, np.float32).reshape(1, d)).to(dev)
         c0 = self._cache.counters[0].clone()

@@ -198,6 +198,10 @@ class WaveLayer:
         self.logden = torch.zeros((U, G), dtype=f32, device=dev)
         self.cov = torch.zeros((U, G), dtype=f32, device=dev)
         self.status = torch.zeros(1, dtype=i32, device=dev)
+        # tie-safe exact selection: fp64 exact-score scratch + fallback counter
+        self.xscr = torch.zeros((U, G, self.m_cap), dtype=torch.float64, device=dev)
+        self.xcount = torch.zeros(1, dtype=i32, device=dev)
+        self.q64 = None  # optional [U, G, d] fp64 queries for the exact re-scoring
         self.n_store_dev = torch.zeros(U, dtype=i32, device=dev)
         self.units = [UnitState() for _ in range(U)]
         self._q = None
@@ -254,7 +258,8 @@ class WaveLayer:
             _ptr(self.status), self.r_cap, self.e_cap, self.ru_cap, self.eu_cap,
             None, None, _ptr(sl(self.sel_done)), 0, 0,
             _ptr(sl(self.eu_x)), _ptr(sl(self.eu_sz)), _ptr(sl(self.rbits)), _ptr(sl(self.ebits)), _ptr(sl(self.pieces)),
-            _ptr(grp["woff"]), self.w_cap, self.pc_cap, None, None, None, None, 0, 0, 0, 2)
+            _ptr(grp["woff"]), self.w_cap, self.pc_cap, None, None, None, None, 0, 0, 0, 2,
+            None, _ptr(sl(self.xscr)), _ptr(self.xcount))
 
     def _launch_split(self, q, k_new, v_new, m_max):
         """Two-stream pipeline over unit groups: scan(g) -> plan(g) -> attention(g),
@@ -306,7 +311,8 @@ class WaveLayer:
             _ptr(self.cache.arena_k) if self.cache else None, _ptr(self.cache.arena_v) if self.cache else None,
             _ptr(self.cache.slot_ids) if self.cache else None, _ptr(self.cache.slot_off) if self.cache else None,
             self.cache.phys * self.cache.bt if self.cache else 0, self.cache.list_cap if self.cache else 0,
-            self.cache.bt if self.cache else 0, 4 if self.offload else 2)
+            self.cache.bt if self.cache else 0, 4 if self.offload else 2,
+            _ptr(self.q64), _ptr(self.xscr), _ptr(self.xcount))
 
     # --------------------------------------------------------------- clustering
     def _run_segments(self, segs: list[dict]):
@@ -456,7 +462,7 @@ class WaveLayer:
                                         self.S, self.store_bf16, stream), "wk_decode_step")
             return
         _lib.check(L.wk_append_tokens(ctypes.byref(self._stv), _ptr(k_new), _ptr(v_new), self.U,
-                                      self.d, self.store_bf16, stream), "wk_append_tokens")
+                                      self.d, self.store_bf16, _ptr(self.status), stream), "wk_append_tokens")
         _lib.check(L.wk_score_topk(ctypes.byref(self._ixv), ctypes.byref(sv), ctypes.byref(self._zp),
                                    self.U, m_max, stream), "wk_score_topk")
         if self.cache is not None:  # wave buffer: lookup, replacement, miss plan
@@ -529,6 +535,54 @@ class WaveLayer:
                                  self.store_bf16, ctypes.c_void_p(_stream()))
         _lib.check(rc, "wk_full_attn")
         return self.out if out is None else out
+
+    # ------------------------------------------------------- index injection
+    def set_index(self, u: int, C64, sizes):
+        """Install a given meta index (fp64 centroids [m, d], sizes [m]) as
+        unit u's clusters -- the state ``ClusterIndex`` holds after a build
+        (index.py:110-139).  Store rows are laid out cluster-contiguously in
+        id order and left empty; used to run the zone planner on externally
+        supplied indexes (rank goldens, function-level API)."""
+        C64 = torch.as_tensor(np.asarray(C64, dtype=np.float64), device=self.dev)
+        sizes = torch.as_tensor(np.asarray(sizes, dtype=np.int64), device=self.dev).to(torch.int32)
+        m = C64.shape[0]
+        if C64.dim() != 2 or C64.shape[1] != self.d or sizes.shape != (m,) or m > self.m_cap:
+            raise ConfigError(f"bad index shapes {tuple(C64.shape)} / {tuple(sizes.shape)} (m_cap {self.m_cap})")
+        off = torch.cumsum(sizes, 0, dtype=torch.int32) - sizes
+        if m and int(off[-1] + sizes[-1]) > self.s_cap:
+            raise ConfigError("index sizes exceed the store capacity")
+        self.C64[u].zero_()
+        self.C64[u, :m] = C64
+        self.C32[u, :m] = C64.float()
+        self.Cnorm[u, :m] = self.C32[u, :m].double().norm(dim=1).float()
+        self.Cmax[u] = float(self.Cnorm[u, :m].max()) * (1 + 1e-6) if m else 0.0
+        self.cl_size[u].zero_()
+        self.cl_size[u, :m] = sizes
+        self.cl_off[u, :m] = off
+        st = self.units[u]
+        st.m = m
+        st.store_fill = int(sizes.sum())
+        self.m_dev[u] = m
+        self.n_store_dev[u] = st.store_fill
+        self.prefilled = True
+
+    def plan(self, q: torch.Tensor, q64: torch.Tensor | None = None):
+        """Zone planning only (ClusterIndex.rank + plan_zones, index.py:61-93)
+        for every unit: the centroid scan and exact selection of one decode
+        step without the append or the attention.  Returns (rlist [U,G,r_cap],
+        nr [U], elist [U,G,e_cap] or None, ne [U]) device views."""
+        q = q.float().contiguous()
+        self._q = q
+        prev, q64 = self.q64, (None if q64 is None else q64.double().contiguous())
+        if q64 is not None:
+            self.q64 = q64
+        sv = self._step_view(q)
+        self.q64 = prev
+        m_max = max(s.m for s in self.units)
+        _lib.check(self.L.wk_score_topk(ctypes.byref(self._ixv), ctypes.byref(sv), ctypes.byref(self._zp),
+                                        self.U, m_max, ctypes.c_void_p(_stream())), "wk_score_topk")
+        self.check_status("plan")
+        return self.rlist, self.nr, self.elist, self.ne
 
     # ---------------------------------------------------------------- checking
     def check_status(self, what="step"):
