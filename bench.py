@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-flashinfer", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the reduced configs[2]/[3]/[4] legs of the default run")
     ap.add_argument("--split", type=int, default=1, help="unit groups pipelined on streams")
     ap.add_argument("--build", action="store_true",
                     help="configs[2]: segmented clustering index build at 120K and 256K, "
@@ -304,22 +306,25 @@ def run_build(a, torch, dev, log):
         log(f"build ctx={ctx}: {dt:.2f}s, parity={ok}")
         del keys, vals, lay
         torch.cuda.empty_cache()
-    print(json.dumps({"metric": "prefill index build throughput (segmented spherical k-means), tokens/s",
-                      "impl": "wave-build", "unit": "tokens/s", "value": rows[0]["tokens_per_s"],
-                      "higher_is_better": True, "data": "synthetic",
-                      "config": {"workload": f"{a.model}-shape build, {a.batch} requests x {HKV} kv heads "
-                                             "(configs[2])", "kmeans_iters": ic.kmeans_iters},
-                      "runs": rows}), flush=True)
+    return {"metric": "prefill index build throughput (segmented spherical k-means), tokens/s",
+            "impl": "wave-build", "unit": "tokens/s", "value": rows[0]["tokens_per_s"],
+            "higher_is_better": True, "data": "synthetic",
+            "config": {"workload": f"{a.model}-shape build, {a.batch} requests x {HKV} kv heads "
+                                   "(configs[2])", "kmeans_iters": ic.kmeans_iters},
+            "runs": rows}
 
 
 # ----------------------------------------------------------- offload (config 4)
-def run_offload(a, torch, dev, log):
+def run_offload(a, torch, dev, log, ctx=None, batch=None, layer_bufs=None, steps=None, warmup=None):
     """configs[3]: long context with the cluster store in pinned host memory
     and the wave buffer (HBM slot arena, cache_fraction of the blocks) on the
     device.  Reports the cumulative hit ratio (per cluster), miss
     bytes, and stall time = offload step time - the same step with the store
     resident in HBM (same data, same zones)."""
     from paper_2505_02922_b200 import EngineConfig, WaveLayer
+    import types
+    a = types.SimpleNamespace(**{**vars(a), **{k: v for k, v in dict(
+        ctx=ctx, batch=batch, layer_bufs=layer_bufs, steps=steps, warmup=warmup).items() if v is not None}})
     G = HQ // HKV
     U = a.batch * HKV
     n_bufs = min(a.layer_bufs, a.layers)
@@ -395,7 +400,8 @@ def run_offload(a, torch, dev, log):
             "host_link_gbs": per_step_miss_blocks * bt * 2 * D * 2 / ((ms_o - ms_h) / 1e3) / 1e9
             if ms_o > ms_h else None,
             "build_s": t_build, "clocks": clk.summary()}
-    print(json.dumps(line), flush=True)
+    del lay_o, lay_h, qpool, kpool
+    return line
 
 
 # ------------------------------------------------------------------- GPU arm
@@ -403,41 +409,79 @@ def _ptr(t):
     return t.data_ptr()
 
 
-def main():
-    global HQ, HKV, D
-    a = parse()
-    HQ, HKV, D, n_layers = MODELS[a.model]
-    if a.layers <= 0:
-        a.layers = n_layers
-    if a.impl == "reference":
-        return run_reference(a)
-    import torch
-    import torch.distributed as dist
-    from paper_2505_02922_b200 import EngineConfig, WaveLayer
+def parity_sample(lay, keys0, vals0, history, G, log):
+    """Sampled oracle check of the benchmarked layer (outside the timed
+    region): unit 0 of layer buffer 0 -- its 120K index (C64, sizes, members)
+    bit-exact against the C oracle's prefill of the same keys, then the oracle
+    replays every decode step that buffer saw (G heads) and the last step's
+    ordered retrieval list, output and log-denominator must match
+    (SURVEY 8c bars: ids bit-exact, rel-L2 <= 1e-5, |dlogden| <= 1e-5)."""
+    import numpy as np
+    from oracle import oracle as O
+    t0 = time.perf_counter()
+    e0 = O.OracleEngine(blas_threads=lay.blas_threads).prefill(keys0, vals0)
+    ix = lay.index_arrays(0)
+    m = e0.m
+    index_ok = bool(lay.units[0].m == m and np.array_equal(ix["C64"], e0.centroids)
+                    and np.array_equal(ix["sizes"], e0.sizes))
+    for c in range(0, m, max(1, m // 64)):  # members of every 64th cluster (+ last)
+        o, s = int(ix["offsets"][c]), int(ix["sizes"][c])
+        index_ok &= bool(np.array_equal(ix["store_tok"][o:o + s], e0.members(c)))
+    o, s = int(ix["offsets"][m - 1]), int(ix["sizes"][m - 1])
+    index_ok &= bool(np.array_equal(ix["store_tok"][o:o + s], e0.members(m - 1)))
+    orcs = [e0] + [e0.clone() for _ in range(G - 1)]
+    outs = []
+    for (q, k, v) in history:
+        outs = [orcs[g].decode_step(q[g], k, v, with_recall=False) for g in range(G)]
+    r = int(lay.nr[0])
+    rl = lay.rlist[0, :, :r].cpu().numpy()
+    out = lay.out[0].double().cpu().numpy()
+    logden = lay.logden[0].cpu().numpy()
+    ids_ok, worst, dlog = True, 0.0, 0.0
+    for g in range(G):
+        o_ref, sm = outs[g]
+        r_ref, _ = orcs[g].last_plan()
+        ids_ok &= bool(r == sm.r and np.array_equal(rl[g], r_ref))
+        worst = max(worst, float(np.linalg.norm(out[g] - o_ref) / np.linalg.norm(o_ref)))
+        dlog = max(dlog, abs(float(logden[g]) - sm.log_denominator))
+    res = {"what": "unit 0 of layer buffer 0 (the benchmarked layer) vs the C oracle (tierkv's algorithm): "
+                   "index after prefill, then the last of the decode steps it replayed",
+           "m": m, "decode_steps_replayed": len(history), "heads": G,
+           "index_bit_exact": index_ok, "retrieval_ids_bit_exact": ids_ok,
+           "max_rel_l2": worst, "max_abs_dlogden": dlog,
+           "pass": bool(index_ok and ids_ok and worst <= 1e-5 and dlog <= 1e-5),
+           "seconds": time.perf_counter() - t0}
+    log(f"parity sample: {res}")
+    return res
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    log = lambda *x: print(*x, file=sys.stderr, flush=True) if rank == 0 else None
-    if a.offload:
-        return run_offload(a, torch, dev, log)
-    if a.build:
-        return run_build(a, torch, dev, log)
-    G = HQ // HKV
-    U = a.batch * HKV  # per-rank units (weak scaling: each rank serves `batch` requests)
-    n_bufs = min(a.layer_bufs, a.layers)
-    total_steps = a.warmup + a.steps + 2  # + the per-op breakdown step
-    log = lambda *x: print(*x, file=sys.stderr, flush=True) if rank == 0 else None
+
+def run_decode(a, torch, dev, model, log, rank=0, world=1, batch=None, ctx=None, steps=None,
+               warmup=None, layer_bufs=None, headline=True):
+    """Decode throughput of one BASELINE config (configs[1] llama3-8b or
+    configs[4] qwen2.5-7b): returns the JSON dict."""
+    import ctypes
+    from paper_2505_02922_b200 import EngineConfig, WaveLayer, _lib
+    from paper_2505_02922_b200.wave import _stream
+    hq, hkv, d, n_layers = MODELS[model]
+    layers_n = a.layers if (headline and a.layers > 0) else n_layers
+    batch = batch or a.batch
+    ctx = ctx or a.ctx
+    steps = steps if steps is not None else a.steps
+    warmup = warmup if warmup is not None else a.warmup
+    G = hq // hkv
+    U = batch * hkv  # per-rank units (weak scaling: each rank serves `batch` requests)
+    n_bufs = min(layer_bufs or a.layer_bufs, layers_n)
+    per_buf = math.ceil(layers_n / n_bufs)
+    total_steps = warmup + steps + 2  # + the per-op breakdown step
     cfg = EngineConfig()
     layers, qpool, kpool = [], [], []
+    keys0 = vals0 = None
     t_build = 0.0
     for li in range(n_bufs):
-        keys, vals, cen = gen_layer(torch, U, a.ctx, D, 1000 * rank + li, dev)
-        lay = WaveLayer(cfg, U, G, D, max_prefill=a.ctx, max_decode=64, store_dtype=torch.bfloat16,
+        keys, vals, cen = gen_layer(torch, U, ctx, d, 1000 * rank + li, dev)
+        if li == 0 and headline and rank == 0:
+            keys0, vals0 = keys[0].cpu().numpy(), vals[0].cpu().numpy()
+        lay = WaveLayer(cfg, U, G, d, max_prefill=ctx, max_decode=64, store_dtype=torch.bfloat16,
                         split=a.split)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -445,65 +489,56 @@ def main():
         torch.cuda.synchronize()
         t_build += time.perf_counter() - t0
         layers.append(lay)
-        per_buf = math.ceil(a.layers / n_bufs)
         qpool.append(gen_queries(torch, cen, G, total_steps * per_buf, 7 + li))
-        kpool.append(torch.randn((total_steps * per_buf, 2, U, D), device=dev).bfloat16().float())
+        kpool.append(torch.randn((total_steps * per_buf, 2, U, d), device=dev).bfloat16().float())
         del keys, vals, cen
         torch.cuda.empty_cache()
-        log(f"layer buffer {li}: m={lay.units[0].m} build {t_build:.1f}s")
+        log(f"[{model}] layer buffer {li}: m={lay.units[0].m} build {t_build:.1f}s")
     use = [0] * n_bufs
+    gather_buf = torch.empty((world, U, G, d), device=dev) if world > 1 else None
 
-    gather_buf = torch.empty((world, U, G, D), device=dev) if world > 1 else None
-
-    def wave_step(step_i, timers=None):
-        for l in range(a.layers):
+    def wave_step():
+        for l in range(layers_n):
             b = l % n_bufs
             lay = layers[b]
             j = use[b]
             use[b] += 1
-            if timers is not None:
-                timers[l][0].record()
             lay.launch_step(qpool[b][j], kpool[b][j, 0], kpool[b][j, 1])
-            if timers is not None:
-                timers[l][1].record()
             for s in lay.units:
                 s.total += 1
                 s.n_steady += 1
         if world > 1:
             # the path's one collective: final gather of the attention outputs
             # (SURVEY 8(e)); NCCL over NVLink, ordered on the current stream
-            dist.all_gather_into_tensor(gather_buf, layers[(a.layers - 1) % n_bufs].out)
+            dist.all_gather_into_tensor(gather_buf, layers[(layers_n - 1) % n_bufs].out)
 
-    # ---- warmup + timed wave steps ----
-    for i in range(a.warmup):
-        wave_step(i)
+    import torch.distributed as dist
+    for _ in range(warmup):
+        wave_step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(torch.cuda.current_device()) as clk:
         torch.cuda.synchronize()
         ev0.record()
-        for i in range(a.steps):
-            wave_step(i)
+        for _ in range(steps):
+            wave_step()
         ev1.record()
         torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1) / a.steps
+    ms = ev0.elapsed_time(ev1) / steps
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t)
     for lay in layers:
         lay.check_status("bench")
-    value = a.batch * world / (ms / 1e3)
+    value = batch * world / (ms / 1e3)
 
     # ---- per-op device time inside one more step (events on the launch stream) ----
-    import ctypes
-    from paper_2505_02922_b200 import _lib
-    from paper_2505_02922_b200.wave import _stream
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(a.layers)]
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(layers_n)]
     torch.cuda.synchronize()
-    for l in range(a.layers):
+    for l in range(layers_n):
         b_ = l % n_bufs
         lay = layers[b_]
         j = use[b_]
@@ -525,9 +560,24 @@ def main():
             s_.total += 1
             s_.n_steady += 1
     torch.cuda.synchronize()
-    t_app = sum(ev[l][0].elapsed_time(ev[l][1]) for l in range(a.layers)) / a.layers
-    t_score = sum(ev[l][1].elapsed_time(ev[l][2]) for l in range(a.layers)) / a.layers
-    t_attn = sum(ev[l][2].elapsed_time(ev[l][3]) for l in range(a.layers)) / a.layers
+    for lay in layers:
+        lay.check_status("bench breakdown")
+    t_app = sum(ev[l][0].elapsed_time(ev[l][1]) for l in range(layers_n)) / layers_n
+    t_score = sum(ev[l][1].elapsed_time(ev[l][2]) for l in range(layers_n)) / layers_n
+    t_attn = sum(ev[l][2].elapsed_time(ev[l][3]) for l in range(layers_n)) / layers_n
+
+    # ---- sampled oracle parity of the benchmarked layer (outside the timed region) ----
+    par = None
+    if keys0 is not None and not a.no_cpu:
+        hist = []
+        lay0 = layers[0]
+        for j in range(use[0]):
+            hist.append((qpool[0][j][0].double().cpu().numpy(), kpool[0][j, 0][0].cpu().numpy(),
+                         kpool[0][j, 1][0].cpu().numpy()))
+        try:
+            par = parity_sample(lay0, keys0, vals0, hist, G, log)
+        except Exception as exc:  # reported, never silently passed
+            par = {"pass": False, "error": repr(exc)}
 
     # ---- algorithmic bytes: per layer, from the live zone counts ----
     elem = 2
@@ -538,8 +588,8 @@ def main():
         cnt = lay.cnt.cpu().double()
         n_st = lay.st_n.cpu().double()
         mm = torch.tensor([s_.m for s_ in lay.units], dtype=torch.float64)
-        attn_bytes_l.append(float((cnt[:, 1] + n_st).sum() * 2 * D * elem + cnt[:, 2].sum() * (D * 4 + 4)))
-        score_bytes_l.append(float(mm.sum() * D * 4))
+        attn_bytes_l.append(float((cnt[:, 1] + n_st).sum() * 2 * d * elem + cnt[:, 2].sum() * (d * 4 + 4)))
+        score_bytes_l.append(float(mm.sum() * d * 4))
         zs["n_steady"] += float(n_st.mean()) / n_bufs
         zs["n_retrieved_tokens"] += float(cnt[:, 1].mean()) / n_bufs
         zs["n_retrieval_pieces"] += float(cnt[:, 3].mean()) / n_bufs
@@ -547,7 +597,7 @@ def main():
         zs["m"] += float(mm.mean()) / n_bufs
     attn_bytes = sum(attn_bytes_l) / n_bufs
     score_bytes = sum(score_bytes_l) / n_bufs
-    step_bytes = (attn_bytes + score_bytes) * a.layers
+    step_bytes = (attn_bytes + score_bytes) * layers_n
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     peak = float(peaks.get("hbm_gbs", 6650.0))
@@ -555,80 +605,161 @@ def main():
     achieved = attn_bytes / (t_attn / 1e3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp) and a.model == "llama3-8b":  # captured on the configs[1] workload only
+    if os.path.exists(tp) and model == "llama3-8b":  # captured on the configs[1] workload only
         traffic = json.load(open(tp)).get("wk_tripartite_attn")
 
     # ---- full-attention comparators (same batch, heads, context, bf16 KV) ----
     fa_ms = None
-    if a.fa_steps > 0:
-        outs = torch.empty((U, G, D), device=dev)
-        for l in range(a.layers):
+    fa_steps = a.fa_steps if headline else min(a.fa_steps, 2)
+    if fa_steps > 0:
+        outs = torch.empty((U, G, d), device=dev)
+        for l in range(layers_n):
             layers[l % n_bufs].full_attention(qpool[l % n_bufs][0], out=outs)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for i in range(a.fa_steps):
-            for l in range(a.layers):
+        for i in range(fa_steps):
+            for l in range(layers_n):
                 layers[l % n_bufs].full_attention(qpool[l % n_bufs][i], out=outs)
         e1.record()
         torch.cuda.synchronize()
-        fa_ms = e0.elapsed_time(e1) / a.fa_steps
-    fa_bytes_layer = sum(s_.store_fill + s_.n_steady for s_ in layers[0].units) * 2 * D * elem
-    fi = None
-    if a.fa_steps > 0 and not a.no_flashinfer:
-        fi = flashinfer_decode(torch, a.batch, HQ, HKV, D, a.ctx, a.layers, max(3, a.fa_steps), log)
+        fa_ms = e0.elapsed_time(e1) / fa_steps
+    fa_bytes_layer = sum(s_.store_fill + s_.n_steady for s_ in layers[0].units) * 2 * d * elem
 
     # ---- e2e: host buffers, copies inside the timed region ----
     e2e = None
-    if not a.no_e2e:
-        hq = torch.empty((a.layers, U, G, D), dtype=torch.float32).pin_memory()
-        hkv = torch.empty((a.layers, 2, U, D), dtype=torch.float32).pin_memory()
-        hout = torch.empty((a.layers, U, G, D), dtype=torch.float32).pin_memory()
-        dq = torch.empty((a.layers, U, G, D), device=dev)
-        dkv = torch.empty((a.layers, 2, U, D), device=dev)
-        hq.copy_(qpool[0][: a.layers].cpu() if qpool[0].shape[0] >= a.layers else hq)
-        hkv.copy_(kpool[0][: a.layers].cpu() if kpool[0].shape[0] >= a.layers else hkv.normal_())
+    if not a.no_e2e and headline:
+        hq_ = torch.empty((layers_n, U, G, d), dtype=torch.float32).pin_memory()
+        hkv_buf = torch.empty((layers_n, 2, U, d), dtype=torch.float32).pin_memory()
+        hout = torch.empty((layers_n, U, G, d), dtype=torch.float32).pin_memory()
+        dq = torch.empty((layers_n, U, G, d), device=dev)
+        dkv = torch.empty((layers_n, 2, U, d), device=dev)
+        hq_.copy_(qpool[0][: layers_n].cpu() if qpool[0].shape[0] >= layers_n else hq_)
+        hkv_buf.copy_(kpool[0][: layers_n].cpu() if kpool[0].shape[0] >= layers_n else hkv_buf.normal_())
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        k_e2e = max(1, min(a.steps, 5))
+        k_e2e = max(1, min(steps, 5))
         # Pipelined host I/O: the q/k/v of a group of GR layers go up on an H2D stream
         # while earlier layers compute; a group's outputs come down on a D2H stream
         # once its last layer is done (overlapping the next group).  Stream waits /
         # event records only at group boundaries, so the kernels of a group stay
         # back to back (programmatic dependent launch).  The timed region ends when
         # the last output has landed.
-        GR = int(os.environ.get("WK_E2E_GROUP", "4"))
-        main = torch.cuda.current_stream()
+        GR = 4
+        main_s = torch.cuda.current_stream()
         up, down = torch.cuda.Stream(), torch.cuda.Stream()
-        ngr = -(-a.layers // GR)
+        ngr = -(-layers_n // GR)
         ev_in = [torch.cuda.Event() for _ in range(ngr)]
         ev_out = [torch.cuda.Event() for _ in range(ngr)]
-        dout = torch.empty((a.layers, U, G, D), device=dev)
+        dout = torch.empty((layers_n, U, G, d), device=dev)
         torch.cuda.synchronize()
         e0.record()
         for i in range(k_e2e):
-            up.wait_stream(main)
+            up.wait_stream(main_s)
             with torch.cuda.stream(up):
                 for gi in range(ngr):
-                    l0, l1 = gi * GR, min(a.layers, gi * GR + GR)
-                    dq[l0:l1].copy_(hq[l0:l1], non_blocking=True)
-                    dkv[l0:l1].copy_(hkv[l0:l1], non_blocking=True)
+                    l0, l1 = gi * GR, min(layers_n, gi * GR + GR)
+                    dq[l0:l1].copy_(hq_[l0:l1], non_blocking=True)
+                    dkv[l0:l1].copy_(hkv_buf[l0:l1], non_blocking=True)
                     ev_in[gi].record(up)
             for gi in range(ngr):
-                l0, l1 = gi * GR, min(a.layers, gi * GR + GR)
-                main.wait_event(ev_in[gi])
+                l0, l1 = gi * GR, min(layers_n, gi * GR + GR)
+                main_s.wait_event(ev_in[gi])
                 for l in range(l0, l1):
                     layers[l % n_bufs].launch_step(dq[l], dkv[l, 0], dkv[l, 1], out=dout[l])
-                ev_out[gi].record(main)
+                ev_out[gi].record(main_s)
                 down.wait_event(ev_out[gi])
                 with torch.cuda.stream(down):
                     hout[l0:l1].copy_(dout[l0:l1], non_blocking=True)
-            main.wait_stream(down)
+            main_s.wait_stream(down)
         e1.record()
         torch.cuda.synchronize()
         e2e_ms = e0.elapsed_time(e1) / k_e2e
-        e2e = {"value": a.batch * world / (e2e_ms / 1e3), "unit": "tokens/s",
-               "h2d_bytes_per_step": int(hq.numel() * 4 + hkv.numel() * 4),
+        e2e = {"value": batch * world / (e2e_ms / 1e3), "unit": "tokens/s",
+               "h2d_bytes_per_step": int(hq_.numel() * 4 + hkv_buf.numel() * 4),
                "d2h_bytes_per_step": int(hout.numel() * 4), "ms_per_step": e2e_ms}
+    del layers, qpool, kpool
+    torch.cuda.empty_cache()
+    fi = None
+    if fa_steps > 0 and not a.no_flashinfer:
+        fi = flashinfer_decode(torch, batch, hq, hkv, d, ctx, layers_n, max(3, fa_steps), log)
+
+    fa_block = {"impl": "wk_full_attn (this repo, same kernel family reading every token)",
+                "ms_per_step": fa_ms,
+                "value": (batch * world / (fa_ms / 1e3)) if fa_ms else None,
+                "speedup_wave_vs_full": (fa_ms / ms) if fa_ms else None,
+                "bytes_per_layer": fa_bytes_layer,
+                "hbm_gbs": (fa_bytes_layer * layers_n / (fa_ms / 1e3) / 1e9) if fa_ms else None}
+    if fi:
+        fi["speedup_wave_vs_full"] = fi["ms_per_step"] / ms
+        fi["value"] = batch * world / (fi["ms_per_step"] / 1e3)
+    read_peak = fi["hbm_gbs"] if fi else None
+    cfg_name = "configs[1]" if model == "llama3-8b" else "configs[4]"
+    return {
+        "metric": METRIC,
+        "value": value, "unit": "tokens/s", "n_gpus": world, "steps": steps,
+        "warmup": warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16 KV / fp32 accumulate (fp64 scoring)", "data": "synthetic",
+        "config": {"workload": f"{model}-shape {layers_n}-layer decode, {ctx // 1024}K ctx, batch {batch} ({cfg_name})",
+                   "model_shape": model,
+                   "batch_per_gpu": batch, "ctx": ctx, "layers": layers_n,
+                   "layer_buffers": n_bufs, "heads": f"{hq}q/{hkv}kv", "d": d,
+                   "l2": "inputs larger than L2 (each layer buffer >> 126 MB, cycled)"},
+        "full_attention": fi or fa_block,
+        "full_attention_own_kernel": fa_block,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "kernel": "wk_tripartite_attn (attend_v4 + att4_merge)",
+                     "bytes_per_launch": attn_bytes, "ms_per_launch": t_attn,
+                     "read_peak_demonstrated": read_peak,
+                     "frac_vs_read_peak": (achieved / read_peak) if read_peak else None,
+                     "read_peak_source": "flashinfer full-attention decode on the same box, same run "
+                                         "(a read-only stream; the copy peak counts read+write)"},
+        "step_roofline": {"bytes_per_step": step_bytes, "achieved": step_bytes / (ms / 1e3) / 1e9,
+                          "frac": step_bytes / (ms / 1e3) / 1e9 / peak,
+                          "frac_vs_read_peak": (step_bytes / (ms / 1e3) / 1e9 / read_peak) if read_peak else None,
+                          "what": "HBM bytes touched per decode step (C32 scan + steady/retrieved K,V "
+                                  "+ estimation value sums) / device step time"},
+        "breakdown_ms_per_layer": {"append": t_app, "score_topk": t_score, "tripartite_attn": t_attn,
+                                   "score_scan_gbs": score_bytes / (t_score / 1e3) / 1e9},
+        "zone_stats_per_unit": zs,
+        "build_s": t_build,
+        "parity_sample": par,
+        "e2e": e2e,
+        "clocks": clk.summary(),
+        "gpu_launches": steps * layers_n * LAUNCHES_PER_LAYER,
+    }
+
+
+def _compact(line, keys):
+    return {k: line.get(k) for k in keys}
+
+
+def main():
+    global HQ, HKV, D
+    a = parse()
+    HQ, HKV, D, n_layers = MODELS[a.model]
+    if a.layers <= 0:
+        a.layers = n_layers
+    if a.impl == "reference":
+        return run_reference(a)
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    log = lambda *x: print(*x, file=sys.stderr, flush=True) if rank == 0 else None
+    if a.offload:
+        print(json.dumps(run_offload(a, torch, dev, log)), flush=True)
+        return
+    if a.build:
+        print(json.dumps(run_build(a, torch, dev, log)), flush=True)
+        return
+    line = run_decode(a, torch, dev, a.model, log, rank=rank, world=world)
 
     # ---- CPU baseline (oracle port of tierkv, one host core) ----
     cpu = None
@@ -638,51 +769,47 @@ def main():
         cpu = {"value": cpu_tok, "unit": "tokens/s", "cores": 1, "kind": "port",
                "sample": f"one q-head unit at {a.ctx} ctx, {a.cpu_steps} decode steps (prefill "
                          f"untimed, no recall metric), {t_unit * 1e3:.2f} ms/unit-step, "
-                         f"extrapolated x{HQ} heads x{a.layers} layers"}
+                         f"extrapolated x{HQ} heads x{a.layers} layers",
+               "host": host_info()}
+    line["cpu_baseline"] = cpu
 
+    # ---- the other BASELINE configs, reduced, in front of the driver (1 GPU only) ----
+    if world == 1 and not a.no_extras:
+        extras = {}
+        for name, fn in (("qwen", lambda: _compact(
+                              run_decode(a, torch, dev, "qwen2.5-7b", log, steps=5, warmup=3, headline=False),
+                              ("value", "ms_per_step", "config", "full_attention", "full_attention_own_kernel",
+                               "roofline", "step_roofline", "breakdown_ms_per_layer", "zone_stats_per_unit",
+                               "clocks"))),
+                         ("build", lambda: run_build(a, torch, dev, log)),
+                         ("offload", lambda: run_offload(a, torch, dev, log, ctx=1048576, batch=4, layer_bufs=2,
+                                                         steps=3, warmup=2))):
+            try:
+                t0 = time.perf_counter()
+                extras[name] = fn()
+                extras[name]["wall_s"] = time.perf_counter() - t0
+            except Exception as exc:  # an extra leg never hides the headline
+                extras[name] = {"error": repr(exc)}
+            torch.cuda.empty_cache()
+        line["configs_other"] = extras
     if rank == 0:
-        fa_block = {"impl": "wk_full_attn (this repo, same kernel family reading every token)",
-                    "ms_per_step": fa_ms,
-                    "value": (a.batch * world / (fa_ms / 1e3)) if fa_ms else None,
-                    "speedup_wave_vs_full": (fa_ms / ms) if fa_ms else None,
-                    "bytes_per_layer": fa_bytes_layer,
-                    "hbm_gbs": (fa_bytes_layer * a.layers / (fa_ms / 1e3) / 1e9) if fa_ms else None}
-        if fi:
-            fi["speedup_wave_vs_full"] = fi["ms_per_step"] / ms
-            fi["value"] = a.batch * world / (fi["ms_per_step"] / 1e3)
-        line = {
-            "metric": METRIC,
-            "value": value, "unit": "tokens/s", "n_gpus": world, "steps": a.steps,
-            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "bf16 KV / fp32 accumulate (fp64 scoring)", "data": "synthetic",
-            "config": {"workload": (f"{a.model}-shape {a.layers}-layer decode, {a.ctx // 1024}K ctx, batch {a.batch}"
-                                    + (" (configs[1])" if a.model == "llama3-8b" else " (configs[4])")),
-                       "model_shape": a.model,
-                       "batch_per_gpu": a.batch, "ctx": a.ctx, "layers": a.layers,
-                       "layer_buffers": n_bufs, "heads": f"{HQ}q/{HKV}kv", "d": D,
-                       "l2": "inputs larger than L2 (each layer buffer >> 126 MB, cycled)"},
-            "full_attention": fi or fa_block,
-            "full_attention_own_kernel": fa_block,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "kernel": "wk_tripartite_attn (attend_v4 + att4_merge)",
-                         "bytes_per_launch": attn_bytes, "ms_per_launch": t_attn},
-            "step_roofline": {"bytes_per_step": step_bytes, "achieved": step_bytes / (ms / 1e3) / 1e9,
-                              "frac": step_bytes / (ms / 1e3) / 1e9 / peak,
-                              "what": "HBM bytes touched per decode step (C32 scan + steady/retrieved K,V "
-                                      "+ estimation value sums) / device step time"},
-            "breakdown_ms_per_layer": {"append": t_app, "score_topk": t_score, "tripartite_attn": t_attn,
-                                       "score_scan_gbs": score_bytes / (t_score / 1e3) / 1e9},
-            "zone_stats_per_unit": zs,
-            "build_s": t_build,
-            "cpu_baseline": cpu,
-            "e2e": e2e,
-            "clocks": clk.summary(),
-            "gpu_launches": a.steps * a.layers * LAUNCHES_PER_LAYER,
-        }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def host_info():
+    model = None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "os_cpu_count": os.cpu_count(),
+            "OPENBLAS_NUM_THREADS": os.environ.get("OPENBLAS_NUM_THREADS"),
+            "oracle_threads": 1}
 
 
 if __name__ == "__main__":
