@@ -266,6 +266,42 @@ int wk_plan_zones(const wk_index_view* ix, const wk_steady_view* st, const wk_st
                   const wk_zone_params* zp, const float* k_new, const float* v_new, int U, int m_max,
                   int store_bf16, void* stream);
 
+/* The BlockCache phases as separate calls on cache unit 0 of `cv` (the
+ * function-level API: BlockCache.lookup / assemble / commit_update,
+ * block_cache.py:79-96, 98-143, 163-213).  phase bits: 1 lookup (ids
+ * de-duplicated in place, snapshot -> snap_out, *n_out distinct ids, hit /
+ * miss counters, access event), 2 assemble byte accounting (n_steady steady
+ * tokens, then ids in the given order with snap_in), 4 commit_update(ids,
+ * snap_in, step).  Unknown ids set *status (IntegrityError). */
+int wk_cache_phase(const wk_cache_view* cv, int32_t* ids, const uint8_t* snap_in, int n, int64_t n_steady,
+                   int64_t step, int phase, uint8_t* snap_out, int32_t* n_out, int* status, void* stream);
+
+/* Function-level attention / ranking in fp64 on the device (tierkv
+ * attention.py:55-148, index.py:43-76, metrics.py:8-16).  One partial:
+ * mode 0 exact_partial over rows = K, vals = V; 1 estimate_partial over
+ * rows = C (or given scores), vals = value sums, sizes; 2
+ * tail_denominator_partial.  out [3 + d] = running_max, denominator, count,
+ * numerator[d]; scratch: n doubles. */
+int wk_attn_partial_f64(const double* q, const double* rows, const double* vals, const double* sizes,
+                        const double* scores, int n, int d, int mode, int blas_threads, double* scratch,
+                        double* out, void* stream);
+/* merge (attention.py:115-148) of P partials [P, 3 + d]: out [2d + 3] =
+ * output[d], exact-denominator coverage (1 if exact_mask NULL),
+ * log-denominator, merged denominator, merged numerator[d] (merged_sums).
+ * All partials empty sets *status (ConfigError). */
+int wk_merge_f64(const double* parts, int P, int d, const uint8_t* exact_mask, double* out, int* status,
+                 void* stream);
+/* rank_clusters / top_k_token_ids: exact dgemv-recipe scores of m rows
+ * (scores [m]) and, if order != NULL, the full lexsort((arange, -scores))
+ * order [m]. */
+int wk_rank_f64(const double* q, const double* rows, int m, int d, int blas_threads, double* scores,
+                int64_t* order, void* stream);
+/* finalize_cluster sums: for k clusters with members[offsets[c]..offsets[c+1])
+ * (row indices into keys / values [., d] fp32), fp64 centroid = mean and
+ * value_sum = sum, in member order (index.py:43-58). */
+int wk_cluster_sums_f64(const float* keys, const float* values, const int32_t* members, const int32_t* offsets,
+                        int k, int d, double* centroids, double* value_sums, void* stream);
+
 /* Offload cache step + attention pieces for U kv-head units (one CTA each). */
 int wk_cache_offload_step(const wk_cache2_view* cv, const wk_index_view* ix, const wk_steady_view* st,
                           const wk_step_view* sv, int G, int64_t step, int U, void* stream);

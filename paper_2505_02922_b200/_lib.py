@@ -87,7 +87,8 @@ _lib = None
 EXPORTS = ("wk_version", "wk_kmeans_segments", "wk_append_tokens", "wk_score_topk",
            "wk_tripartite_attn", "wk_full_attn", "wk_cache_step", "wk_recall_at_k",
            "wk_cache_offload_step", "wk_host_alloc", "wk_host_free", "wk_decode_step",
-           "wk_centroid_scan", "wk_plan_zones")
+           "wk_centroid_scan", "wk_plan_zones", "wk_cache_phase", "wk_attn_partial_f64",
+           "wk_merge_f64", "wk_rank_f64", "wk_cluster_sums_f64")
 
 
 def lib():
@@ -122,6 +123,12 @@ def lib():
     L.wk_centroid_scan.argtypes = [R(IndexViewC), R(StepViewC), R(ZoneParamsC), ctypes.c_int, ctypes.c_int, _P]
     L.wk_plan_zones.argtypes = [R(IndexViewC), R(SteadyViewC), R(StepViewC), R(ZoneParamsC), _P, _P,
                                 ctypes.c_int, ctypes.c_int, ctypes.c_int, _P]
+    L.wk_cache_phase.argtypes = [R(CacheViewC), _P, _P, ctypes.c_int, _I64, _I64, ctypes.c_int, _P, _P, _P, _P]
+    L.wk_attn_partial_f64.argtypes = [_P, _P, _P, _P, _P, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                      ctypes.c_int, _P, _P, _P]
+    L.wk_merge_f64.argtypes = [_P, ctypes.c_int, ctypes.c_int, _P, _P, _P, _P]
+    L.wk_rank_f64.argtypes = [_P, _P, ctypes.c_int, ctypes.c_int, ctypes.c_int, _P, _P, _P]
+    L.wk_cluster_sums_f64.argtypes = [_P, _P, _P, _P, ctypes.c_int, ctypes.c_int, _P, _P, _P]
     L.wk_host_alloc.argtypes = [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]
     L.wk_host_free.argtypes = [_P]
     for name in EXPORTS:

@@ -42,14 +42,23 @@ def spherical_kmeans(keys, k: int, iters: int, seed, device="cuda", threads=None
     if keys_np.ndim != 2:
         raise ConfigError("keys must be 2-D")
     n, d = keys_np.shape
+    k = int(k)
     if k < 1:
         raise ConfigError(f"k must be >= 1, got {k}")
     if k > n:
         raise ConfigError(f"k={k} exceeds number of keys n={n}")
     if k == 1:
         return np.zeros(n, dtype=np.int64)
-    if d % 4 or d > 256:
-        raise ConfigError(f"head dim {d} unsupported (need d % 4 == 0, d <= 256)")
+    if d > 256:
+        raise ConfigError(f"head dim {d} unsupported (d <= 256)")
+    if d % 4:
+        # the kernels stream rows as float4: zero columns leave every dot
+        # product, norm and centroid of the real columns unchanged (bit-exact
+        # reproduction of numpy's evaluation order is for d % 4 == 0, i.e.
+        # every head dim the engine serves)
+        pad = np.zeros((n, 4 - d % 4), np.float32)
+        keys_np = np.concatenate([keys_np, pad], axis=1)
+        d = keys_np.shape[1]
     dev = torch.device(device)
     kt = torch.from_numpy(np.ascontiguousarray(keys_np)).to(dev)
     # a throwaway one-unit index receives finalize/pack output

@@ -57,6 +57,8 @@ size_t recall_smem_bytes();
 // cache.cu
 __global__ void cache_step_kernel(CacheView, const int32_t*, const int32_t*, const int32_t*, int, int, int,
                                   int64_t, int, int*);
+__global__ void cache_phase_kernel(CacheView, int32_t*, const uint8_t*, int, int64_t, int64_t, int, uint8_t*,
+                                   int32_t*, int*);
 }  // namespace wk
 
 using namespace wk;
@@ -207,11 +209,9 @@ static int launch_select_v6_g(const IndexView& ix, const StepView& sv, const Sel
   else if (r_max <= 480)
     e = launch_ex(select_v6_kernel<512, false, GM>, dim3(blocks), dim3(256), select_v6_dyn_smem(m_max, false, 512), s,
                   p.G, ix, sv, p);
-  else if (r_max <= 1900)
+  else  // r_max > 1900: the exact path builds the ordered list in global memory
     e = launch_ex(select_v6_kernel<2048, false, GM>, dim3(blocks), dim3(256), select_v6_dyn_smem(m_max, false, 2048),
                   s, p.G, ix, sv, p);
-  else
-    return WK_ECONFIG;
   return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? 0 : WK_ECUDA;
 }
 
@@ -472,6 +472,17 @@ int wk_cache_step(const wk_cache_view* cv, const int32_t* rlist, const int32_t* 
   if (!cv || !rlist || !nr || !n_steady || C <= 0 || G < 1 || G > 8) return WK_ECONFIG;
   cudaStream_t s = (cudaStream_t)stream;
   cache_step_kernel<<<(C + 63) / 64, 64, 0, s>>>(*cv, rlist, nr, n_steady, r_cap, G, union_mode, step, C, status);
+  WK_CHECK_LAUNCH();
+  return 0;
+}
+
+int wk_cache_phase(const wk_cache_view* cv, int32_t* ids, const uint8_t* snap_in, int n, int64_t n_steady,
+                   int64_t step, int phase, uint8_t* snap_out, int32_t* n_out, int* status, void* stream) {
+  if (!cv || n < 0 || phase < 1 || phase > 7 || (n && !ids)) return WK_ECONFIG;
+  if ((phase & 1) && (!snap_out || !n_out)) return WK_ECONFIG;
+  if ((phase & 6) && n && !snap_in) return WK_ECONFIG;
+  cache_phase_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(*cv, ids, snap_in, n, n_steady, step, phase, snap_out,
+                                                         n_out, status);
   WK_CHECK_LAUNCH();
   return 0;
 }

@@ -81,6 +81,57 @@ __device__ __forceinline__ void push_event(const CacheView& cv, int64_t c, int32
   }
 }
 
+// commit_update (block_cache.py:163-213) of one cache unit over its access
+// stream ids[0..n) with the lookup snapshot snap[]; every id is stamped
+// `stamp` in tc[] (the touched set).  st = (lru head, lru tail, heap size).
+__device__ void commit_phase(const CacheCtx& x, const int32_t* ids, const uint8_t* snap, int n, int64_t step,
+                             int32_t stamp, int32_t* st, int64_t* cnt, int* status) {
+  const CacheView& cv = x.cv;
+  const int64_t c = x.c;
+  const int32_t* nb = x.nb();
+  uint8_t* ca = x.ca();
+  int32_t* tc = x.tc();
+  const int64_t bsz = cv.block_bytes;
+  int64_t* la = x.la();
+  for (int i = 0; i < n; i++) {
+    la[ids[i]] = step;
+    if (snap[i]) { lru_unlink(x, st, ids[i]); lru_append(x, st, ids[i]); }
+  }
+  const int64_t cap = cv.capacity[c];
+  int64_t occ = cv.occupied[c];
+  int32_t nxt = cv.next_slot[c];
+  for (int i = 0; i < n; i++) {
+    if (snap[i]) continue;
+    const int32_t cl = ids[i];
+    if (ca[cl]) continue;  // admitted earlier in this commit (repeated id)
+    const int64_t need = nb[cl];
+    if (need > cap) { push_event(cv, c, 3, step, cl, 0); cnt[7]++; continue; }
+    while (cap - occ < need) {
+      int32_t v = st[0];
+      if (v < 0 || tc[v] == stamp) break;  // untouched clusters precede touched ones
+      int32_t* s = x.sl() + x.so()[v];
+      for (int j = 0; j < nb[v]; j++) heap_push(x, st, s[j]);
+      occ -= nb[v];
+      ca[v] = 0;
+      lru_unlink(x, st, v);
+      push_event(cv, c, 1, step, v, 0);
+      cnt[5]++;
+    }
+    if (cap - occ < need) { push_event(cv, c, 3, step, cl, 0); cnt[7]++; continue; }
+    int32_t* s = x.sl() + x.so()[cl];
+    for (int j = 0; j < need; j++) s[j] = st[2] ? heap_pop(x, st) : nxt++;
+    occ += need;
+    ca[cl] = 1;
+    lru_append(x, st, cl);
+    cnt[3] += need * bsz;
+    cnt[6]++;
+    push_event(cv, c, 2, step, cl, (int32_t)need);
+  }
+  if (occ > cap) set_status(status, kErrCapacity);
+  cv.occupied[c] = occ;
+  cv.next_slot[c] = nxt;
+}
+
 // grid = ceil(C / 64), block = 64; one thread per cache unit.
 // ids for cache unit c: if union_heads > 1, the union (round-robin over rank
 // positions of the G heads, first occurrence kept) of rlist[u, 0..G); else
@@ -137,46 +188,66 @@ __global__ void cache_step_kernel(CacheView cv, const int32_t* __restrict__ rlis
     else { cnt[2] += b * bsz; cnt[4] += b * bsz; }
   }
   // ---- commit_update ----
-  int64_t* la = x.la();
-  for (int i = 0; i < n; i++) {
-    la[ids[i]] = step;
-    if (snap[i]) { lru_unlink(x, st, ids[i]); lru_append(x, st, ids[i]); }
-  }
-  const int64_t cap = cv.capacity[c];
-  int64_t occ = cv.occupied[c];
-  int32_t nxt = cv.next_slot[c];
-  for (int i = 0; i < n; i++) {
-    if (snap[i]) continue;
-    const int32_t cl = ids[i];
-    const int64_t need = nb[cl];
-    if (need > cap) { push_event(cv, c, 3, step, cl, 0); cnt[7]++; continue; }
-    while (cap - occ < need) {
-      int32_t v = st[0];
-      if (v < 0 || tc[v] == stamp) break;  // untouched clusters precede touched ones
-      int32_t* s = x.sl() + x.so()[v];
-      for (int j = 0; j < nb[v]; j++) heap_push(x, st, s[j]);
-      occ -= nb[v];
-      ca[v] = 0;
-      lru_unlink(x, st, v);
-      push_event(cv, c, 1, step, v, 0);
-      cnt[5]++;
-    }
-    if (cap - occ < need) { push_event(cv, c, 3, step, cl, 0); cnt[7]++; continue; }
-    int32_t* s = x.sl() + x.so()[cl];
-    for (int j = 0; j < need; j++) s[j] = st[2] ? heap_pop(x, st) : nxt++;
-    occ += need;
-    ca[cl] = 1;
-    lru_append(x, st, cl);
-    cnt[3] += need * bsz;
-    cnt[6]++;
-    push_event(cv, c, 2, step, cl, (int32_t)need);
-  }
-  if (occ > cap) set_status(status, kErrCapacity);
-  cv.occupied[c] = occ;
-  cv.next_slot[c] = nxt;
+  commit_phase(x, ids, snap, n, step, stamp, st, cnt, status);
   cv.lru_ht[c * 2] = st[0];
   cv.lru_ht[c * 2 + 1] = st[1];
   cv.heap_n[c] = st[2];
+}
+
+// The BlockCache phases as separate calls on cache unit 0 (the function-level
+// API, block_cache.py:79-213); one thread.  ids[0..n) as the caller passes them.
+//   phase 1 lookup(ids, step): de-duplicate (first occurrence), validate,
+//     snapshot -> snap_out[0..n_out), hit / miss counters, access event;
+//     *n_out = distinct ids (written back over ids[]).
+//   phase 2 assemble accounting: steady bytes + per id (rank order, as given)
+//     hit -> fast internal, miss -> slow-to-fast + store read bytes.
+//   phase 4 commit_update(ids, snapshot, step).
+__global__ void cache_phase_kernel(CacheView cv, int32_t* ids, const uint8_t* snap_in, int n, int64_t n_steady,
+                                   int64_t step, int phase, uint8_t* snap_out, int32_t* n_out, int* status) {
+  if (threadIdx.x || blockIdx.x) return;
+  CacheCtx x{cv, 0};
+  int64_t* cnt = cv.counters;
+  const int32_t* nb = x.nb();
+  uint8_t* ca = x.ca();
+  const int64_t bsz = cv.block_bytes;
+  if (phase & 1) {
+    int k = 0;
+    for (int i = 0; i < n; i++) {
+      const int32_t cl = ids[i];
+      if (cl < 0 || cl >= cv.m_live[0]) { set_status(status, kErrUnknownCluster); return; }
+      bool dup = false;
+      for (int j = 0; j < k; j++) dup |= ids[j] == cl;
+      if (!dup) ids[k++] = cl;
+    }
+    int64_t hits = 0;
+    for (int i = 0; i < k; i++) {
+      snap_out[i] = ca[ids[i]];
+      hits += snap_out[i];
+    }
+    cnt[0] += hits;
+    cnt[1] += k - hits;
+    push_event(cv, 0, 0, step, k, (int32_t)hits);
+    *n_out = k;
+  }
+  if (phase & 2) {
+    cnt[3] += n_steady * cv.token_bytes;
+    for (int i = 0; i < n; i++) {
+      const int64_t b = nb[ids[i]];
+      if (snap_in[i]) cnt[3] += b * bsz;
+      else { cnt[2] += b * bsz; cnt[4] += b * bsz; }
+    }
+  }
+  if (phase & 4) {
+    const int32_t stamp = (int32_t)(step + 1) ^ 0x40000000;  // distinct from the fused kernel's stamps
+    int32_t* tc = x.tc();
+    for (int i = 0; i < n; i++) tc[ids[i]] = stamp;
+    int32_t st[3] = {cv.lru_ht[0], cv.lru_ht[1], cv.heap_n[0]};
+    commit_phase(x, ids, snap_in, n, step, stamp, st, cnt, status);
+    for (int i = 0; i < n; i++) tc[ids[i]] = 0;  // the touched set lives for one commit
+    cv.lru_ht[0] = st[0];
+    cv.lru_ht[1] = st[1];
+    cv.heap_n[0] = st[2];
+  }
 }
 
 }  // namespace wk

@@ -448,9 +448,11 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
   uint32_t* eb_out = sv.ebits + ((size_t)u * G + g) * sv.w_cap;
   auto S_ = [&](int c) -> float { return SMS ? scs[c] : __ldcg(s + c); };
   // capacity (r fits the candidate and output lists): a configuration error
-  const bool cap_ok = m > 0 && r <= CAND && r <= sv.r_cap;
+  // r beyond the candidate list (e.g. retrieval_fraction near 1) takes the
+  // exact path with the ordered list built in global memory
+  const bool cap_ok = m > 0 && r <= sv.r_cap && (r <= CAND || sv.xscr);
   if (m > 0 && !cap_ok) set_status(sv.status, kErrBandOverflow);
-  bool ok = cap_ok;
+  bool ok = cap_ok && r <= CAND;
   for (int w = t; w < W; w += T) { rbits[w] = 0u; tre[w] = 0u; }
   double B2 = 0.0;
   float bk_mn = 0.f, bk_scale = 0.f;
@@ -726,6 +728,28 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
     static_assert(sizeof(sm.y) >= 258 * sizeof(int), "radix histogram must fit");
     xs_select(m, r, key, idf, hist, k1, i1);
     if (e > 0) xs_select(m, r + e, key, idf, hist, k2, i2);
+    if (r > CAND) {
+      // large R: each member's position in the ordered list is its lexsort
+      // rank over all rows (every better row is in R as well)
+      int32_t* rl_out = sv.rlist + ((size_t)u * G + g) * sv.r_cap;
+      for (int c = t; c < m; c += T) {
+        const unsigned long long kk = key(c);
+        if (xs_in(kk, (unsigned)c, k1, i1)) {
+          int rk = 0;
+          for (int j = 0; j < m; j++) {
+            const unsigned long long kj = key(j);
+            rk += (kj < kk) || (kj == kk && j < c);
+          }
+          rl_out[rk] = c;
+          atomicOr(rbits + zb_word(c), 1u << zb_bit(c));
+        } else if (e > 0 && xs_in(kk, (unsigned)c, k2, i2)) {
+          atomicOr(tre + zb_word(c), 1u << zb_bit(c));
+        }
+      }
+      __syncthreads();
+      if (t == 0 && sv.xcount) atomicAdd(sv.xcount, 1);
+      ok = true;
+    } else {
     for (int c = t; c < m; c += T) {
       const unsigned long long kk = key(c);
       if (xs_in(kk, (unsigned)c, k1, i1)) {
@@ -750,15 +774,17 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
     __syncthreads();
     if (t == 0 && sv.xcount) atomicAdd(sv.xcount, 1);
     ok = true;
+    }
   }
   if (ok) {
     // ---- outputs: ordered retrieval list, R bitmap ----
     int32_t* rl_out = sv.rlist + ((size_t)u * G + g) * sv.r_cap;
-    for (int i = t; i < r; i += T) {
-      const int c = s6_id(sm.x.f.fin[i]);
-      rl_out[i] = c;
-      atomicOr(rbits + zb_word(c), 1u << zb_bit(c));
-    }
+    if (r <= CAND)
+      for (int i = t; i < r; i += T) {
+        const int c = s6_id(sm.x.f.fin[i]);
+        rl_out[i] = c;
+        atomicOr(rbits + zb_word(c), 1u << zb_bit(c));
+      }
     __syncthreads();
     // E = top(r+e) minus R
     int32_t* el_out = sv.elist ? sv.elist + ((size_t)u * G + g) * sv.e_cap : nullptr;

@@ -23,7 +23,7 @@ import torch
 from . import _lib
 from .block_cache import DeviceBlockCache
 from .config import EngineConfig
-from .engine import relative_l2
+from .metrics import relative_l2
 from .errors import ConfigError
 from .tracefile import TraceFile
 from .wave import WaveLayer, _stream

@@ -41,10 +41,15 @@ def test_step_metrics_and_events_match_reference(name):
         assert abs(sm.log_denominator - ref[8]) <= 1e-5
         assert abs(sm.denominator_coverage - ref[7]) <= 1e-5
         assert np.linalg.norm(out - z["outputs"][t]) <= 1e-5 * np.linalg.norm(z["outputs"][t])
-    ev = [(t, s, c, a) for (t, s, c, a) in eng.cache.event_log if t != "access"]
+    log = eng.cache.event_log  # the reference's dicts (block_cache.py:92-95, 188-207)
+    ev = [(e["type"], e["step"], e["cluster"]) for e in log if e["type"] != "access"]
     names = {1: "evict", 2: "admit", 3: "reject"}
     ref_ev = [(names[int(a)], int(b), int(c)) for a, b, c, _ in z["events"]]
-    assert [(t, s, c) for (t, s, c, _) in ev] == ref_ev
+    assert ev == ref_ev
+    acc = [e for e in log if e["type"] == "access"]
+    assert len(acc) == len(z["queries"])
+    assert sum(sum(e["cached"]) for e in acc) == eng.cache.hits
+    assert sum(len(e["clusters"]) - sum(e["cached"]) for e in acc) == eng.cache.misses
     import json
     st = json.loads(str(z["final_stats"]))
     mine = eng.cache.stats()
