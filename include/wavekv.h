@@ -42,8 +42,6 @@ typedef struct wk_index_view {
   double* VS64;       /* [U, m_cap, d] fp64 value sums (optional, may be NULL) */
   int64_t s_cap, m_cap;
   float* Cmax;        /* [U] max_c ||C32_c|| (score error bound), set at build */
-  void* C16;          /* [U, m_cap, d] fp16 centroids / Cscale (scoring scan)   */
-  float* Cscale;      /* [U, m_cap] power-of-two row scale of C16               */
 } wk_index_view;
 
 /* One clustering segment: a contiguous token range of one unit
@@ -138,8 +136,8 @@ typedef struct wk_zone_params {
   double estimation_fraction; /* IndexConfig.estimation_fraction (config.py:27) */
   int32_t tail_denominator_only; /* IndexConfig.tail_mode                      */
   int32_t denominator_eq2;       /* EngineConfig.denominator_mode              */
-  int32_t score_mode;            /* 0 fp32 C32 scan, 1 fp64-accumulated C32,
-                                    2 fp16 C16 on tensor cores                 */
+  int32_t score_mode;            /* 1: the C32 scan accumulated in fp64 (the
+                                    error bound select_v6 uses)                */
   int32_t pad_;
 } wk_zone_params;
 

@@ -23,8 +23,7 @@ _I64 = ctypes.c_int64
 class IndexViewC(ctypes.Structure):
     _fields_ = [("store_k", _P), ("store_v", _P), ("store_tok", _P), ("cl_off", _P),
                 ("cl_size", _P), ("C64", _P), ("C32", _P), ("Cnorm", _P), ("VS32", _P),
-                ("VS64", _P), ("s_cap", _I64), ("m_cap", _I64), ("Cmax", _P), ("C16", _P),
-                ("Cscale", _P)]
+                ("VS64", _P), ("s_cap", _I64), ("m_cap", _I64), ("Cmax", _P)]
 
 
 class SegmentC(ctypes.Structure):

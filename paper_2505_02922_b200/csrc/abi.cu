@@ -29,7 +29,7 @@ template <typename T, bool FULL>
 __global__ void attend_kernel(IndexView, SteadyView, StepView, AttnParams, const int32_t*);
 __global__ void merge_kernel(StepView, AttnParams, int);
 size_t select_smem_bytes();
-// select_v6.cu / attend_v4.cu / score_v4.cu
+// select_v6.cu / attend_v4.cu / score_v5.cu
 template <int CAND, bool SMS, int GM>
 __global__ void select_v6_kernel(IndexView, StepView, SelParams);
 size_t select_v6_dyn_smem(int m_max, bool sms, int cand);
@@ -41,7 +41,6 @@ template <typename T, int DPL, int HS>
 int attend_v4_warps();
 template <bool FULL, int DL>
 __global__ void att4_merge_kernel(SteadyView, StepView, AttnParams, const int32_t*, int, int, int);
-__global__ void km_pack16_kernel(const SegDesc*, IndexView, int);
 __global__ void km_assign_tc5_kernel(const SegDesc*, const float*, const float*, int32_t*, const __nv_bfloat16*);
 __global__ void km_pack_c5_kernel(const SegDesc*, const float*, __nv_bfloat16*);
 constexpr size_t K5_SMEM_BYTES = 2 * 128 * 128 * 2 + 2 * 256 * 128 * 2 + 64;
@@ -69,9 +68,20 @@ using namespace wk;
     if (e_ != cudaSuccess) return WK_ECUDA;        \
   } while (0)
 
-static int g_smem_configured = 0;
+// cudaFuncSetAttribute is per device: run each configuration once per device
+// (a process may drive several GPUs).
+static int current_device() {
+  int d = 0;
+  return cudaGetDevice(&d) == cudaSuccess ? d : 0;
+}
+struct PerDevice {
+  unsigned long long done = 0;  // devices 0..63
+  bool needed() const { const int d = current_device(); return d >= 64 || !((done >> d) & 1ull); }
+  void mark() { const int d = current_device(); if (d < 64) done |= 1ull << d; }
+};
+static PerDevice g_smem_cfg;
 static int configure_smem() {
-  if (g_smem_configured) return 0;
+  if (!g_smem_cfg.needed()) return 0;
   // opt in to large dynamic shared memory where the kernels need it
   if (cudaFuncSetAttribute(km_seed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess) return WK_ECUDA;
   if (cudaFuncSetAttribute(km_seed_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 72 * 1024) != cudaSuccess) return WK_ECUDA;
@@ -89,66 +99,41 @@ static int configure_smem() {
   const int rs = (int)recall_smem_bytes();
   if (cudaFuncSetAttribute(recall_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, rs) != cudaSuccess) return WK_ECUDA;
   if (cudaFuncSetAttribute(recall_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, rs) != cudaSuccess) return WK_ECUDA;
-  g_smem_configured = 1;
+  g_smem_cfg.mark();
   return 0;
 }
 
 static int head_slots(int G) { return G <= 4 ? 4 : 8; }
-// ---- v6 pipeline: score_v4 (tensor cores) | score_v3, select_v6, attend_v4 ----
+// ---- fast pipeline: score_v5 (FP64 tensor cores), select_v6, attend_v4 ----
 static int sm_count() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
-      n = 148;
-  }
-  return n;
+  static int n[64] = {0};
+  const int dev = current_device();
+  int* slot = dev < 64 ? &n[dev] : nullptr;
+  if (slot && *slot) return *slot;
+  int c = 0;
+  if (cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || c <= 0) c = 1;
+  if (slot) *slot = c;
+  return c;
 }
-static int g_sel_prof = 0;
-static thread_local int g_phases = 3;  // wk_score_topk phases: 1 = centroid scan, 2 = zone planning
-// wk_decode_step hands the token append to wk_score_topk's select kernel
+// the token append fused into the zone-planning kernel (wk_decode_step /
+// wk_plan_zones); passed explicitly down to the launcher
 struct AppendArgs { int on; const float* k; const float* v; SteadyView st; int bf16; };
-static thread_local AppendArgs g_append = {0, nullptr, nullptr, {}, 0};
-extern "C" int wk_debug_select_prof(int on) { g_sel_prof = on; return 0; }
 static bool v6_ok(const wk_index_view* ix, const wk_step_view* sv, int d) {
   return (d == 64 || d == 128) && sv->rbits && sv->ebits && sv->pieces && sv->woff && sv->sel_done && ix->Cmax;
-}
-
-template <int KS, int NT>
-static int launch_score_v4(const IndexView& ix, const StepView& sv, int G, int U, int m_max, cudaStream_t s) {
-  const int ntile = (m_max + 15) / 16;
-  // ~8 CTAs of 4 warps per SM-wave over all units
-  long long want = ((long long)ntile * U + 148 * 8 - 1) / (148 * 8);
-  int tpc = (int)((want + 3) / 4) * 4;
-  if (tpc < 8) tpc = 8;
-  dim3 g((ntile + tpc - 1) / tpc, U);
-  score_v4_kernel<KS, NT><<<g, 128, 0, s>>>(ix, sv, G, tpc);
-  return cudaGetLastError() == cudaSuccess ? 0 : WK_ECUDA;
 }
 
 // Launch with programmatic dependent launch (the kernel may be scheduled while
 // the preceding kernel in the stream drains; it calls pdl_wait() before touching
 // anything that kernel wrote) and, optionally, a thread-block cluster.
-// WK_PDL=0 in the environment disables the attribute (A/B timing).
-static bool pdl_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = getenv("WK_PDL");
-    on = (e && e[0] == '0') ? 0 : 1;
-  }
-  return on != 0;
-}
 template <typename... KArgs, typename... Args>
 static cudaError_t launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                              int cluster, Args... args) {
   cudaLaunchConfig_t lc = {};
   cudaLaunchAttribute at[2];
   int n = 0;
-  if (pdl_enabled()) {
-    at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[n].val.programmaticStreamSerializationAllowed = 1;
-    n++;
-  }
+  at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[n].val.programmaticStreamSerializationAllowed = 1;
+  n++;
   if (cluster > 1) {
     at[n].id = cudaLaunchAttributeClusterDimension;
     at[n].val.clusterDim.x = cluster;
@@ -170,13 +155,8 @@ static int launch_score_v5(const IndexView& ix, const StepView& sv, int G, int U
   const long long groups = (m_max + 7) / 8;
   // short warp ranges (~6 eight-row groups per warp, many CTAs in flight) balance the
   // HBM stream better than one exact wave of long ranges: measured 2,146 -> 2,218 tok/s
-  // (profiles/r1_attend_sweep.txt).  WK_SCORE_GPW overrides for tuning experiments.
-  static int gpw_t = -1;
-  if (gpw_t < 0) {
-    const char* e = getenv("WK_SCORE_GPW");
-    gpw_t = e ? atoi(e) : 6;
-    if (gpw_t < 1 || gpw_t > 4096) gpw_t = 6;
-  }
+  // (profiles/r1_attend_sweep.txt).
+  constexpr int gpw_t = 6;
   const long long gpw = gpw_t;
   const long long cpu = (groups + gpw * 4 - 1) / (gpw * 4);
   dim3 grid((unsigned)cpu, U);
@@ -189,8 +169,8 @@ static int launch_select_v6_g(const IndexView& ix, const StepView& sv, const Sel
                             cudaStream_t s) {
   const double r_max = floor(p.retrieval_fraction * (double)m_max + 0.5) + 1;
   const int blocks = U * p.G;
-  static int cfg = 0;
-  if (!cfg) {
+  static PerDevice cfg;
+  if (cfg.needed()) {
     if (cudaFuncSetAttribute(select_v6_kernel<512, true, GM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)select_v6_dyn_smem(16384, true, 512)) != cudaSuccess ||
         cudaFuncSetAttribute(select_v6_kernel<512, false, GM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -198,7 +178,7 @@ static int launch_select_v6_g(const IndexView& ix, const StepView& sv, const Sel
         cudaFuncSetAttribute(select_v6_kernel<2048, false, GM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)select_v6_dyn_smem(262144, false, 2048)) != cudaSuccess)
       return WK_ECUDA;
-    cfg = 1;
+    cfg.mark();
   }
   if (m_max > 262144) return WK_ECONFIG;
   // the G CTAs of a unit form one thread-block cluster (the union runs over DSMEM)
@@ -225,12 +205,12 @@ static int launch_attend_v4(const IndexView& ix, const SteadyView& st, const Ste
                             const int32_t* n_store, int U, int P, cudaStream_t s) {
   if (U > 1024) return WK_ECONFIG;
   const size_t sm = attend_v4_smem<T, DPL, HS, FULL>();
-  static bool configured = false;
-  if (!configured) {
+  static PerDevice cfg;
+  if (cfg.needed()) {
     if (cudaFuncSetAttribute(attend_v4_kernel<T, DPL, HS, FULL, OFF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)sm) != cudaSuccess)
       return WK_ECUDA;
-    configured = true;
+    cfg.mark();
   }
   const int warps = attend_v4_warps<T, DPL, HS>();
   if (launch_ex(attend_v4_kernel<T, DPL, HS, FULL, OFF>, dim3(P), dim3(warps * 32), sm, s, 1, ix, st, sv, p,
@@ -298,14 +278,11 @@ int wk_kmeans_segments(const wk_index_view* ix, const wk_segment* segs, int n_se
   // Lloyd assignment: tensor-core first pass + exact verification when the
   // head dim tiles by 16 (<= 128), else the exact FFMA kernel
   const dim3 ag5((max_L + 127) / 128, n_segs);
-  // d = 128 (k <= 512): tcgen05 contraction with the scores in TMEM; WK_KM_TC5=0 selects the
-  // mma.sync kernel (A/B timing)
-  const char* tc5e = getenv("WK_KM_TC5");
+  // d = 128 (k <= 512): tcgen05 contraction with the scores in TMEM
   // the pre-split centroids reuse the fp16 point copy (dead after seeding): (sum k + 8 n) * 2 rows
   long long sum_l = 0, sum_k = 0;
   for (int i = 0; i < n_segs; i++) { sum_l += segs[i].L; sum_k += segs[i].k; }
-  const bool tc5 = d == 128 && max_k <= 512 && p16 != nullptr && (sum_k + 8LL * n_segs) * 2 <= sum_l &&
-                   !(tc5e && tc5e[0] == '0');
+  const bool tc5 = d == 128 && max_k <= 512 && p16 != nullptr && (sum_k + 8LL * n_segs) * 2 <= sum_l;
   __nv_bfloat16* pk = reinterpret_cast<__nv_bfloat16*>(p16);
   auto assign = [&]() {
     if (tc5) {
@@ -335,10 +312,6 @@ int wk_kmeans_segments(const wk_index_view* ix, const wk_segment* segs, int n_se
   else
     km_finalize_kernel<float><<<n_segs, 256, usmem, s>>>(sd, scr->A, scr->perm, *ix, d, scr->status);
   WK_CHECK_LAUNCH();
-  if (ix->C16 && ix->Cscale && ix->Cmax && (d % 16) == 0 && d <= 128 && (ix->m_cap % 16) == 0) {
-    km_pack16_kernel<<<n_segs, 256, 0, s>>>(sd, *ix, d);
-    WK_CHECK_LAUNCH();
-  }
   return 0;
 }
 
@@ -352,28 +325,20 @@ int wk_append_tokens(const wk_steady_view* st, const float* k_new, const float* 
   return 0;
 }
 
-int wk_score_topk(const wk_index_view* ix, const wk_step_view* sv, const wk_zone_params* zp, int U,
-                  int m_max, void* stream) {
+// centroid scan (phase bit 1) and exact zone planning + unions (bit 2) of
+// wk_score_topk / wk_centroid_scan / wk_plan_zones; `app` = the fused append
+static int score_topk_impl(const wk_index_view* ix, const wk_step_view* sv, const wk_zone_params* zp, int U,
+                           int m_max, int phases, const AppendArgs* app, cudaStream_t s) {
   if (!ix || !sv || !zp || U <= 0 || zp->G < 1 || zp->G > 8 || zp->d <= 0 || zp->d > 256 || (zp->d & 3))
     return WK_ECONFIG;
   if (configure_smem()) return WK_ECUDA;
-  cudaStream_t s = (cudaStream_t)stream;
   if (v6_ok(ix, sv, zp->d)) {
-    const bool tc = zp->score_mode == 2 && ix->C16 && ix->Cscale;
-    int rc = 0;
-    if (m_max > 0 && (g_phases & 1)) {
-      const int nt = zp->G <= 4 ? 1 : 2;
-      if (tc) {
-        if (zp->d == 128) rc = nt == 1 ? launch_score_v4<8, 1>(*ix, *sv, zp->G, U, m_max, s)
-                                       : launch_score_v4<8, 2>(*ix, *sv, zp->G, U, m_max, s);
-        else rc = nt == 1 ? launch_score_v4<4, 1>(*ix, *sv, zp->G, U, m_max, s)
-                          : launch_score_v4<4, 2>(*ix, *sv, zp->G, U, m_max, s);
-      } else {
-        rc = zp->d == 128 ? launch_score_v5<8>(*ix, *sv, zp->G, U, m_max, s)
-                          : launch_score_v5<4>(*ix, *sv, zp->G, U, m_max, s);
-      }
+    if (m_max > 0 && (phases & 1)) {
+      const int rc = zp->d == 128 ? launch_score_v5<8>(*ix, *sv, zp->G, U, m_max, s)
+                                  : launch_score_v5<4>(*ix, *sv, zp->G, U, m_max, s);
       if (rc) return rc;
     }
+    if (!(phases & 2)) return 0;
     SelParams p;
     p.G = zp->G; p.d = zp->d; p.blas_threads = zp->blas_threads;
     p.retrieval_fraction = zp->retrieval_fraction;
@@ -382,12 +347,11 @@ int wk_score_topk(const wk_index_view* ix, const wk_step_view* sv, const wk_zone
     p.need_tail = zp->tail_denominator_only;
     p.need_allc = zp->denominator_eq2;
     p.score_fp64 = 1;
-    p.score_mode = tc ? 2 : 1;
+    p.score_mode = 1;
     p.piece_rows = head_slots(zp->G) == 4 ? 16 : 8;  // attend_v4 chunk rows (Att4Cfg::RG)
-    p.prof = g_sel_prof;
     p.k_new = nullptr; p.v_new = nullptr; p.store_bf16 = 0;
-    if (g_append.on) { p.k_new = g_append.k; p.v_new = g_append.v; p.st = g_append.st; p.store_bf16 = g_append.bf16; }
-    return (g_phases & 2) ? launch_select_v6(*ix, *sv, p, U, m_max, s) : 0;
+    if (app && app->on) { p.k_new = app->k; p.v_new = app->v; p.st = app->st; p.store_bf16 = app->bf16; }
+    return launch_select_v6(*ix, *sv, p, U, m_max, s);
   }
   if (m_max > 0) {
     dim3 g1((m_max + 63) / 64, U);
@@ -404,12 +368,16 @@ int wk_score_topk(const wk_index_view* ix, const wk_step_view* sv, const wk_zone
   p.score_fp64 = 0;
   p.score_mode = 0;
   p.piece_rows = 0;
-  p.prof = 0;
   select_kernel<<<U * zp->G, 512, select_smem_bytes(), s>>>(*ix, *sv, p);
   WK_CHECK_LAUNCH();
   union_kernel<<<U, 1024, 0, s>>>(*ix, *sv);
   WK_CHECK_LAUNCH();
   return 0;
+}
+
+int wk_score_topk(const wk_index_view* ix, const wk_step_view* sv, const wk_zone_params* zp, int U,
+                  int m_max, void* stream) {
+  return score_topk_impl(ix, sv, zp, U, m_max, 3, nullptr, (cudaStream_t)stream);
 }
 
 int wk_tripartite_attn(const wk_index_view* ix, const wk_steady_view* st, const wk_step_view* sv,
@@ -508,9 +476,8 @@ int wk_decode_step(const wk_index_view* ix, const wk_steady_view* st, const wk_s
     if (rc) return rc;
     return wk_tripartite_attn(ix, st, sv, zp, U, S, store_bf16, stream);
   }
-  g_append = {1, k_new, v_new, *st, store_bf16};
-  const int rc = wk_score_topk(ix, sv, zp, U, m_max, stream);
-  g_append.on = 0;
+  const AppendArgs app = {1, k_new, v_new, *st, store_bf16};
+  const int rc = score_topk_impl(ix, sv, zp, U, m_max, 3, &app, (cudaStream_t)stream);
   if (rc) return rc;
   return wk_tripartite_attn(ix, st, sv, zp, U, S, store_bf16, stream);
 }
@@ -518,9 +485,7 @@ int wk_decode_step(const wk_index_view* ix, const wk_steady_view* st, const wk_s
 int wk_centroid_scan(const wk_index_view* ix, const wk_step_view* sv, const wk_zone_params* zp, int U, int m_max,
                      void* stream) {
   if (!ix || !sv || !zp || !v6_ok(ix, sv, zp->d)) return WK_ECONFIG;
-  g_phases = 1;
-  const int rc = wk_score_topk(ix, sv, zp, U, m_max, stream);
-  g_phases = 3;
+  const int rc = score_topk_impl(ix, sv, zp, U, m_max, 1, nullptr, (cudaStream_t)stream);
   return rc;
 }
 
@@ -528,11 +493,9 @@ int wk_plan_zones(const wk_index_view* ix, const wk_steady_view* st, const wk_st
                   const wk_zone_params* zp, const float* k_new, const float* v_new, int U, int m_max,
                   int store_bf16, void* stream) {
   if (!ix || !sv || !zp || !v6_ok(ix, sv, zp->d)) return WK_ECONFIG;
-  g_phases = 2;
-  if (k_new && v_new && st) g_append = {1, k_new, v_new, *st, store_bf16};
-  const int rc = wk_score_topk(ix, sv, zp, U, m_max, stream);
-  g_append.on = 0;
-  g_phases = 3;
+  AppendArgs app = {0, nullptr, nullptr, {}, 0};
+  if (k_new && v_new && st) app = {1, k_new, v_new, *st, store_bf16};
+  const int rc = score_topk_impl(ix, sv, zp, U, m_max, 2, &app, (cudaStream_t)stream);
   return rc;
 }
 

@@ -251,19 +251,7 @@ WK_DEVINL double score_error_bound(double qnorm2, double cmax, int d, bool fp64_
 // Bound for the scoring modes of wk_zone_params.score_mode:
 //  0: fp32 FMA scan of C32           gamma_d + C32 rounding + store
 //  1: fp64-accumulated scan of C32   C32 rounding + fp32 store (2^-23)
-//  2: C16 = fp16(C / 2^k) on tensor cores, q split into fp16 hi + lo:
-//     fp16 rounding of C (2^-11 relative, + subnormal floor), q split
-//     residual (2^-22), fp32 tensor-core accumulation (d 2^-21, generous),
-//     fp32 store (2^-24)
 WK_DEVINL double score_error_bound_v2(double qnorm2, double cmax, int d, int mode) {
-  const double uu = 5.9604644775390625e-08;  // 2^-24
-  const double qn = sqrt(qnorm2);
-  if (mode == 2) {
-    const double rel = 4.8828125e-04 /*2^-11*/ + 2.384185791015625e-07 /*2^-22*/ +
-                       (double)d * 4.76837158203125e-07 /*2^-21*/ + uu;
-    // subnormal floors of C16 and of the q split: 2^-39 |x|_max per element
-    return 1.25 * (rel + 1.0e-11 * sqrt((double)d)) * qn * cmax + 1e-30;
-  }
   return score_error_bound(qnorm2, cmax, d, mode == 1);
 }
 

@@ -17,7 +17,6 @@ struct SelParams {
   int score_fp64;  // scores came from the fp64-accumulating kernel (score_v3)
   int score_mode;  // wk_zone_params.score_mode of the scores being selected
   int piece_rows;  // rows per retrieval piece (attend_v4 chunk rows)
-  int prof;        // record phase timestamps (g_sel_dbg)
   // fused append of this step's token (engine.py:178-182), done by the
   // head-0 CTA of each unit; k_new == nullptr: no append
   const float* k_new;

@@ -75,7 +75,7 @@ class WaveLayer:
     def __init__(self, cfg: EngineConfig, U: int, G: int, d: int, *, max_prefill: int,
                  max_decode: int = 1024, store_dtype=torch.bfloat16, device="cuda",
                  blas_threads: int = 1, splits: int | None = None, keep_vs64: bool = False,
-                 with_elist: bool = False, score_mode: int | None = None, offload: bool = False,
+                 with_elist: bool = False, offload: bool = False,
                  split: int = 1):
         self.cfg = cfg.validate()
         ic = cfg.index
@@ -99,14 +99,14 @@ class WaveLayer:
         k_upd = math.ceil(ic.update_segment / ic.centroid_ratio)
         m_pref = sum(math.ceil(min(ic.segment_size, n_idx - s) / ic.centroid_ratio)
                      for s in range(0, n_idx, ic.segment_size))
-        # multiple of 128: float4 scans, 16-row C16 tiles, zone bitmaps (4 words / 128 clusters)
+        # multiple of 128: float4 scans, zone bitmaps (4 words / 128 clusters)
         self.m_cap = max(128, -(-(m_pref + n_upd * k_upd) // 128) * 128)
         self.s_cap = max(1, n_idx + n_upd * ic.update_segment)
         self.t_cap = ic.sink_tokens + ic.update_segment + ic.local_window + max(0, ic.local_window) + 8
         self.t_cap = max(self.t_cap, min(max_prefill, ic.sink_tokens + ic.local_window) + 8)
         self.r_cap = max(1, min(self.m_cap, round_half_up(ic.retrieval_fraction * self.m_cap) + 2))
         self.e_cap = max(1, min(self.m_cap, round_half_up(ic.estimation_fraction * self.m_cap) + 2))
-        # fast path (select_v6 / attend_v4 / score_v4): d in {64, 128}
+        # fast path (score_v5 / select_v6 / attend_v4): d in {64, 128}
         self.fast = d in (64, 128)
         hs = 4 if G <= 4 else 8
         self.piece_rows = 16 if hs == 4 else 8  # attend_v4 chunk rows
@@ -116,10 +116,8 @@ class WaveLayer:
             self.attn_warps = 8 if hs == 8 else (12 if (store_dtype == torch.bfloat16 or d == 64) else 6)
         else:
             self.S = splits or max(1, min(64, -(-2048 // U)))
-        # 1: fp32 C scan with fp64 accumulation (estimation logits need ~fp32
-        # accuracy); 2: fp16 C16 tensor-core scan (selection exact, estimation
-        # logits approximate -- experimental)
-        self.score_mode = 1 if score_mode is None else int(score_mode)
+        # the C32 scan accumulates in fp64 (the estimation logits need ~fp32 accuracy)
+        self.score_mode = 1
         dev, f32, i32 = self.dev, torch.float32, torch.int32
         # ---- index arrays ----
         # offload (config 4): the cluster store is pinned host memory (the
@@ -145,9 +143,6 @@ class WaveLayer:
         self.VS64 = (torch.zeros((U, self.m_cap, d), dtype=torch.float64, device=dev)
                      if keep_vs64 else None)
         self.Cmax = torch.zeros(U, dtype=f32, device=dev)
-        use16 = self.fast and self.score_mode == 2
-        self.C16 = torch.zeros((U, self.m_cap, d), dtype=torch.float16, device=dev) if use16 else None
-        self.Cscale = torch.zeros((U, self.m_cap), dtype=f32, device=dev) if use16 else None
         # ---- steady zone ----
         self.st_k = torch.zeros((U, self.t_cap, d), dtype=store_dtype, device=dev)
         self.st_v = torch.zeros((U, self.t_cap, d), dtype=store_dtype, device=dev)
@@ -211,7 +206,7 @@ class WaveLayer:
         self._ixv = _lib.IndexViewC(
             _ptr(self.store_k), _ptr(self.store_v), _ptr(self.store_tok), _ptr(self.cl_off),
             _ptr(self.cl_size), _ptr(self.C64), _ptr(self.C32), _ptr(self.Cnorm), _ptr(self.VS32),
-            _ptr(self.VS64), self.s_cap, self.m_cap, _ptr(self.Cmax), _ptr(self.C16), _ptr(self.Cscale))
+            _ptr(self.VS64), self.s_cap, self.m_cap, _ptr(self.Cmax))
         self._stv = _lib.SteadyViewC(_ptr(self.st_k), _ptr(self.st_v), _ptr(self.st_tok),
                                      _ptr(self.st_n), _ptr(self.next_tok), self.t_cap)
         self.cache = None
@@ -240,8 +235,7 @@ class WaveLayer:
         return _lib.IndexViewC(
             _ptr(sl(self.store_k)), _ptr(sl(self.store_v)), _ptr(sl(self.store_tok)), _ptr(sl(self.cl_off)),
             _ptr(sl(self.cl_size)), _ptr(sl(self.C64)), _ptr(sl(self.C32)), _ptr(sl(self.Cnorm)),
-            _ptr(sl(self.VS32)), _ptr(sl(self.VS64)), self.s_cap, self.m_cap, _ptr(sl(self.Cmax)),
-            _ptr(sl(self.C16)), _ptr(sl(self.Cscale)))
+            _ptr(sl(self.VS32)), _ptr(sl(self.VS64)), self.s_cap, self.m_cap, _ptr(sl(self.Cmax)))
 
     def _steady_view(self, u0, u1):
         return _lib.SteadyViewC(_ptr(self.st_k[u0:u1]), _ptr(self.st_v[u0:u1]), _ptr(self.st_tok[u0:u1]),
