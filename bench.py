@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-flashinfer", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: every rank serves --batch requests; strong: the --batch x H_kv units "
+                         "are split over the ranks (parallel.shard_units)")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the reduced configs[2]/[3]/[4] legs of the default run")
     ap.add_argument("--split", type=int, default=1, help="unit groups pipelined on streams")
@@ -469,7 +472,13 @@ def run_decode(a, torch, dev, model, log, rank=0, world=1, batch=None, ctx=None,
     steps = steps if steps is not None else a.steps
     warmup = warmup if warmup is not None else a.warmup
     G = hq // hkv
-    U = batch * hkv  # per-rank units (weak scaling: each rank serves `batch` requests)
+    shard = None
+    if headline and a.scaling == "strong" and world > 1:
+        from paper_2505_02922_b200.parallel import shard_units
+        shard = shard_units(batch, hkv, world, rank)  # contiguous block of the global units
+        U = shard.count
+    else:
+        U = batch * hkv  # per-rank units (weak scaling: each rank serves `batch` requests)
     n_bufs = min(layer_bufs or a.layer_bufs, layers_n)
     per_buf = math.ceil(layers_n / n_bufs)
     total_steps = warmup + steps + 2  # + the per-op breakdown step
@@ -495,22 +504,34 @@ def run_decode(a, torch, dev, model, log, rank=0, world=1, batch=None, ctx=None,
         torch.cuda.empty_cache()
         log(f"[{model}] layer buffer {li}: m={lay.units[0].m} build {t_build:.1f}s")
     use = [0] * n_bufs
-    gather_buf = torch.empty((world, U, G, d), device=dev) if world > 1 else None
+    # N > 1: the path's one collective -- every layer's attention outputs are
+    # gathered (NCCL all-gather over NVLink) on a side stream, overlapping the
+    # next layers' kernels; shards are padded to the largest
+    gmax = (-(-batch * hkv // world) if shard else U) if world > 1 else 0
+    slabs = torch.zeros((layers_n, gmax, G, d), device=dev) if world > 1 else None
+    gbufs = torch.empty((layers_n, world * gmax, G, d), device=dev) if world > 1 else None
+    comm = torch.cuda.Stream(device=dev) if world > 1 else None
+    gev = [torch.cuda.Event() for _ in range(layers_n)] if world > 1 else None
 
     def wave_step():
+        main_s = torch.cuda.current_stream()
         for l in range(layers_n):
             b = l % n_bufs
             lay = layers[b]
             j = use[b]
             use[b] += 1
-            lay.launch_step(qpool[b][j], kpool[b][j, 0], kpool[b][j, 1])
+            lay.launch_step(qpool[b][j], kpool[b][j, 0], kpool[b][j, 1],
+                            out=slabs[l, :U] if world > 1 else None)
             for s in lay.units:
                 s.total += 1
                 s.n_steady += 1
+            if world > 1:
+                gev[l].record(main_s)
+                comm.wait_event(gev[l])
+                with torch.cuda.stream(comm):
+                    _all_gather_into(dist, gbufs[l], slabs[l])
         if world > 1:
-            # the path's one collective: final gather of the attention outputs
-            # (SURVEY 8(e)); NCCL over NVLink, ordered on the current stream
-            dist.all_gather_into_tensor(gather_buf, layers[(layers_n - 1) % n_bufs].out)
+            main_s.wait_stream(comm)
 
     import torch.distributed as dist
     for _ in range(warmup):
@@ -528,12 +549,35 @@ def run_decode(a, torch, dev, model, log, rank=0, world=1, batch=None, ctx=None,
         torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1) / steps
     if world > 1:
-        t = torch.tensor([ms], device=dev)
+        t = torch.tensor([ms], device=dev if not _DRY else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t)
     for lay in layers:
         lay.check_status("bench")
-    value = batch * world / (ms / 1e3)
+    tok_step = batch if shard else batch * world  # tokens one step produces over all ranks
+    value = tok_step / (ms / 1e3)
+    multi = None
+    if world > 1:
+        # the gathers alone, serialized on the main stream (their cost if nothing overlapped them)
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        g0.record()
+        for l in range(layers_n):
+            _all_gather_into(dist, gbufs[l], slabs[l])
+        g1.record()
+        torch.cuda.synchronize()
+        cdev = dev if not _DRY else "cpu"
+        counts = [torch.zeros(1, device=cdev, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(counts, torch.tensor([U], device=cdev, dtype=torch.int64))
+        counts = [int(c) for c in counts]
+        multi = {"scaling": "strong" if shard else "weak", "units_per_gpu": counts,
+                 "load_imbalance": max(counts) / (sum(counts) / len(counts)),
+                 "per_gpu_tokens_per_s": value / world,
+                 "gather": {"collective": "NCCL all_gather_into_tensor per layer, side stream",
+                            "bytes_per_step": int(gbufs.numel() * 4),
+                            "ms_per_step_serialized": g0.elapsed_time(g1)},
+                 "nccl_debug": os.environ.get("NCCL_DEBUG"),
+                 "backend": "gloo (dry run: ranks share one GPU)" if _DRY else "nccl"}
 
     # ---- per-op device time inside one more step (events on the launch stream) ----
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(layers_n)]
@@ -674,7 +718,7 @@ def run_decode(a, torch, dev, model, log, rank=0, world=1, batch=None, ctx=None,
         e1.record()
         torch.cuda.synchronize()
         e2e_ms = e0.elapsed_time(e1) / k_e2e
-        e2e = {"value": batch * world / (e2e_ms / 1e3), "unit": "tokens/s",
+        e2e = {"value": tok_step / (e2e_ms / 1e3), "unit": "tokens/s",
                "h2d_bytes_per_step": int(hq_.numel() * 4 + hkv_buf.numel() * 4),
                "d2h_bytes_per_step": int(hout.numel() * 4), "ms_per_step": e2e_ms}
     del layers, qpool, kpool
@@ -685,23 +729,25 @@ def run_decode(a, torch, dev, model, log, rank=0, world=1, batch=None, ctx=None,
 
     fa_block = {"impl": "wk_full_attn (this repo, same kernel family reading every token)",
                 "ms_per_step": fa_ms,
-                "value": (batch * world / (fa_ms / 1e3)) if fa_ms else None,
+                "value": (tok_step / (fa_ms / 1e3)) if fa_ms else None,
                 "speedup_wave_vs_full": (fa_ms / ms) if fa_ms else None,
                 "bytes_per_layer": fa_bytes_layer,
                 "hbm_gbs": (fa_bytes_layer * layers_n / (fa_ms / 1e3) / 1e9) if fa_ms else None}
     if fi:
         fi["speedup_wave_vs_full"] = fi["ms_per_step"] / ms
-        fi["value"] = batch * world / (fi["ms_per_step"] / 1e3)
+        fi["value"] = tok_step / (fi["ms_per_step"] / 1e3)
     read_peak = fi["hbm_gbs"] if fi else None
     cfg_name = "configs[1]" if model == "llama3-8b" else "configs[4]"
     return {
         "metric": METRIC,
         "value": value, "unit": "tokens/s", "n_gpus": world, "steps": steps,
-        "warmup": warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong" if shard else "weak", "multi_gpu": multi,
         "vs_baseline": None, "dtype": "bf16 KV / fp32 accumulate (fp64 scoring)", "data": "synthetic",
         "config": {"workload": f"{model}-shape {layers_n}-layer decode, {ctx // 1024}K ctx, batch {batch} ({cfg_name})",
                    "model_shape": model,
-                   "batch_per_gpu": batch, "ctx": ctx, "layers": layers_n,
+                   "batch_per_gpu": batch if not shard else None, "global_batch": tok_step,
+                   "units_this_rank": U, "ctx": ctx, "layers": layers_n,
                    "layer_buffers": n_bufs, "heads": f"{hq}q/{hkv}kv", "d": d,
                    "l2": "inputs larger than L2 (each layer buffer >> 126 MB, cycled)"},
         "full_attention": fi or fa_block,
@@ -730,6 +776,24 @@ def run_decode(a, torch, dev, model, log, rank=0, world=1, batch=None, ctx=None,
     }
 
 
+_DRY = False  # world > visible GPUs: a 1-GPU dry run of the multi-rank path over gloo
+
+
+def _all_gather_into(dist, dst, src):
+    """The per-layer output gather (NCCL all-gather; host-staged on gloo dry runs)."""
+    if not _DRY:
+        dist.all_gather_into_tensor(dst, src)
+        return
+    parts = [torch_mod().empty_like(src, device="cpu") for _ in range(dist.get_world_size())]
+    dist.all_gather(parts, src.cpu())
+    dst.copy_(torch_mod().cat(parts).to(dst.device))
+
+
+def torch_mod():
+    import torch
+    return torch
+
+
 def _compact(line, keys):
     return {k: line.get(k) for k in keys}
 
@@ -748,9 +812,16 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = local % max(1, torch.cuda.device_count())  # (ranks share a GPU only in 1-GPU dry runs)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    global _DRY
+    _DRY = world > torch.cuda.device_count()
+    if world > 1 and _DRY:
+        dist.init_process_group("gloo")  # NCCL refuses two ranks on one GPU
+    elif world > 1:
+        if os.environ.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
+            os.environ["NCCL_DEBUG"] = "INFO"  # the rank / transport lines on stderr
         dist.init_process_group("nccl", device_id=dev)
     log = lambda *x: print(*x, file=sys.stderr, flush=True) if rank == 0 else None
     if a.offload:
