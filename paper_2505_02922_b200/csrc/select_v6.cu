@@ -27,6 +27,14 @@
 
 namespace wk {
 
+// phase timestamps for tools/sel_timing.py (a separate -DWK_SEL_TIMING build;
+// compiled out of the product library)
+#ifdef WK_SEL_TIMING
+__device__ long long g_s6_ts[16384 * 16];
+#define S6_MARK(i) do { if (threadIdx.x == 0) g_s6_ts[(size_t)blockIdx.x * 16 + (i)] = clock64(); } while (0)
+#else
+#define S6_MARK(i) do {} while (0)
+#endif
 
 constexpr int S6_T = 256;
 constexpr int S6_NW = S6_T / 32;
@@ -264,7 +272,9 @@ __device__ void s6_union_cl(const IndexView& ix, const StepView& sv, const SelPa
     if (lane < 4) atomicAdd(&sm.ctot[lane], wc[lane]);
   }
   // ---- slice bases from the peers' totals (DSMEM) ----
+  S6_MARK(8);
   cl.sync();
+  S6_MARK(9);
   if (t < 4) {
     int base = 0, tot = 0;
     const uint32_t loc = (uint32_t)__cvta_generic_to_shared(&sm.ctot[t]);
@@ -364,7 +374,9 @@ __device__ void s6_union_cl(const IndexView& ix, const StepView& sv, const SelPa
     for (int i = 0; i < 4; i++) tb[i] += ttot[i];
   }
   // ---- head g's estimation logits of every row (own staged scores) ----
+  S6_MARK(10);
   cl.sync();  // all rows emitted (cluster-scope release / acquire); peers done with this CTA's smem
+  S6_MARK(11);
   if (!fits) return;
   float* eux = sv.eu_x + (size_t)u * sv.eu_cap * G + g;
   const float isd = p.inv_sqrt_d;
@@ -387,6 +399,7 @@ __device__ void s6_union_cl(const IndexView& ix, const StepView& sv, const SelPa
       }
     }
   }
+  S6_MARK(12);
 }
 
 // ---------------------------------------------------------------------------
@@ -398,6 +411,7 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
   pdl_wait();
   const int G = p.G, d = p.d;
   const int u = blockIdx.x / G, g = blockIdx.x % G;
+  S6_MARK(0);
   const int m = sv.m[u];
   const int t = threadIdx.x, T = S6_T, lane = t & 31, warp = t >> 5;
   const int W = zb_words(m);
@@ -493,6 +507,7 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
     if (t == 0) { sm.ncand = sm.n_in_r = sm.nband_e = sm.n_in_e = sm.nx = sm.ovf = 0; sm.b1 = sm.b2 = -1; }
     float nmn = -mn;
     s6_reduce3(qq, mx, nmn, sm);
+    S6_MARK(1);
     mn = -nmn;
     // |s' - s| <= B; with fp64 queries the scan's fp32 q adds 2^-24 |q| |C|
     const double B = score_error_bound_v2((double)qq, (double)ix.Cmax[u], d, p.score_mode) * (q64 ? 1.6 : 1.0);
@@ -552,6 +567,7 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
     if (b1 < 0 || (e > 0 && b2 < 0)) ok = false;
     hr = edge_hi(b1) + B2; lr = edge_lo(b1) - B2;
     if (e > 0) { he = edge_hi(b2) + B2; le = edge_lo(b2) - B2; }
+    S6_MARK(2);
   }
   if (ok) {
     // ---- pass D: candidates for R (certain-in + band), band around tau_e,
@@ -575,7 +591,6 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
         for (int k = 0; k < 4; k++) v[k] = 4 * qi + k < m ? S_(4 * qi + k) : -INFINITY;
       }
       bool cand[4], bd_e[4];
-      bool anyc = false, anyb = false;
 #pragma unroll
       for (int k = 0; k < 4; k++) {
         const bool in_r = v[k] > fhr, in_e = v[k] > fhe;
@@ -585,26 +600,44 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
         cnt_in_e += in_e;
         const unsigned mie = __ballot_sync(0xffffffffu, in_e);
         if (lane == k && 4 * (base + 32 * warp) + k < m) tre[((base + 32 * warp) >> 5) * 4 + k] = mie;
-        anyc |= cand[k] && !in_r;
-        anyb |= bd_e[k];
       }
-      if (anyc || anyb) {
+      if (base == 0) S6_MARK(13);
+      // warp-aggregated appends: one warp prefix sum + one shared-memory
+      // atomic per list per iteration (all four clusters of every lane)
+      {
+        const int nc4 = (int)cand[0] + (int)cand[1] + (int)cand[2] + (int)cand[3];
+        const int nb4 = (int)bd_e[0] + (int)bd_e[1] + (int)bd_e[2] + (int)bd_e[3];
+        int xc = nc4 | (nb4 << 16);  // both counts in one scan (each <= 128 per warp)
 #pragma unroll
-        for (int k = 0; k < 4; k++)
-          if ((cand[k] && !(v[k] > fhr)) || bd_e[k]) {
-            const char* row = reinterpret_cast<const char*>(C64 + (size_t)(4 * qi + k) * d);
-            for (int o = 0; o < d * 8; o += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(row + o));
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, xc, o);
+          if (lane >= o) xc += y;
+        }
+        const int tot = __shfl_sync(0xffffffffu, xc, 31);
+        if (tot) {
+          int bc = 0, bb = 0;
+          if (lane == 0) {
+            if (tot & 0xffff) bc = atomicAdd(&sm.ncand, tot & 0xffff);
+            if (tot >> 16) bb = atomicAdd(&sm.nband_e, tot >> 16);
           }
-      }
-      if (__any_sync(0xffffffffu, cand[0] || cand[1] || cand[2] || cand[3])) {
+          bc = __shfl_sync(0xffffffffu, bc, 0) + (xc & 0xffff) - nc4;
+          bb = __shfl_sync(0xffffffffu, bb, 0) + (xc >> 16) - nb4;
 #pragma unroll
-        for (int k = 0; k < 4; k++) s6_append(cand[k], s6_key(v[k], 4 * qi + k), sm.y.cand, &sm.ncand, CAND, &sm.ovf);
+          for (int k = 0; k < 4; k++) {
+            if (cand[k]) {
+              if (bc < CAND) sm.y.cand[bc] = s6_key(v[k], 4 * qi + k); else sm.ovf = 1;
+              bc++;
+            }
+            if (bd_e[k]) {
+              if (bb < S6_BAND) sm.be_id[bb] = 4 * qi + k; else sm.ovf = 1;
+              bb++;
+            }
+          }
+        }
       }
-      if (__any_sync(0xffffffffu, anyb)) {
-#pragma unroll
-        for (int k = 0; k < 4; k++) s6_append(bd_e[k], 4 * qi + k, sm.be_id, &sm.nband_e, S6_BAND, &sm.ovf);
-      }
+      if (base == 0) S6_MARK(14);
     }
+    S6_MARK(15);
     cnt_in_r = __reduce_add_sync(0xffffffffu, cnt_in_r);
     cnt_in_e = __reduce_add_sync(0xffffffffu, cnt_in_e);
     if (lane == 0) {
@@ -612,10 +645,26 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
       atomicAdd(&sm.n_in_e, cnt_in_e);
     }
     __syncthreads();
+    S6_MARK(3);
     const int nc = sm.ncand, nin_r = sm.n_in_r, nbe = sm.nband_e, nin_e = e > 0 ? sm.n_in_e : 0;
     if (sm.ovf || nin_r > r || nc < r || (e > 0 && (nin_e > r + e || nin_e + nbe < r + e))) {
       ok = false;
     } else {
+      // the band rows' fp64 centroid rows (the exact round's input) go to L2
+      // while the candidates are ordered
+      const int lpr = d >> 4;  // 128-byte lines per fp64 row
+      for (int i = t; i < (nc + nbe) * lpr; i += T) {
+        const int row = i / lpr;
+        int c;
+        if (row < nc) {
+          const unsigned long long kk = sm.y.cand[row];
+          if (s6_score(kk) > fhr) continue;  // certainly in: exact only if it is in a clump
+          c = s6_id(kk);
+        } else {
+          c = sm.be_id[row - nc];
+        }
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(C64 + (size_t)c * d) + (i - row * lpr) * 128));
+      }
       // ---- order candidates by (approx desc, id asc): rank by counting ----
       for (int i = t; i < nc; i += T) {
         const unsigned long long k = sm.y.cand[i];
@@ -624,6 +673,7 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
         sm.cs[rk] = k;
       }
       __syncthreads();
+      S6_MARK(4);
       // ---- positions needing an exact score: band rows and clump members ----
       for (int base = 0; base < nc; base += T) {
         const int i = base + t;
@@ -655,6 +705,7 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
         }
       }
       __syncthreads();
+      S6_MARK(5);
       // ---- band winners for R: best (r - nin_r) band rows by exact score ----
       const int need_r = r - nin_r;
       for (int i = nin_r + t; i < nc; i += T) {
@@ -840,11 +891,19 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
     for (int w = t; w < W; w += T) { rb_out[w] = 0u; eb_out[w] = 0u; rbits[w] = 0u; tre[w] = 0u; }
   }
   if (!ok && t == 0) { tailp[0] = -INFINITY; tailp[1] = 0.f; tailp[2] = -INFINITY; tailp[3] = 0.f; }
+  S6_MARK(6);
   pdl_trigger<2>();
   // ---- the unit's G CTAs (one cluster) build the union together ----
   cooperative_groups::this_cluster().sync();  // every head's R / E bitmaps final in its smem
+  S6_MARK(7);
   s6_union_cl<CAND, SMS, GM>(ix, sv, p, u, g, m, sm, rbits, tre, scs);
 }
+
+#ifdef WK_SEL_TIMING
+extern "C" int wk_sel_timing(long long* host, int n) {
+  return cudaMemcpyFromSymbol(host, g_s6_ts, sizeof(long long) * (size_t)n) == cudaSuccess ? 0 : -2;
+}
+#endif
 
 size_t select_v6_dyn_smem(int m_max, bool sms, int cand) {
   const int W = zb_words(m_max);
