@@ -43,6 +43,7 @@ template <bool FULL, int DL>
 __global__ void att4_merge_kernel(SteadyView, StepView, AttnParams, const int32_t*, int, int, int);
 __global__ void km_assign_tc5_kernel(const SegDesc*, const float*, const float*, int32_t*, const __nv_bfloat16*);
 __global__ void km_pack_c5_kernel(const SegDesc*, const float*, __nv_bfloat16*);
+constexpr int KS_CK = 8192 / 32 + 4;  // km_seed_v2 cumsum checkpoint slots (kmeans.cu)
 constexpr size_t K5_SMEM_BYTES = 2 * 128 * 128 * 2 + 2 * 256 * 128 * 2 + 64;
 template <int EPL>
 __global__ void km_prep_v2_kernel(const SegDesc*, float*, __half*);
@@ -261,7 +262,7 @@ int wk_kmeans_segments(const wk_index_view* ix, const wk_segment* segs, int n_se
     // v2: 256 threads; centre + centre-distance bounds + (md, best) rows in smem
     // when they fit 72 KB (4 segments per SM at 120K: 52 KB)
     const int L4 = (max_L + 3) & ~3, K4 = (max_k + 3) & ~3;
-    const size_t base = (size_t)(d + K4) * sizeof(float);
+    const size_t base = (size_t)(d + K4 + KS_CK) * sizeof(float);  // centre, bounds, cumsum checkpoints
     const size_t rows = (size_t)L4 * sizeof(float) + (size_t)L4 * sizeof(unsigned short);
     const bool in_smem = base + rows + 16 <= 72 * 1024;
     km_seed_v2_kernel<<<n_segs, 256, base + (in_smem ? rows : 0) + 16, s>>>(sd, scr->P, scr->C, scr->md, d,

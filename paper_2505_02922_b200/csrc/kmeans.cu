@@ -221,6 +221,21 @@ __global__ void km_seed_kernel(const SegDesc* __restrict__ segs, const float* __
 // grid = n_segments, block = 256
 // ---------------------------------------------------------------------------
 constexpr float KS_EPS = 1e-4f;
+constexpr int KS_CKS = 32;                 // cumsum checkpoint stride (elements)
+constexpr int KS_CK = 8192 / KS_CKS + 4;   // checkpoint slots (stride grows with L past 8192)
+// per-phase cycle totals of km_seed_v2 for tools/seed_timing.py (a separate
+// -DWK_SEED_TIMING build; compiled out of the product library)
+#ifdef WK_SEED_TIMING
+__device__ long long g_seed_ts[8192 * 4];
+extern "C" int wk_seed_timing(long long* host, int n) {
+  return cudaMemcpyFromSymbol(host, g_seed_ts, sizeof(long long) * (size_t)n) == cudaSuccess ? 0 : -2;
+}
+#define KS_T0() long long ks_t = clock64()
+#define KS_LAP(i) do { if (threadIdx.x == 0) { const long long n_ = clock64(); ks_acc[i] += n_ - ks_t; ks_t = n_; } } while (0)
+#else
+#define KS_T0() do {} while (0)
+#define KS_LAP(i) do {} while (0)
+#endif
 #ifndef KS_MINB
 #define KS_MINB 4  // 4 segments per SM (64 registers): the seeding is latency-bound
 #endif
@@ -233,17 +248,22 @@ __global__ void __launch_bounds__(256, KS_MINB) km_seed_v2_kernel(const SegDesc*
   extern __shared__ __align__(16) float sm2[];
   float* cent = sm2;          // d floats: current centroid
   float* ccd = sm2 + d;       // max_k floats: lower bounds of ||C[a] - cent||
+  float* ck = ccd + ((max_k + 3) & ~3);  // KS_CK cumsum checkpoints
   const int L = sg.L;
   float* md;
   unsigned short* best;       // the centre each row's md was last set by
+  unsigned short* lst;        // rows the new centre may improve (compacted), global scratch
   const int L4 = (L + 3) & ~3;
   if (in_smem) {
-    md = ccd + ((max_k + 3) & ~3);
+    md = ck + KS_CK;
     best = reinterpret_cast<unsigned short*>(md + L4);
+    lst = reinterpret_cast<unsigned short*>(scratch_all + (size_t)sg.p_off * 2);
   } else {
     md = scratch_all + (size_t)sg.p_off * 2;
     best = reinterpret_cast<unsigned short*>(md + L);
+    lst = best + L;
   }
+  __shared__ int s_nact;
   const float* P = P_all + (size_t)sg.p_off * d;
   const __half* P16 = P16_all ? P16_all + (size_t)sg.p_off * d : nullptr;
   float* C = C_all + (size_t)sg.c_off * d;
@@ -258,6 +278,10 @@ __global__ void __launch_bounds__(256, KS_MINB) km_seed_v2_kernel(const SegDesc*
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   const int h = lane & 1, rsub = lane >> 1;  // 16 rows per warp, 2 lanes per row
   const int nq = d >> 3;                     // 16-byte slices per lane (d % 8 == 0)
+#ifdef WK_SEED_TIMING
+  long long ks_acc[4] = {0, 0, 0, 0};
+#endif
+  KS_T0();
   // rows [0, main_end) of every chunk are class 0; find the first non-main row
   for (int c = 0; c < sg.k; c++) {
     const long long idx = s_idx;
@@ -268,22 +292,53 @@ __global__ void __launch_bounds__(256, KS_MINB) km_seed_v2_kernel(const SegDesc*
     }
     __syncthreads();
     if (c == sg.k - 1) break;
-    // lower bounds of the distances from the earlier centres to the new one
-    for (int a = warp; a < c; a += nwarp) {
-      float dp = 0.f;
-      for (int t = lane; t < d; t += 32) dp = fmaf(C[(size_t)a * d + t], cent[t], dp);
-      dp = warp_sum(dp);
-      if (lane == 0) ccd[a] = sqrtf(fmaxf(0.f, 2.f * (1.f - dp - KS_EPS)));
+    // lower bounds of the distances from the earlier centres to the new one:
+    // one thread per earlier centre, the row's 16-byte slices loaded together
+    // (independent rows in flight instead of a serial warp reduction per row)
+    for (int a = threadIdx.x; a < c; a += blockDim.x) {
+      const float4* cr = reinterpret_cast<const float4*>(C + (size_t)a * d);
+      float dp0 = 0.f, dp1 = 0.f;
+      for (int q0 = 0; q0 < (d >> 2); q0 += 8) {
+        float4 x[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) x[j] = q0 + j < (d >> 2) ? __ldcg(cr + q0 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+          if (q0 + j >= (d >> 2)) break;
+          const float4 y = reinterpret_cast<const float4*>(cent)[q0 + j];
+          dp0 = fmaf(x[j].x, y.x, dp0); dp1 = fmaf(x[j].y, y.y, dp1);
+          dp0 = fmaf(x[j].z, y.z, dp0); dp1 = fmaf(x[j].w, y.w, dp1);
+        }
+      }
+      ccd[a] = sqrtf(fmaxf(0.f, 2.f * (1.f - (dp0 + dp1) - KS_EPS)));
     }
+    if (threadIdx.x == 0) s_nact = 0;
     __syncthreads();
-    for (int base = warp * 16; base < L; base += nwarp * 16) {
-      const int i = base + rsub;
+    KS_LAP(0);
+    // compaction: the rows the new centre may improve (the triangle test
+    // fails); the row pass below then keeps every lane busy on those only
+    for (int i0 = 0; i0 < L; i0 += blockDim.x) {
+      const int i = i0 + threadIdx.x;
       bool act = i < L;
       if (act && c > 0) {
         const float m = md[i];
         const float rh = sqrtf(2.f * (m + KS_EPS)), dl = ccd[best[i]];
         if (dl > rh && 0.5f * (dl - rh) * (dl - rh) >= m + KS_EPS) act = false;
       }
+      const unsigned am = __ballot_sync(0xffffffffu, act);
+      if (am) {
+        int b = 0;
+        if (lane == 0) b = atomicAdd(&s_nact, __popc(am));
+        b = __shfl_sync(0xffffffffu, b, 0);
+        if (act) lst[b + __popc(am & ((1u << lane) - 1u))] = (unsigned short)i;
+      }
+    }
+    __syncthreads();
+    const int nact = s_nact;
+    for (int base = warp * 16; base < nact; base += nwarp * 16) {
+      const int j = base + rsub;
+      bool act = j < nact;
+      const int i = act ? (int)lst[j] : 0;
       if (act && c > 0 && P16) {
         // first pass on the fp16 copy: |dot' - dot| <= 2^-11 + 2 gamma_d for
         // unit rows, so v' - 1e-3 >= md[i] proves min(md, v) == md (no update)
@@ -345,24 +400,22 @@ __global__ void __launch_bounds__(256, KS_MINB) km_seed_v2_kernel(const SegDesc*
       }
     }
     __syncthreads();
+    KS_LAP(1);
     if (threadIdx.x == 0) {
-      // the reference's sequential fp32 cumsum (register-batched, runs at the
-      // FADD latency); pass 1 gives cdf[-1], pass 2 re-walks the same chain up
-      // to the first cdf > threshold (searchsorted 'right')
+      // the reference's sequential fp32 cumsum (clustering.py:35): one pass
+      // with batched loads (the chain runs at the FADD latency) storing the
+      // running sum every KS_CKS elements; searchsorted('right') then
+      // re-walks the same chain from the last checkpoint <= threshold (the
+      // cumsum is non-decreasing: md >= 0 and rounding is monotone)
       float sacc = 0.f;  // 0 + md[0] == md[0] (md >= +0)
-      const bool v4 = in_smem && L == L4;
-      if (v4) {
-        const float4* __restrict__ m4 = reinterpret_cast<const float4*>(md);
-#pragma unroll 4
-        for (int q = 0; q < L4 / 4; q++) {
-          const float4 v = m4[q];
-          sacc = __fadd_rn(sacc, v.x);
-          sacc = __fadd_rn(sacc, v.y);
-          sacc = __fadd_rn(sacc, v.z);
-          sacc = __fadd_rn(sacc, v.w);
-        }
-      } else {
-        for (int i = 0; i < L; i++) sacc = __fadd_rn(sacc, md[i]);
+      const int cks = KS_CKS * ((L + 8191) / 8192);  // checkpoint stride: <= KS_CK checkpoints
+      for (int i0 = 0; i0 < L; i0 += KS_CKS) {
+        if (i0 % cks == 0) ck[i0 / cks] = sacc;
+        float v[KS_CKS];
+#pragma unroll
+        for (int q = 0; q < KS_CKS; q++) v[q] = i0 + q < L ? md[i0 + q] : 0.f;
+#pragma unroll
+        for (int q = 0; q < KS_CKS; q++) sacc = __fadd_rn(sacc, v[q]);  // +0 past L: exact
       }
       long long nidx;
       if (sacc <= 0.0f) {
@@ -370,31 +423,28 @@ __global__ void __launch_bounds__(256, KS_MINB) km_seed_v2_kernel(const SegDesc*
       } else {
         const float u = (float)pcg_next_double(g);
         const float thr = __fmul_rn(u, sacc);
-        float s2 = 0.f;
-        int i = 0;
-        if (v4) {
-          const float4* __restrict__ m4 = reinterpret_cast<const float4*>(md);
-          for (; i < L; i += 4) {
-            const float4 v = m4[i >> 2];
-            float o0, o1, o2, o3;
-            s2 = __fadd_rn(s2, v.x); o0 = s2;
-            s2 = __fadd_rn(s2, v.y); o1 = s2;
-            s2 = __fadd_rn(s2, v.z); o2 = s2;
-            s2 = __fadd_rn(s2, v.w); o3 = s2;
-            if (o3 > thr) { i += o0 > thr ? 0 : (o1 > thr ? 1 : (o2 > thr ? 2 : 3)); break; }
-          }
-        } else {
-          for (; i < L; i++) {
-            s2 = __fadd_rn(s2, md[i]);
-            if (s2 > thr) break;
-          }
+        int lo = 0, hi = (L - 1) / cks;  // last checkpoint <= thr (ck[0] = 0 <= thr)
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (ck[mid] <= thr) lo = mid; else hi = mid - 1;
+        }
+        float s2 = ck[lo];
+        int i = lo * cks;
+        for (; i < L; i++) {
+          s2 = __fadd_rn(s2, md[i]);
+          if (s2 > thr) break;
         }
         nidx = i > L - 1 ? L - 1 : i;
       }
       s_idx = nidx;
     }
     __syncthreads();
+    KS_LAP(2);
   }
+#ifdef WK_SEED_TIMING
+  if (threadIdx.x == 0)
+    for (int i = 0; i < 3; i++) g_seed_ts[blockIdx.x * 4 + i] = ks_acc[i];
+#endif
 }
 
 // ---------------------------------------------------------------------------
