@@ -4,6 +4,8 @@
 // evaluation orders are reproduced with round-to-nearest intrinsics (see
 // common.cuh).  All segments of all (request, kv-head) units of a layer are
 // processed by one launch per phase.
+#include <type_traits>
+
 #include "common.cuh"
 #include "wavekv_internal.h"
 
@@ -280,6 +282,7 @@ __global__ void __launch_bounds__(256, KS_MINB) km_seed_v2_kernel(const SegDesc*
   const int nq = d >> 3;                     // 16-byte slices per lane (d % 8 == 0)
 #ifdef WK_SEED_TIMING
   long long ks_acc[4] = {0, 0, 0, 0};
+  long long ks_nact = 0;
 #endif
   KS_T0();
   // rows [0, main_end) of every chunk are class 0; find the first non-main row
@@ -334,7 +337,11 @@ __global__ void __launch_bounds__(256, KS_MINB) km_seed_v2_kernel(const SegDesc*
       }
     }
     __syncthreads();
+    KS_LAP(3);
     const int nact = s_nact;
+#ifdef WK_SEED_TIMING
+    if (threadIdx.x == 0) ks_nact += nact;
+#endif
     for (int base = warp * 16; base < nact; base += nwarp * 16) {
       const int j = base + rsub;
       bool act = j < nact;
@@ -409,14 +416,33 @@ __global__ void __launch_bounds__(256, KS_MINB) km_seed_v2_kernel(const SegDesc*
       // cumsum is non-decreasing: md >= 0 and rounding is monotone)
       float sacc = 0.f;  // 0 + md[0] == md[0] (md >= +0)
       const int cks = KS_CKS * ((L + 8191) / 8192);  // checkpoint stride: <= KS_CK checkpoints
-      for (int i0 = 0; i0 < L; i0 += KS_CKS) {
-        if (i0 % cks == 0) ck[i0 / cks] = sacc;
-        float v[KS_CKS];
+      const int nfull = (L / KS_CKS) * KS_CKS;
+      // full blocks: unpredicated 16-byte loads issued before the FADD chain
+      // (shared or global md; the serial thread competes for issue slots)
+      auto blocks = [&](const float* mdp, auto vec) {
+        int ci = 0;
+        for (int i0 = 0; i0 < nfull; i0 += KS_CKS) {
+          if (i0 == ci * cks) { ck[ci] = sacc; ci++; }
+          float v[KS_CKS];
+          if (vec) {
 #pragma unroll
-        for (int q = 0; q < KS_CKS; q++) v[q] = i0 + q < L ? md[i0 + q] : 0.f;
+            for (int q = 0; q < KS_CKS / 4; q++) {
+              const float4 x = reinterpret_cast<const float4*>(mdp + i0)[q];
+              v[4 * q] = x.x; v[4 * q + 1] = x.y; v[4 * q + 2] = x.z; v[4 * q + 3] = x.w;
+            }
+          } else {
 #pragma unroll
-        for (int q = 0; q < KS_CKS; q++) sacc = __fadd_rn(sacc, v[q]);  // +0 past L: exact
-      }
+            for (int q = 0; q < KS_CKS; q++) v[q] = mdp[i0 + q];
+          }
+#pragma unroll
+          for (int q = 0; q < KS_CKS; q++) sacc = __fadd_rn(sacc, v[q]);
+        }
+        if (nfull < L && nfull == ci * cks) ck[ci] = sacc;
+        for (int i = nfull; i < L; i++) sacc = __fadd_rn(sacc, mdp[i]);
+      };
+      // md in shared memory is 16-byte aligned (d, K4, KS_CK multiples of 4)
+      if (in_smem) blocks(ck + KS_CK, std::true_type{});
+      else blocks(md, std::false_type{});
       long long nidx;
       if (sacc <= 0.0f) {
         nidx = pcg_integers(g, L);
@@ -443,7 +469,8 @@ __global__ void __launch_bounds__(256, KS_MINB) km_seed_v2_kernel(const SegDesc*
   }
 #ifdef WK_SEED_TIMING
   if (threadIdx.x == 0)
-    for (int i = 0; i < 3; i++) g_seed_ts[blockIdx.x * 4 + i] = ks_acc[i];
+    for (int i = 0; i < 4; i++) g_seed_ts[blockIdx.x * 4 + i] = ks_acc[i];
+  if (threadIdx.x == 0) g_seed_ts[8192 * 4 - 1 - blockIdx.x] = ks_nact;
 #endif
 }
 
