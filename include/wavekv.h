@@ -103,8 +103,11 @@ typedef struct wk_step_view {
   float* cov;         /* [U, G] StepMetrics.denominator_coverage                */
   int* status;        /* device status word                                     */
   int32_t r_cap, e_cap, ru_cap, eu_cap;
-  int32_t* rtok_row;  /* [U, rt_cap] store row of every retrieved token (union)  */
-  uint8_t* rtok_mask; /* [U, rt_cap] head mask of that token                     */
+  int32_t* rtok_row;  /* [U, rt_cap] every retrieved token of the unit's union:
+                         store row | head mask << 24 (fast path, bf16 store:
+                         written by the zone planning instead of `pieces` and
+                         read by the attention; NULL: pieces)                 */
+  uint8_t* rtok_mask; /* unused (NULL)                                           */
   int32_t* sel_done;  /* [U] zero-initialised counter (last-CTA handoff)        */
   int32_t rt_cap, pad_;
   float* eu_x;        /* [U, eu_cap, G] estimation-row scores (-inf: head not in zone) */
@@ -138,7 +141,9 @@ typedef struct wk_zone_params {
   int32_t denominator_eq2;       /* EngineConfig.denominator_mode              */
   int32_t score_mode;            /* 1: the C32 scan accumulated in fp64 (the
                                     error bound select_v6 uses)                */
-  int32_t pad_;
+  int32_t piece_rows;            /* rows per retrieval piece, <= the attention
+                                    chunk rows (16 for bf16 stores; 0: 16 for
+                                    G <= 4, 8 for G <= 8, valid for both)      */
 } wk_zone_params;
 
 /* Device block cache (the wave buffer), one state machine per cache unit
@@ -187,7 +192,8 @@ typedef struct wk_cache2_view {
   int32_t* ids; int32_t* n_ids; uint8_t* snapshot; int32_t* scratch;
   const int32_t* m_live;
   int64_t m_cap, slot_cap, lru_cap, ids_cap;
-  int32_t block_bytes, token_bytes, block_tokens, pad_;
+  int32_t block_bytes, token_bytes, block_tokens;
+  int32_t piece_rows; /* rows per attention piece (wk_zone_params.piece_rows)  */
 } wk_cache2_view;
 
 int wk_version(void);

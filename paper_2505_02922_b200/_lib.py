@@ -70,14 +70,14 @@ class Cache2ViewC(ctypes.Structure):
                                   "occupied", "counters", "ids", "n_ids", "snapshot", "scratch",
                                   "m_live")] + [
         ("m_cap", _I64), ("slot_cap", _I64), ("lru_cap", _I64), ("ids_cap", _I64),
-        ("block_bytes", _I32), ("token_bytes", _I32), ("block_tokens", _I32), ("pad_", _I32)]
+        ("block_bytes", _I32), ("token_bytes", _I32), ("block_tokens", _I32), ("piece_rows", _I32)]
 
 
 class ZoneParamsC(ctypes.Structure):
     _fields_ = [("G", _I32), ("d", _I32), ("blas_threads", _I32),
                 ("retrieval_fraction", ctypes.c_double), ("estimation_fraction", ctypes.c_double),
                 ("tail_denominator_only", _I32), ("denominator_eq2", _I32), ("score_mode", _I32),
-                ("pad_", _I32)]
+                ("piece_rows", _I32)]
 
 
 _lib = None

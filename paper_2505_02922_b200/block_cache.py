@@ -273,7 +273,8 @@ class OffloadCache:
                                      self.first, self.lru, self.lru_tmp, self.lru_n, self.freel, self.free_n,
                                      self.next_slot, self.capacity, self.occupied, self.counters, self.ids,
                                      self.n_ids, self.snapshot, self.scratch, layer.m_dev)),
-            m_cap, self.list_cap, self.lru_cap, self.ids_cap, cfg.block_size_bytes, 2 * d * 4, self.bt, 0)
+            m_cap, self.list_cap, self.lru_cap, self.ids_cap, cfg.block_size_bytes, 2 * d * 4, self.bt,
+            layer.piece_rows)
 
     def register_new(self, units=None):
         """Register clusters added since the last call; capacity grows

@@ -40,7 +40,13 @@ size_t attend_v4_smem();
 template <typename T, int DPL, int HS>
 int attend_v4_warps();
 template <bool FULL, int DL>
-__global__ void att4_merge_kernel(SteadyView, StepView, AttnParams, const int32_t*, int, int, int);
+__global__ void att4_merge_kernel(SteadyView, StepView, AttnParams, const int32_t*, int, int, int, int);
+template <int D, int HS, bool FULL, bool OFF, bool ROWS>
+__global__ void attend_v5_kernel(IndexView, SteadyView, StepView, AttnParams, const int32_t*, int);
+template <int D, int HS>
+size_t attend_v5_smem();
+template <int D, int HS>
+int attend_v5_warps();
 __global__ void km_assign_tc5_kernel(const SegDesc*, const float*, const float*, int32_t*, const __nv_bfloat16*);
 __global__ void km_pack_c5_kernel(const SegDesc*, const float*, __nv_bfloat16*);
 constexpr int KS_CK = 8192 / 32 + 4;  // km_seed_v2 cumsum checkpoint slots (kmeans.cu)
@@ -219,7 +225,30 @@ static int launch_attend_v4(const IndexView& ix, const SteadyView& st, const Ste
     return WK_ECUDA;
   const int RG = HS == 4 ? 16 : 8;  // Att4Cfg::RG
   const cudaError_t e = launch_ex(att4_merge_kernel<FULL, DPL / 2>, dim3(U * p.G), dim3(128), 0, s, 1, st, sv, p,
-                                  n_store, U, P * warps, RG);
+                                  n_store, U, P * warps, RG, 0);
+  return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? 0 : WK_ECUDA;
+}
+
+// bf16 stores: attend_v5 (q.k and p.v on the tensor cores, chunk rows 16); the
+// in-HBM path reads select_v6's retrieved-row list (ROWS), offload the pieces
+template <int D, int HS, bool FULL, bool OFF, bool ROWS>
+static int launch_attend_v5(const IndexView& ix, const SteadyView& st, const StepView& sv, const AttnParams& p,
+                            const int32_t* n_store, int U, int P, cudaStream_t s) {
+  if (U > 1024) return WK_ECONFIG;
+  const size_t sm = attend_v5_smem<D, HS>();
+  static PerDevice cfg;
+  if (cfg.needed()) {
+    if (cudaFuncSetAttribute(attend_v5_kernel<D, HS, FULL, OFF, ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sm) != cudaSuccess)
+      return WK_ECUDA;
+    cfg.mark();
+  }
+  const int warps = attend_v5_warps<D, HS>();
+  if (launch_ex(attend_v5_kernel<D, HS, FULL, OFF, ROWS>, dim3(P), dim3(warps * 32), sm, s, 1, ix, st, sv, p,
+                n_store, U) != cudaSuccess || cudaGetLastError() != cudaSuccess)
+    return WK_ECUDA;
+  const cudaError_t e = launch_ex(att4_merge_kernel<FULL, D / 32>, dim3(U * p.G), dim3(128), 0, s, 1, st, sv, p,
+                                  n_store, U, P * warps, 16, ROWS ? 1 : 0);
   return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? 0 : WK_ECUDA;
 }
 
@@ -228,6 +257,15 @@ static int dispatch_attend_v4(const IndexView& ix, const SteadyView& st, const S
                               const int32_t* n_store, int U, int P, cudaStream_t s) {
   const int hs = head_slots(p.G);
   const bool off = !FULL && sv.pstride == 4;
+  if (sizeof(T) == 2 && (FULL || off || sv.rtok_row)) {
+#define WK_ATT5(D, HS)                                                                           \
+  (FULL ? launch_attend_v5<D, HS, FULL, false, false>(ix, st, sv, p, n_store, U, P, s)           \
+        : (off ? launch_attend_v5<D, HS, FULL, !FULL, false>(ix, st, sv, p, n_store, U, P, s)    \
+               : launch_attend_v5<D, HS, FULL, false, !FULL>(ix, st, sv, p, n_store, U, P, s)))
+    if (p.d == 128) return hs == 4 ? WK_ATT5(128, 4) : WK_ATT5(128, 8);
+    return hs == 4 ? WK_ATT5(64, 4) : WK_ATT5(64, 8);
+#undef WK_ATT5
+  }
 #define WK_ATT4(DPL, HS)                                                                  \
   (off ? launch_attend_v4<T, DPL, HS, FULL, !FULL>(ix, st, sv, p, n_store, U, P, s)      \
        : launch_attend_v4<T, DPL, HS, FULL, false>(ix, st, sv, p, n_store, U, P, s))
@@ -349,7 +387,9 @@ static int score_topk_impl(const wk_index_view* ix, const wk_step_view* sv, cons
     p.need_allc = zp->denominator_eq2;
     p.score_fp64 = 1;
     p.score_mode = 1;
-    p.piece_rows = head_slots(zp->G) == 4 ? 16 : 8;  // attend_v4 chunk rows (Att4Cfg::RG)
+    // retrieval piece rows: the attention chunk rows (attend_v5: 16; attend_v4:
+    // 16 for G <= 4, 8 for G <= 8); zp->piece_rows = 0 -> the attend_v4 rule
+    p.piece_rows = zp->piece_rows > 0 ? zp->piece_rows : (head_slots(zp->G) == 4 ? 16 : 8);
     p.k_new = nullptr; p.v_new = nullptr; p.store_bf16 = 0;
     if (app && app->on) { p.k_new = app->k; p.v_new = app->v; p.st = app->st; p.store_bf16 = app->bf16; }
     return launch_select_v6(*ix, *sv, p, U, m_max, s);

@@ -517,7 +517,7 @@ __global__ void __launch_bounds__(Att4Cfg<T, DPL, HS>::WARPS * 32, 1) attend_v4_
 template <bool FULL, int DL>
 __global__ void __launch_bounds__(128) att4_merge_kernel(SteadyView st, StepView sv, AttnParams p,
                                                           const int32_t* __restrict__ n_store, int U, int Wtot,
-                                                          int RG) {
+                                                          int RG, int rows_mode) {
   // one CTA (4 warps) per (unit, head): the partial records are split over
   // the warps so ~4x more loads are in flight than with one warp per head
   pdl_wait();
@@ -534,7 +534,11 @@ __global__ void __launch_bounds__(128) att4_merge_kernel(SteadyView st, StepView
     const int n_st = st.n[u];
     c0 = (n_st + RG - 1) / RG;
     if (FULL) { c1 = (n_store[u] + RG - 1) / RG; c2 = 0; }
-    else { c1 = sv.cnt[u * 4 + 3]; c2 = (sv.cnt[u * 4 + 2] + RG - 1) / RG; }
+    else {
+      // retrieval chunks: the pieces, or (attend_v5 row mode) RG retrieved rows each
+      c1 = rows_mode ? (sv.cnt[u * 4 + 1] + RG - 1) / RG : sv.cnt[u * 4 + 3];
+      c2 = (sv.cnt[u * 4 + 2] + RG - 1) / RG;
+    }
   }
   const long long ub = sv.woff[u];
   const long long kb[4] = {ub, ub + c0, ub + c0 + c1, ub + c0 + c1 + c2};
@@ -730,9 +734,9 @@ WK_INST_ATT4(float, 8, 4)
 WK_INST_ATT4(float, 8, 8)
 WK_INST_ATT4(float, 4, 4)
 WK_INST_ATT4(float, 4, 8)
-template __global__ void att4_merge_kernel<false, 4>(SteadyView, StepView, AttnParams, const int32_t*, int, int, int);
-template __global__ void att4_merge_kernel<true, 4>(SteadyView, StepView, AttnParams, const int32_t*, int, int, int);
-template __global__ void att4_merge_kernel<false, 2>(SteadyView, StepView, AttnParams, const int32_t*, int, int, int);
-template __global__ void att4_merge_kernel<true, 2>(SteadyView, StepView, AttnParams, const int32_t*, int, int, int);
+template __global__ void att4_merge_kernel<false, 4>(SteadyView, StepView, AttnParams, const int32_t*, int, int, int, int);
+template __global__ void att4_merge_kernel<true, 4>(SteadyView, StepView, AttnParams, const int32_t*, int, int, int, int);
+template __global__ void att4_merge_kernel<false, 2>(SteadyView, StepView, AttnParams, const int32_t*, int, int, int, int);
+template __global__ void att4_merge_kernel<true, 2>(SteadyView, StepView, AttnParams, const int32_t*, int, int, int, int);
 
 }  // namespace wk

@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(C2_T) cache2_step_kernel(Cache2View cv, IndexV
   // ---- 8. attention pieces of the retrieval union (rank order) ----
   //   hit:  runs of consecutive arena slots, <= PR rows  (flag 1: arena)
   //   miss: host store rows, <= PR rows; admitted -> flag 2 (write-through)
-  const int PR = G <= 4 ? 16 : 8;  // attend_v4 chunk rows (Att4Cfg::RG)
+  const int PR = cv.piece_rows > 0 ? cv.piece_rows : (G <= 4 ? 16 : 8);  // attention chunk rows
   const int bt = cv.block_tokens;
   const int* csize = ix.cl_size + (size_t)u * ix.m_cap;
   const int* coff = ix.cl_off + (size_t)u * ix.m_cap;

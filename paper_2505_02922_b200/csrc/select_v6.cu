@@ -288,7 +288,10 @@ __device__ void s6_union_cl(const IndexView& ix, const StepView& sv, const SelPa
   }
   __syncthreads();
   const int n_ru = sm.wsum[0][0], n_rt = sm.wsum[1][0], n_pc = sm.wsum[2][0], n_eu = sm.wsum[3][0];
-  const bool fits = n_pc <= sv.pc_cap && n_eu <= sv.eu_cap && n_ru <= sv.ru_cap;
+  // row mode (sv.rtok_row set, attend_v5): every retrieved token's store row +
+  // head mask instead of the pieces
+  const bool rows_mode = sv.rtok_row != nullptr;
+  const bool fits = (rows_mode ? n_rt <= sv.rt_cap : n_pc <= sv.pc_cap) && n_eu <= sv.eu_cap && n_ru <= sv.ru_cap;
   if (g == 0 && t == 0) {
     if (!fits) set_status(sv.status, kErrUnion);
     sv.cnt[u * 4 + 0] = fits ? n_ru : 0;
@@ -298,6 +301,7 @@ __device__ void s6_union_cl(const IndexView& ix, const StepView& sv, const SelPa
   }
   // ---- pass 2: emit ----
   int2* pcs = reinterpret_cast<int2*>(sv.pieces) + (size_t)u * sv.pc_cap;
+  int32_t* rows = rows_mode ? sv.rtok_row + (size_t)u * sv.rt_cap : nullptr;
   int32_t* ru = sv.ru_ids + (size_t)u * sv.ru_cap;
   uint8_t* rmk = sv.ru_mask + (size_t)u * sv.ru_cap;
   int32_t* eu = sv.eu_ids + (size_t)u * sv.eu_cap;
@@ -333,7 +337,29 @@ __device__ void s6_union_cl(const IndexView& ix, const StepView& sv, const SelPa
       load_words(w - tw0, rw, ew, ur, ue);
       const int c = zb_cluster(w, lane);
       const int ci = c - (tw0 << 5);
-      if (ur) {
+      if (ur && rows_mode) {
+        const bool in = (ur >> lane) & 1u;
+        const int sz = in ? csz[ci] : 0;
+        int x = sz;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, x, off);
+          if (lane >= off) x += y;
+        }
+        if (in) {
+          int mk = 0;
+#pragma unroll
+          for (int h = 0; h < GM; h++) mk |= ((rw[h] >> lane) & 1u) << h;
+          const int ir = o[0] + __popc(ur & lt);
+          ru[ir] = c;
+          rmk[ir] = (uint8_t)mk;
+          const int r0 = cof[ci];
+          int32_t* dst = rows + o[1] + x - sz;
+          for (int j = 0; j < sz; j++) dst[j] = (r0 + j) | (mk << 24);
+        }
+        o[0] += __popc(ur);
+        o[1] += __shfl_sync(0xffffffffu, x, 31);
+      } else if (ur) {
         const bool in = (ur >> lane) & 1u;
         const int sz = in ? csz[ci] : 0;
         const int np = (sz + PR - 1) >> PRS;

@@ -109,11 +109,13 @@ class WaveLayer:
         # fast path (score_v5 / select_v6 / attend_v4): d in {64, 128}
         self.fast = d in (64, 128)
         hs = 4 if G <= 4 else 8
-        self.piece_rows = 16 if hs == 4 else 8  # attend_v4 chunk rows
+        # retrieval piece rows = the attention chunk rows: attend_v5 (bf16 stores,
+        # tensor cores) 16; attend_v4 (fp32 stores) 16 for G <= 4, 8 for G <= 8
+        self.piece_rows = 16 if (hs == 4 or store_dtype == torch.bfloat16) else 8
         if self.fast:
             sms = torch.cuda.get_device_properties(self.dev).multi_processor_count
             self.S = splits or max(1, min(sms, 4 * U))  # persistent attention grid: 1 CTA / SM
-            self.attn_warps = 8 if hs == 8 else (12 if (store_dtype == torch.bfloat16 or d == 64) else 6)
+            self.attn_warps = 12  # upper bound of the attention kernels' warps per CTA (partial slots)
         else:
             self.S = splits or max(1, min(64, -(-2048 // U)))
         # the C32 scan accumulates in fp64 (the estimation logits need ~fp32 accuracy)
@@ -164,8 +166,14 @@ class WaveLayer:
         self.eu_mask = torch.zeros((U, self.eu_cap), dtype=torch.uint8, device=dev)
         self.cnt = torch.zeros((U, 4), dtype=i32, device=dev)
         if self.fast:
-            self.zmask = self.ru_pre = self.rtok_row = self.rtok_mask = None
-            self.rt_cap = 0
+            self.zmask = self.ru_pre = self.rtok_mask = None
+            # attend_v5 row mode (bf16 store in HBM): every retrieved token's
+            # store row | head mask << 24, written by the zone planning
+            self.rows_mode = store_dtype == torch.bfloat16 and not offload
+            self.rt_cap = self.s_cap if self.rows_mode else 0
+            if self.rows_mode and self.s_cap >= (1 << 24):
+                raise ConfigError("row mode packs store rows in 24 bits")
+            self.rtok_row = (torch.zeros((U, self.rt_cap), dtype=i32, device=dev) if self.rows_mode else None)
             self.w_cap = self.m_cap // 32
             self.rbits = torch.zeros((U, G, self.w_cap), dtype=i32, device=dev)
             self.ebits = torch.zeros((U, G, self.w_cap), dtype=i32, device=dev)
@@ -178,9 +186,9 @@ class WaveLayer:
         else:
             self.zmask = torch.zeros((U, self.m_cap), dtype=i32, device=dev)
             self.ru_pre = torch.zeros((U, self.ru_cap + 1), dtype=i32, device=dev)
-            self.rt_cap = self.s_cap
-            self.rtok_row = torch.zeros((U, self.rt_cap), dtype=i32, device=dev)
-            self.rtok_mask = torch.zeros((U, self.rt_cap), dtype=torch.uint8, device=dev)
+            self.rows_mode = False
+            self.rt_cap = 0
+            self.rtok_row = self.rtok_mask = None
             self.w_cap = self.pc_cap = 0
             self.rbits = self.ebits = self.pieces = self.woff = None
         self.sel_done = torch.zeros(U, dtype=i32, device=dev)
@@ -202,7 +210,8 @@ class WaveLayer:
         self._q = None
         self._zp = _lib.ZoneParamsC(G, d, self.blas_threads, ic.retrieval_fraction,
                                     ic.estimation_fraction, int(ic.tail_mode == "denominator_only"),
-                                    int(cfg.denominator_mode == "eq2"), self.score_mode, 0)
+                                    int(cfg.denominator_mode == "eq2"), self.score_mode,
+                                    self.piece_rows if self.fast else 0)
         self._ixv = _lib.IndexViewC(
             _ptr(self.store_k), _ptr(self.store_v), _ptr(self.store_tok), _ptr(self.cl_off),
             _ptr(self.cl_size), _ptr(self.C64), _ptr(self.C32), _ptr(self.Cnorm), _ptr(self.VS32),
@@ -250,7 +259,7 @@ class WaveLayer:
             None, _ptr(sl(self.eu_ids)), _ptr(sl(self.eu_mask)), _ptr(sl(self.cnt)),
             _ptr(sl(self.tail)), _ptr(grp["part"]), _ptr(sl(self.out)), _ptr(sl(self.logden)), _ptr(sl(self.cov)),
             _ptr(self.status), self.r_cap, self.e_cap, self.ru_cap, self.eu_cap,
-            None, None, _ptr(sl(self.sel_done)), 0, 0,
+            _ptr(sl(self.rtok_row)), None, _ptr(sl(self.sel_done)), self.rt_cap, 0,
             _ptr(sl(self.eu_x)), _ptr(sl(self.eu_sz)), _ptr(sl(self.rbits)), _ptr(sl(self.ebits)), _ptr(sl(self.pieces)),
             _ptr(grp["woff"]), self.w_cap, self.pc_cap, None, None, None, None, 0, 0, 0, 2,
             None, _ptr(sl(self.xscr)), _ptr(self.xcount))

@@ -141,9 +141,11 @@ def test_full_attention_matches_fp64():
 
 @pytest.mark.parametrize("split", [2, 4])
 def test_split_pipeline_matches_single_launch(split):
-    """split > 1 (per-group centroid scans on the main stream, the groups'
-    zone planning on a side stream overlapping the next group's scan, one
-    attention over all units) gives bit-identical zones and outputs."""
+    """split > 1 (per-group centroid scans, the groups' zone planning and
+    attention on side streams overlapping the next group's scan) gives
+    bit-identical zones; outputs agree to fp32 round-off (each group's
+    attention partitions its chunks over the persistent warps differently, so
+    the partial sums are added in a different order)."""
     from paper_2505_02922_b200 import EngineConfig, WaveLayer
     rng = np.random.default_rng(21)
     U, Gh, d, n, steps = 8, 4, 128, 3000, 5
@@ -165,7 +167,8 @@ def test_split_pipeline_matches_single_launch(split):
             lay.check_status()
         assert torch.equal(lays[0].rlist, lays[1].rlist)
         assert torch.equal(lays[0].cnt, lays[1].cnt)
-        assert torch.equal(outs[0], outs[1]), t
+        rel = float((outs[0] - outs[1]).norm() / outs[0].norm())
+        assert rel <= 1e-6, (t, rel)
 
 
 def test_launch_step_out_argument():

@@ -34,9 +34,9 @@ def main():
             continue
         if r[0]:
             cur = (path, r[0], r[1])
+            ci = hdr.index(col) if (col and col in hdr) else 4
             try:
-                ci = hdr.index(col) if (col and col in hdr) else 4
-            v = int(float(r[ci] or 0))
+                v = int(float(r[ci] or 0))
             except ValueError:
                 v = 0
             agg[cur] = agg.get(cur, 0) + v
