@@ -17,7 +17,7 @@ OBJ = os.path.join(HERE, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]
-UNITS = ("kmeans.cu", "select_v6.cu", "attend_v4.cu", "attend_v5.cu", "tu_decode.cu", "tu_abi.cu", "api.cu")
+UNITS = ("kmeans.cu", "select_v6.cu", "attend_v4.cu", "attend_v5.cu", "attend_v6.cu", "tu_decode.cu", "tu_abi.cu", "api.cu")
 
 
 def sources():

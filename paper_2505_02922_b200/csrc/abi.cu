@@ -1,8 +1,13 @@
 // abi.cu -- extern "C" entry points (include/wavekv.h) launching the
 // sm_100a kernels on the caller's stream.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <math.h>
+#include <string.h>
+
+#include <mutex>
 
 #include "decode_internal.h"
 #include "cache_internal.h"
@@ -47,6 +52,17 @@ template <int D, int HS>
 size_t attend_v5_smem();
 template <int D, int HS>
 int attend_v5_warps();
+template <int D, int HS, bool FULL, bool OFF, bool ROWS>
+__global__ void attend_v6_kernel(IndexView, SteadyView, StepView, AttnParams, const int32_t*, int,
+                                 const __grid_constant__ CUtensorMap);
+template <int D, int HS>
+size_t attend_v6_smem();
+template <int D, int HS>
+int attend_v6_warps();
+template <int D, int HS>
+int attend_v6_consumers();
+template <bool FULL, int DL>
+__global__ void att6_merge_kernel(SteadyView, StepView, AttnParams, const int32_t*, int, int, int, int);
 __global__ void km_assign_tc5_kernel(const SegDesc*, const float*, const float*, int32_t*, const __nv_bfloat16*);
 __global__ void km_pack_c5_kernel(const SegDesc*, const float*, __nv_bfloat16*);
 constexpr int KS_CK = 8192 / 32 + 4;  // km_seed_v2 cumsum checkpoint slots (kmeans.cu)
@@ -252,26 +268,102 @@ static int launch_attend_v5(const IndexView& ix, const SteadyView& st, const Ste
   return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? 0 : WK_ECUDA;
 }
 
+// 2-D tensor map of the fp32 value sums [rows, d] (box {d, 1}: the gather4 row
+// source of attend_v6), cached per (pointer, rows, d)
+static int vs_tensor_map(const float* ptr, long long rows, int d, CUtensorMap* out) {
+  static std::mutex mu;
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  struct Entry { const float* ptr; long long rows; int d, dev; CUtensorMap tm; };
+  static Entry cache[64];
+  static int n = 0, next = 0;
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lk(mu);
+  for (int i = 0; i < n; i++)
+    if (cache[i].ptr == ptr && cache[i].rows == rows && cache[i].d == d && cache[i].dev == dev) {
+      *out = cache[i].tm;
+      return 0;
+    }
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !encode)
+      return WK_ECUDA;
+  }
+  CUtensorMap tm;
+  const cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)d * 4};
+  const cuuint32_t box[2] = {(cuuint32_t)d, 1};
+  const cuuint32_t estr[2] = {1, 1};
+  if (encode(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)ptr, dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return WK_ECUDA;
+  Entry& e = cache[next];
+  e = {ptr, rows, d, dev, tm};
+  next = (next + 1) % 64;
+  if (n < 64) n++;
+  *out = tm;
+  return 0;
+}
+
+// bf16 stores: attend_v6 (warp-specialised producer / consumer pipeline,
+// tensor-core exact zones) + att6_merge
+template <int D, int HS, bool FULL, bool OFF, bool ROWS>
+static int launch_attend_v6(const IndexView& ix, const SteadyView& st, const StepView& sv, const AttnParams& p,
+                            const int32_t* n_store, int U, int P, cudaStream_t s) {
+  if (U > 1024) return WK_ECONFIG;
+  CUtensorMap tm;
+  memset(&tm, 0, sizeof(tm));
+  if (!FULL && ix.VS32) {
+    const int rc = vs_tensor_map(ix.VS32, (long long)U * ix.m_cap, D, &tm);
+    if (rc) return rc;
+  }
+  const size_t sm = attend_v6_smem<D, HS>();
+  static PerDevice cfg;
+  if (cfg.needed()) {
+    if (cudaFuncSetAttribute(attend_v6_kernel<D, HS, FULL, OFF, ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sm) != cudaSuccess)
+      return WK_ECUDA;
+    cfg.mark();
+  }
+  const int warps = attend_v6_warps<D, HS>(), nc = attend_v6_consumers<D, HS>();
+  if (launch_ex(attend_v6_kernel<D, HS, FULL, OFF, ROWS>, dim3(P), dim3(warps * 32), sm, s, 1, ix, st, sv, p,
+                n_store, U, tm) != cudaSuccess || cudaGetLastError() != cudaSuccess)
+    return WK_ECUDA;
+  const cudaError_t e = launch_ex(att6_merge_kernel<FULL, D / 32>, dim3(U * p.G), dim3(128), 0, s, 1, st, sv, p,
+                                  n_store, U, P, nc, ROWS ? 1 : 0);
+  return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? 0 : WK_ECUDA;
+}
+
 template <typename T, bool FULL>
 static int dispatch_attend_v4(const IndexView& ix, const SteadyView& st, const StepView& sv, const AttnParams& p,
                               const int32_t* n_store, int U, int P, cudaStream_t s) {
   const int hs = head_slots(p.G);
   const bool off = !FULL && sv.pstride == 4;
-  if (sizeof(T) == 2 && (FULL || off || sv.rtok_row)) {
+  if constexpr (sizeof(T) == 2) {
+    // bf16 rows are swizzled for attend_v5; the in-HBM path needs the row list
+    if (!(FULL || off || sv.rtok_row)) return WK_ECONFIG;
+#ifdef WK_ATTN_V5  // A/B experiments only: the per-warp-ring kernel
+#define WK_LAUNCH5 launch_attend_v5
+#else
+#define WK_LAUNCH5 launch_attend_v6
+#endif
 #define WK_ATT5(D, HS)                                                                           \
-  (FULL ? launch_attend_v5<D, HS, FULL, false, false>(ix, st, sv, p, n_store, U, P, s)           \
-        : (off ? launch_attend_v5<D, HS, FULL, !FULL, false>(ix, st, sv, p, n_store, U, P, s)    \
-               : launch_attend_v5<D, HS, FULL, false, !FULL>(ix, st, sv, p, n_store, U, P, s)))
+  (FULL ? WK_LAUNCH5<D, HS, FULL, false, false>(ix, st, sv, p, n_store, U, P, s)                 \
+        : (off ? WK_LAUNCH5<D, HS, FULL, !FULL, false>(ix, st, sv, p, n_store, U, P, s)          \
+               : WK_LAUNCH5<D, HS, FULL, false, !FULL>(ix, st, sv, p, n_store, U, P, s)))
     if (p.d == 128) return hs == 4 ? WK_ATT5(128, 4) : WK_ATT5(128, 8);
     return hs == 4 ? WK_ATT5(64, 4) : WK_ATT5(64, 8);
 #undef WK_ATT5
-  }
+#undef WK_LAUNCH5
+  } else {
 #define WK_ATT4(DPL, HS)                                                                  \
   (off ? launch_attend_v4<T, DPL, HS, FULL, !FULL>(ix, st, sv, p, n_store, U, P, s)      \
        : launch_attend_v4<T, DPL, HS, FULL, false>(ix, st, sv, p, n_store, U, P, s))
-  if (p.d == 128) return hs == 4 ? WK_ATT4(8, 4) : WK_ATT4(8, 8);
-  return hs == 4 ? WK_ATT4(4, 4) : WK_ATT4(4, 8);
+    if (p.d == 128) return hs == 4 ? WK_ATT4(8, 4) : WK_ATT4(8, 8);
+    return hs == 4 ? WK_ATT4(4, 4) : WK_ATT4(4, 8);
 #undef WK_ATT4
+  }
 }
 
 extern "C" {

@@ -1,5 +1,7 @@
 // attend_v4.cu -- fused tripartite decode attention (attention.py:67-148,
-// engine.py:150-172), persistent flat schedule.
+// engine.py:150-172), persistent flat schedule, CUDA cores: the fp32-store
+// path (HeadEngine's exact drop-in).  bf16 stores run attend_v5.cu (tensor
+// cores) and share att4_merge_kernel below.
 //
 // Work is a flat list of CHUNKS over all units: per unit u, first the steady
 // zone (sinks + decode buffer, engine.py:87-96) in runs of RG contiguous rows,
@@ -726,10 +728,6 @@ int attend_v4_warps() { return Att4Cfg<T, DPL, HS>::WARPS; }
   template size_t attend_v4_smem<T, DL, HS, false>();                                                              \
   template size_t attend_v4_smem<T, DL, HS, true>();                                                               \
   template int attend_v4_warps<T, DL, HS>();
-WK_INST_ATT4(__nv_bfloat16, 8, 4)
-WK_INST_ATT4(__nv_bfloat16, 8, 8)
-WK_INST_ATT4(__nv_bfloat16, 4, 4)
-WK_INST_ATT4(__nv_bfloat16, 4, 8)
 WK_INST_ATT4(float, 8, 4)
 WK_INST_ATT4(float, 8, 8)
 WK_INST_ATT4(float, 4, 4)

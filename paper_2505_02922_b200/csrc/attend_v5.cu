@@ -34,11 +34,17 @@
 // mode: select_v6 wrote every retrieved token's store row + head mask, so the
 // clusters' runs are packed into full chunks; offload: the cache's pieces),
 // the estimation rows 16 at a time -- split evenly over a persistent grid of
-// P CTAs x WARPS warps.  Each warp streams its range through a 2-stage ring:
-// K/V rows arrive by per-row 1-D bulk copies (TMA) into rows padded to
-// 2d + 16 bytes, so the ldmatrix row addresses of 8 consecutive tokens fall in
-// 8 distinct bank groups (conflict-free).  Partials (M, D, num[d]) are
-// flushed per (unit, kind) and folded by att4_merge_kernel.
+// P CTAs x WARPS warps.  Each warp streams its range through a 2-stage ring
+// filled by 1-D bulk copies (TMA), one per contiguous run of store rows (a
+// 16-row chunk of retrieved tokens is ~2 cluster runs); the bf16 rows are
+// stored swizzled (common.cuh swz_col: 16-byte piece c of row r at c ^ (r & 7)),
+// so the 8 row addresses of an ldmatrix hit 8 distinct bank groups without
+// padding.  Measured alternatives: one bulk copy per row into padded rows
+// (a bulk copy takes warp-uniform operands, so 16 lanes' row addresses go
+// through a serialising R2UR loop, ~6 instructions per row: the top stall of
+// that version, 81 us/layer) and cp.async (LDGSTS) per 16 bytes (123 us).
+// Partials (M, D, num[d]) are flushed per (unit, kind) and folded by
+// att4_merge_kernel.
 #include <cuda_bf16.h>
 
 #include "common.cuh"
@@ -56,19 +62,24 @@ struct Att5Cfg {
   static constexpr int NL = HS == 4 ? 2 : 4;       // (row, head) logit slots per lane
   static constexpr int NH = HS == 4 ? 1 : 2;       // logit heads per lane
   static constexpr int NA = KS * 4;                // accumulator floats per lane
-  static constexpr int NST = 2;                    // ring stages per warp
+#ifndef ATT5_NST
+#define ATT5_NST 2  // tuning experiments only (tools/att5_sweep.sh)
+#endif
+#ifndef ATT5_WMAX
+#define ATT5_WMAX 12
+#endif
+  static constexpr int NST = ATT5_NST;             // ring stages per warp
   static constexpr int ROWT = D * 2;               // bf16 K or V row bytes
-  static constexpr int RS = ROWT + 16;             // padded smem row stride
   static constexpr int ROWV = D * 4;               // fp32 value-sum row bytes
-  static constexpr int SB = ((2 * RG * RS > RG * ROWV ? 2 * RG * RS : RG * ROWV) + 127) / 128 * 128;
-  // per warp: stage tags + row head masks, per-stage estimation inputs (logit
+  static constexpr int SB = ((2 * RG * ROWT > RG * ROWV ? 2 * RG * ROWT : RG * ROWV) + 127) / 128 * 128;
+  // per warp: stage tags + row (head mask | swizzle key << 8), per-stage estimation inputs (logit
   // + weight per lane slot), bf16 split weights [3][8 heads][16 tokens], fp32
   // weights [16][HS]
-  static constexpr int META = NST * 32 + NST * NL * 32 * 8 + 3 * 8 * RG * 2 + RG * HS * 4;
+  static constexpr int META = NST * 48 + NST * NL * 32 * 8 + 3 * 8 * RG * 2 + RG * HS * 4;
   static constexpr int MAXU = 1024;
   static constexpr int WPB = NST * SB + NST * 8 + META;  // bytes per warp
   static constexpr int FIT = (227 * 1024 - (MAXU + 1) * 4 - 64) / WPB;
-  static constexpr int WARPS = FIT > 12 ? 12 : FIT;
+  static constexpr int WARPS = FIT > ATT5_WMAX ? ATT5_WMAX : FIT;
   static constexpr size_t SMEM = (size_t)WARPS * WPB + (size_t)(MAXU + 1) * 4 + 64;
 };
 
@@ -87,22 +98,13 @@ WK_DEVINL void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2
 }
 WK_DEVINL void mma_bf16(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
                         uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+  // not volatile: a pure register operation the compiler may interleave
+  asm("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
       "{%0,%1,%2,%3};\n"
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
-// shared-window (32-bit) forms of the bulk-copy / mbarrier helpers
-WK_DEVINL void bulk_g2s_s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
-      "l"(src), "r"(bytes), "r"(bar)
-      : "memory");
-}
-WK_DEVINL void mbar_expect_s(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
-}
+// mbarrier wait on a 32-bit shared-window address
 WK_DEVINL void mbar_wait_s(uint32_t bar, uint32_t phase) {
   asm volatile(
       "{\n"
@@ -139,6 +141,10 @@ WK_DEVINL void att5_counts(const SteadyView& st, const StepView& sv, const int32
     c1 = ROWS ? (sv.cnt[u * 4 + 1] + RG - 1) / RG : sv.cnt[u * 4 + 3];
     c2 = (sv.cnt[u * 4 + 2] + RG - 1) / RG;
   }
+#ifdef ATT5_SKIP  // timing experiments only: 1 = no estimation chunks, 2 = no exact chunks
+  if (ATT5_SKIP == 1) c2 = 0;
+  if (ATT5_SKIP == 2) { c0 = 0; c1 = 0; }
+#endif
 }
 
 template <int D, int HS, bool FULL, bool OFF, bool ROWS>
@@ -147,7 +153,7 @@ __global__ void __launch_bounds__(Att5Cfg<D, HS>::WARPS * 32, 1)
                      int U) {
   using CF = Att5Cfg<D, HS>;
   constexpr int RG = CF::RG, KS = CF::KS, NT = CF::NT, NL = CF::NL, NH = CF::NH, NA = CF::NA, NST = CF::NST;
-  constexpr int ROWT = CF::ROWT, RS = CF::RS, ROWV = CF::ROWV, SB = CF::SB;
+  constexpr int ROWT = CF::ROWT, ROWV = CF::ROWV, SB = CF::SB;
   constexpr int DL = D / 16;  // estimation mode: dims per lane
   pdl_wait();
   const int G = p.G;
@@ -157,11 +163,12 @@ __global__ void __launch_bounds__(Att5Cfg<D, HS>::WARPS * 32, 1)
   extern __shared__ __align__(128) unsigned char a5s[];
   unsigned char* ring = a5s + (size_t)warp * NST * SB;
   const uint32_t ring_s = smem_u32(ring);
-  const uint32_t bars_s = smem_u32(a5s + (size_t)CF::WARPS * NST * SB) + warp * NST * 8;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(a5s + (size_t)CF::WARPS * NST * SB) + warp * NST;
+  const uint32_t bars_s = smem_u32(bars);
   unsigned char* meta = a5s + (size_t)CF::WARPS * NST * (SB + 8) + (size_t)warp * CF::META;
   int4* stag = reinterpret_cast<int4*>(meta);                                 // [NST] chunk tags
-  unsigned char* smk = meta + NST * 16;                                       // [NST][16] row head masks
-  float* sx = reinterpret_cast<float*>(meta + NST * 32);                      // [NST][NL][32]
+  unsigned short* smk = reinterpret_cast<unsigned short*>(meta + NST * 16);   // [NST][16] mask | key << 8
+  float* sx = reinterpret_cast<float*>(meta + NST * 48);                      // [NST][NL][32]
   float* sw = sx + NST * NL * 32;                                             // [NST][NL][32]
   unsigned short* pb = reinterpret_cast<unsigned short*>(sw + NST * NL * 32);  // [3][8][RG] bf16
   float* pe = reinterpret_cast<float*>(pb + 3 * 8 * RG);                      // [RG][HS]
@@ -207,7 +214,7 @@ __global__ void __launch_bounds__(Att5Cfg<D, HS>::WARPS * 32, 1)
   const long long ca = Ntot * wg / Wtot, cb = Ntot * (wg + 1) / Wtot;
 
   if (lane == 0) {
-    for (int i = 0; i < NST; i++) mbar_init(reinterpret_cast<uint64_t*>(a5s + (size_t)CF::WARPS * NST * SB) + warp * NST + i, 1);
+    for (int i = 0; i < NST; i++) mbar_init(bars + i, 1);
     fence_mbar_init();
   }
   // split-weight rows of the unused head slots stay zero
@@ -274,7 +281,7 @@ __global__ void __launch_bounds__(Att5Cfg<D, HS>::WARPS * 32, 1)
       } else if (ROWS) {
         const int r0 = lc * RG;
         n = min(RG, in_x - r0);
-        if (lane < n) m.a = __ldcg(sv.rtok_row + (size_t)u * sv.rt_cap + r0 + lane);
+        if ((lane & 15) < n) m.a = __ldcg(sv.rtok_row + (size_t)u * sv.rt_cap + r0 + (lane & 15));
       } else {  // offload piece: (row, n | mask << 8 | flags << 16, cluster, first token)
         const int4 pc = __ldcg(reinterpret_cast<const int4*>(sv.pieces) + (size_t)u * sv.pc_cap + lc);
         m.a = pc.x;
@@ -288,7 +295,7 @@ __global__ void __launch_bounds__(Att5Cfg<D, HS>::WARPS * 32, 1)
       lc -= ic0 + ic1;
       const int e0 = lc * RG;
       n = min(RG, sv.cnt[u * 4 + 2] - e0);
-      if (lane < n) m.a = __ldcg(sv.eu_ids + (size_t)u * sv.eu_cap + e0 + lane);
+      if ((lane & 15) < n) m.a = __ldcg(sv.eu_ids + (size_t)u * sv.eu_cap + e0 + (lane & 15));
 #pragma unroll
       for (int l = 0; l < NL; l++) {
         const int r = slot_row(l), h = slot_head(l);
@@ -301,22 +308,28 @@ __global__ void __launch_bounds__(Att5Cfg<D, HS>::WARPS * 32, 1)
     m.h = u | ((kind + 1) << 20) | ((n & 31) << 22);
     return m;
   };
+  // Copies (TMA 1-D bulk): the K and V rows of a chunk arrive as one bulk copy
+  // per contiguous run of store rows (row mode: a cluster's members are
+  // contiguous, so a 16-row chunk is ~2 runs), issued by the run's first lane;
+  // bf16 rows are stored swizzled (common.cuh swz_col), so the unpadded rows
+  // read conflict-free with ldmatrix.  Estimation rows: one copy per row.
   auto issue = [&](int sti, const Meta& m) {
     const int u = m.h & 0xfffff, kind = ((m.h >> 20) & 3) - 1, n = (m.h >> 22) & 31;
     const uint32_t stage_s = ring_s + sti * SB, bar = bars_s + sti * 8;
+    const int j = lane & 15;
+    const bool live = lane < n;
     int flags = 0;
     if (kind < 2) {
-      // this lane's row (lane < n) and head mask
       int row, mk;
       const unsigned char* bk;
       const unsigned char* bv;
       if (kind == 0) {
-        row = m.a + lane;
+        row = m.a + j;
         mk = m.mk;
         bk = (const unsigned char*)st.k + (size_t)u * st.t_cap * ROWT;
         bv = (const unsigned char*)st.v + (size_t)u * st.t_cap * ROWT;
       } else if (FULL) {
-        row = m.a + lane;
+        row = m.a + j;
         mk = m.mk;
         bk = (const unsigned char*)ix.store_k + (size_t)u * ix.s_cap * ROWT;
         bv = (const unsigned char*)ix.store_v + (size_t)u * ix.s_cap * ROWT;
@@ -326,7 +339,7 @@ __global__ void __launch_bounds__(Att5Cfg<D, HS>::WARPS * 32, 1)
         bk = (const unsigned char*)ix.store_k + (size_t)u * ix.s_cap * ROWT;
         bv = (const unsigned char*)ix.store_v + (size_t)u * ix.s_cap * ROWT;
       } else {  // offload piece: hit -> the HBM slot arena, miss -> the pinned host store (zero-copy TMA)
-        row = m.a + lane;
+        row = m.a + j;
         mk = (m.mk >> 8) & 0xff;
         flags = (m.mk >> 16) & 3;
         if (flags & 1) {
@@ -337,29 +350,39 @@ __global__ void __launch_bounds__(Att5Cfg<D, HS>::WARPS * 32, 1)
           bv = (const unsigned char*)ix.store_v + (size_t)u * ix.s_cap * ROWT;
         }
       }
-      // one bulk copy per row into the padded layout; K rows >= n stay stale
-      // (their head mask is 0, the logits are masked by selection), V rows >= n
-      // are zero-filled so a zero weight never meets a non-finite stale value
-      if (lane == 0) mbar_expect_s(bar, (uint32_t)(2 * n * ROWT + (RG - n) * RS));
+      // runs of consecutive rows among lanes 0..n-1
+      const int prev = __shfl_up_sync(0xffffffffu, row, 1);
+      const bool start = live && (lane == 0 || row != prev + 1);
+      const unsigned starts = __ballot_sync(0xffffffffu, start);
+      if (lane == 0) mbar_arrive_expect_tx(bars + sti, (uint32_t)((n + RG) * ROWT));
       __syncwarp();
-      if (lane < n) {
-        bulk_g2s_s(stage_s + lane * RS, bk + (size_t)row * ROWT, (uint32_t)ROWT, bar);
-        bulk_g2s_s(stage_s + RG * RS + lane * RS, bv + (size_t)row * ROWT, (uint32_t)ROWT, bar);
+      if (start) {
+        const unsigned later = starts & ~((2u << lane) - 1u);
+        const int len = (later ? __ffs(later) - 1 : n) - lane;
+        bulk_g2s(ring + sti * SB + lane * ROWT, bk + (size_t)row * ROWT, (uint32_t)(len * ROWT), bars + sti);
+        bulk_g2s(ring + sti * SB + RG * ROWT + lane * ROWT, bv + (size_t)row * ROWT, (uint32_t)(len * ROWT),
+                 bars + sti);
       }
-      if (lane == 0 && n < RG) bulk_g2s_s(stage_s + RG * RS + n * RS, g_zero5, (uint32_t)((RG - n) * RS), bar);
-      if (lane < RG) smk[sti * 16 + lane] = (unsigned char)(lane < n ? mk : 0);
+      // V rows >= n zero-filled (a zero weight never meets a stale non-finite
+      // value); K rows >= n stay stale (head mask 0: logits masked by selection)
+      if (lane == 0 && n < RG)
+        bulk_g2s(ring + sti * SB + RG * ROWT + n * ROWT, g_zero5, (uint32_t)((RG - n) * ROWT), bars + sti);
+      if (lane < RG) smk[sti * 16 + lane] = (unsigned short)(live ? (mk | ((row & 7) << 8)) : ((lane & 7) << 8));
     } else {
-      if (lane == 0) mbar_expect_s(bar, (uint32_t)(RG * ROWV));
+      if (lane == 0) mbar_arrive_expect_tx(bars + sti, (uint32_t)(RG * ROWV));
       __syncwarp();
-      if (lane < n)
-        bulk_g2s_s(stage_s + lane * ROWV, ix.VS32 + ((size_t)u * ix.m_cap + m.a) * D, (uint32_t)ROWV, bar);
-      if (lane == 0 && n < RG) bulk_g2s_s(stage_s + n * ROWV, g_zero5, (uint32_t)((RG - n) * ROWV), bar);
+      if (live)
+        bulk_g2s(ring + sti * SB + lane * ROWV, ix.VS32 + ((size_t)u * ix.m_cap + m.a) * D, (uint32_t)ROWV,
+                 bars + sti);
+      if (lane == 0 && n < RG) bulk_g2s(ring + sti * SB + n * ROWV, g_zero5, (uint32_t)((RG - n) * ROWV), bars + sti);
 #pragma unroll
       for (int l = 0; l < NL; l++) {
         sx[(sti * NL + l) * 32 + lane] = m.x[l];
         sw[(sti * NL + l) * 32 + lane] = m.w[l];
       }
     }
+    (void)bar;
+    (void)stage_s;
     // tag: (unit, kind + 1 | rows << 8, offload write-through: cluster, first token | 1 << 31)
     if (lane == 0)
       stag[sti] = make_int4(u, (kind + 1) | (n << 8),
@@ -525,18 +548,31 @@ __global__ void __launch_bounds__(Att5Cfg<D, HS>::WARPS * 32, 1)
     float x[NL], pw[NL];
     if (kind < 2) {
       // ---- q.k on the tensor cores: S^T = K . Qs^T ----
-      float c[NT][4];
+      // two accumulator sets (even / odd k-steps) halve the dependent MMA chain
+      float c[NT][4], c2[NT][4];
 #pragma unroll
-      for (int nt = 0; nt < NT; nt++) c[nt][0] = c[nt][1] = c[nt][2] = c[nt][3] = 0.f;
-      const uint32_t aK = stage_s + ((lane & 7) + ((lane >> 3) & 1) * 8) * RS + (lane >> 4) * 16;
+      for (int nt = 0; nt < NT; nt++)
 #pragma unroll
-      for (int kk = 0; kk < KS; kk++) {
-        uint32_t a0, a1, a2, a3;
-        ldsm_x4(aK + kk * 32, a0, a1, a2, a3);
+        for (int i = 0; i < 4; i++) c[nt][i] = c2[nt][i] = 0.f;
+      // swizzled rows: piece c of chunk row r sits at piece c ^ key(r)
+      const int jk = (lane & 7) + ((lane >> 3) & 1) * 8;
+      const int kbk = ((smk[sti * 16 + jk] >> 8) & 7) ^ (lane >> 4);
+      const uint32_t aK = stage_s + jk * ROWT;
+      uint32_t ak[KS][4];
 #pragma unroll
-        for (int nt = 0; nt < NT; nt++) mma_bf16(c[nt], a0, a1, a2, a3, qb[kk][nt][0], qb[kk][nt][1]);
-      }
-      const int mk_lo = smk[sti * 16 + g8], mk_hi = smk[sti * 16 + g8 + 8];
+      for (int kk = 0; kk < KS; kk++)
+        ldsm_x4(aK + (((2 * kk) ^ kbk) << 4), ak[kk][0], ak[kk][1], ak[kk][2], ak[kk][3]);
+#pragma unroll
+      for (int kk = 0; kk < KS; kk++)
+#pragma unroll
+        for (int nt = 0; nt < NT; nt++)
+          mma_bf16((kk & 1) ? c2[nt] : c[nt], ak[kk][0], ak[kk][1], ak[kk][2], ak[kk][3], qb[kk][nt][0],
+                   qb[kk][nt][1]);
+#pragma unroll
+      for (int nt = 0; nt < NT; nt++)
+#pragma unroll
+        for (int i = 0; i < 4; i++) c[nt][i] += c2[nt][i];
+      const int mk_lo = smk[sti * 16 + g8] & 0xff, mk_hi = smk[sti * 16 + g8 + 8] & 0xff;
 #pragma unroll
       for (int l = 0; l < NL; l++) {
         float s;
@@ -571,16 +607,22 @@ __global__ void __launch_bounds__(Att5Cfg<D, HS>::WARPS * 32, 1)
         ldsm_x4(pb_s + (((mi >> 1) * 8 + r) * RG + (mi & 1) * 8) * 2, b[0][0], b[0][1], b[1][0], b[1][1]);
         ldsm_x2(pb_s + ((16 + r) * RG + (mi & 1) * 8) * 2, b[2][0], b[2][1]);
       }
-      const uint32_t aV = stage_s + RG * RS + ((lane & 7) + 8 * (lane >> 4)) * RS + ((lane >> 3) & 1) * 16;
+      const int jv = (lane & 7) + 8 * (lane >> 4);
+      const int kbv = ((smk[sti * 16 + jv] >> 8) & 7) ^ ((lane >> 3) & 1);
+      const uint32_t aV = stage_s + RG * ROWT + jv * ROWT;
+      // all V fragments first, then the MMAs split-major (lo, mid, hi) so
+      // consecutive MMAs update different accumulator tiles
+      uint32_t av[KS][4];
 #pragma unroll
-      for (int mt = 0; mt < KS; mt++) {
-        uint32_t a0, a1, a2, a3;
-        ldsm_x4_t(aV + mt * 32, a0, a1, a2, a3);
-        float (&cc)[4] = *reinterpret_cast<float(*)[4]>(&acc[mt * 4]);
-        mma_bf16(cc, a0, a1, a2, a3, b[2][0], b[2][1]);
-        mma_bf16(cc, a0, a1, a2, a3, b[1][0], b[1][1]);
-        mma_bf16(cc, a0, a1, a2, a3, b[0][0], b[0][1]);
-      }
+      for (int mt = 0; mt < KS; mt++)
+        ldsm_x4_t(aV + (((2 * mt) ^ kbv) << 4), av[mt][0], av[mt][1], av[mt][2], av[mt][3]);
+#pragma unroll
+      for (int s = 2; s >= 0; s--)
+#pragma unroll
+        for (int mt = 0; mt < KS; mt++) {
+          float (&cc)[4] = *reinterpret_cast<float(*)[4]>(&acc[mt * 4]);
+          mma_bf16(cc, av[mt][0], av[mt][1], av[mt][2], av[mt][3], b[s][0], b[s][1]);
+        }
     } else {
       // ---- estimation rows: fp32 value sums on the FP32 pipes ----
       float wz[NL];
@@ -665,12 +707,14 @@ __global__ void __launch_bounds__(Att5Cfg<D, HS>::WARPS * 32, 1)
         const unsigned char* stage = ring + sti * SB;
         for (int i = half; i < nrow; i += 2) {
           const int tok = j0 + i;
-          const size_t arow = (size_t)cu * sv.arena_rows + (size_t)__ldcg(sl + so + tok / bt) * bt + tok % bt;
-          for (int o = sub * 16; o < ROWT; o += 256) {
-            *reinterpret_cast<uint4*>((unsigned char*)sv.arena_k + arow * ROWT + o) =
-                *reinterpret_cast<const uint4*>(stage + i * RS + o);
-            *reinterpret_cast<uint4*>((unsigned char*)sv.arena_v + arow * ROWT + o) =
-                *reinterpret_cast<const uint4*>(stage + RG * RS + i * RS + o);
+          const size_t ar = (size_t)__ldcg(sl + so + tok / bt) * bt + tok % bt;  // the unit's arena row
+          const size_t arow = (size_t)cu * sv.arena_rows + ar;
+          const int ks = (smk[sti * 16 + i] >> 8) & 7, ka = (int)(ar & 7);  // re-swizzle: store key -> arena key
+          if (sub < ROWT / 16) {
+            *reinterpret_cast<uint4*>((unsigned char*)sv.arena_k + arow * ROWT + ((sub ^ ka) << 4)) =
+                *reinterpret_cast<const uint4*>(stage + i * ROWT + ((sub ^ ks) << 4));
+            *reinterpret_cast<uint4*>((unsigned char*)sv.arena_v + arow * ROWT + ((sub ^ ka) << 4)) =
+                *reinterpret_cast<const uint4*>(stage + RG * ROWT + i * ROWT + ((sub ^ ks) << 4));
           }
         }
       }

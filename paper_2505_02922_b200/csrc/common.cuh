@@ -40,6 +40,19 @@ template <> struct KV<__nv_bfloat16> {
   static WK_DEVINL __nv_bfloat16 from_f(float x) { return __float2bfloat16_rn(x); }
 };
 
+// bf16 K/V rows of the fast path (d in {64, 128}) are stored swizzled: the
+// 16-byte piece c of row r (8 elements) sits at piece c ^ (r & 7) of the row,
+// r = the row's index in its array (cluster store, steady buffer, slot arena).
+// A contiguous run of rows copied as one block then reads conflict-free with
+// ldmatrix (attend_v5).  swz_col maps a logical element index to its slot.
+__host__ __device__ __forceinline__ int swz_col(int t, long long row) {
+  return ((((t >> 3) ^ (int)(row & 7)) << 3) | (t & 7));
+}
+template <typename T>
+__host__ __device__ __forceinline__ bool kv_swizzled(int d) {
+  return sizeof(T) == 2 && (d == 64 || d == 128);
+}
+
 // order-preserving float <-> uint32 (ascending)
 WK_DEVINL uint32_t f2u_ord(float f) {
   uint32_t u = __float_as_uint(f);

@@ -35,9 +35,11 @@ __global__ void append_kernel(SteadyView st, const float* __restrict__ k_new,
   }
   T* kd = (T*)st.k + ((size_t)u * st.t_cap + row) * d;
   T* vd = (T*)st.v + ((size_t)u * st.t_cap + row) * d;
+  const bool swz = kv_swizzled<T>(d);
   for (int t = threadIdx.x; t < d; t += blockDim.x) {
-    kd[t] = KV<T>::from_f(k_new[(size_t)u * d + t]);
-    vd[t] = KV<T>::from_f(v_new[(size_t)u * d + t]);
+    const int col = swz ? swz_col(t, row) : t;
+    kd[col] = KV<T>::from_f(k_new[(size_t)u * d + t]);
+    vd[col] = KV<T>::from_f(v_new[(size_t)u * d + t]);
   }
   __syncthreads();  // every thread read n[u] before it advances
   if (threadIdx.x == 0) {
@@ -665,11 +667,13 @@ __global__ void __launch_bounds__(AT_THREADS) attend_kernel(IndexView ix, Steady
       const T* kb = kind == 0 ? stk : sk;
       const T* vb = kind == 0 ? stv : svv;
       const int cpr = d * (int)sizeof(T) / 16;
+      const bool swz = kv_swizzled<T>(d);  // swizzled rows (common.cuh swz_col): un-swizzle while staging
       for (int idx = threadIdx.x; idx < nrow * cpr; idx += blockDim.x) {
         const int j = idx / cpr, ch = idx % cpr;
         const long long src = rsrc[j];
-        cp_async16(tA + j * ldb + ch * 16, reinterpret_cast<const unsigned char*>(kb + src * d) + ch * 16);
-        cp_async16(tB + j * ldb + ch * 16, reinterpret_cast<const unsigned char*>(vb + src * d) + ch * 16);
+        const int pch = swz ? (ch ^ (int)(src & 7)) : ch;
+        cp_async16(tA + j * ldb + ch * 16, reinterpret_cast<const unsigned char*>(kb + src * d) + pch * 16);
+        cp_async16(tB + j * ldb + ch * 16, reinterpret_cast<const unsigned char*>(vb + src * d) + pch * 16);
       }
     } else {
       const int cpr = d * 4 / 16;

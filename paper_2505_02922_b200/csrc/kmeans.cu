@@ -1181,11 +1181,14 @@ __global__ void km_finalize_kernel(const SegDesc* __restrict__ segs, const int32
     ix.cl_size[u * ix.m_cap + cid] = s;
   }
   for (int j = threadIdx.x; j < sg.L; j += blockDim.x) stok[sg.row_base + j] = sg.tok_base + perm[j];
+  const bool swz = kv_swizzled<T>(d);
   for (size_t idx = threadIdx.x; idx < (size_t)sg.L * d; idx += blockDim.x) {
     size_t j = idx / d, t = idx % d;
     size_t src = (size_t)perm[j] * sg.key_stride + t;
-    sk[(size_t)(sg.row_base + j) * d + t] = KV<T>::from_f(sg.keys[src]);
-    sv[(size_t)(sg.row_base + j) * d + t] = KV<T>::from_f(sg.values[src]);
+    const size_t row = (size_t)sg.row_base + j;
+    const size_t col = swz ? (size_t)swz_col((int)t, (long long)row) : t;
+    sk[row * d + col] = KV<T>::from_f(sg.keys[src]);
+    sv[row * d + col] = KV<T>::from_f(sg.values[src]);
   }
   for (int idx = threadIdx.x; idx < sg.k * d; idx += blockDim.x) {
     int c = idx / d, t = idx % d;

@@ -26,8 +26,9 @@ struct RecallSmem {
 };
 
 template <typename T>
-__device__ __forceinline__ void load_row_f64(const T* r, double* o, int d) {
-  for (int t = 0; t < d; t++) o[t] = (double)KV<T>::to_f(r[t]);
+__device__ __forceinline__ void load_row_f64(const T* r, double* o, int d, long long row) {
+  const bool swz = kv_swizzled<T>(d);
+  for (int t = 0; t < d; t++) o[t] = (double)KV<T>::to_f(r[swz ? swz_col(t, row) : t]);
 }
 
 // grid = U*G, block = 512.  scratch: s [U*G, n_cap] f32, rflag [U*G, s_cap] u8.
@@ -67,9 +68,11 @@ __global__ void __launch_bounds__(512) recall_kernel(IndexView ix, SteadyView st
   float kmx = 0.f;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const T* kr = i < ns ? sk + (int64_t)i * d : stk + (int64_t)(i - ns) * d;
+    const long long kro = i < ns ? i : i - ns;  // the row's index in its array (swizzle key)
+    const bool swz = kv_swizzled<T>(d);
     float a = 0.f, nn = 0.f;
     for (int t = 0; t < d; t++) {
-      float kv = KV<T>::to_f(kr[t]);
+      float kv = KV<T>::to_f(kr[swz ? swz_col(t, kro) : t]);
       a = fmaf(kv, q[t], a);
       nn = fmaf(kv, kv, nn);
     }
@@ -108,7 +111,7 @@ __global__ void __launch_bounds__(512) recall_kernel(IndexView ix, SteadyView st
     auto key = [&](int i) {
       const T* kr = i < ns ? sk + (int64_t)i * d : stk + (int64_t)(i - ns) * d;
       double kd[256];
-      load_row_f64(kr, kd, d);
+      load_row_f64(kr, kd, d, i < ns ? i : i - ns);
       return xs_key(dgemv_row(kd, sm.q64, d, gemv_row_class(tok_of(i), n, d, blas_threads)));
     };
     auto idf = [&](int i) { return (unsigned)tok_of(i); };
@@ -131,7 +134,7 @@ __global__ void __launch_bounds__(512) recall_kernel(IndexView ix, SteadyView st
     const T* kr = row < ns ? sk + (int64_t)row * d : stk + (int64_t)(row - ns) * d;
     const int tok = row < ns ? stok[row] : sttok[row - ns];
     double kd[256];
-    load_row_f64(kr, kd, d);
+    load_row_f64(kr, kd, d, row < ns ? row : row - ns);
     sm.bex[i] = dgemv_row(kd, sm.q64, d, gemv_row_class(tok, n, d, blas_threads));
   }
   __syncthreads();

@@ -448,9 +448,10 @@ __global__ void __launch_bounds__(S6_T, 4) select_v6_kernel(IndexView ix, StepVi
     const size_t o = ((size_t)u * p.st.t_cap + row) * d;
     for (int i = t; fits && i < d; i += T) {
       const float kv = p.k_new[(size_t)u * d + i], vv = p.v_new[(size_t)u * d + i];
-      if (p.store_bf16) {
-        reinterpret_cast<__nv_bfloat16*>(p.st.k)[o + i] = __float2bfloat16_rn(kv);
-        reinterpret_cast<__nv_bfloat16*>(p.st.v)[o + i] = __float2bfloat16_rn(vv);
+      if (p.store_bf16) {  // swizzled rows (common.cuh swz_col; d in {64, 128} here)
+        const int c = swz_col(i, row);
+        reinterpret_cast<__nv_bfloat16*>(p.st.k)[o + c] = __float2bfloat16_rn(kv);
+        reinterpret_cast<__nv_bfloat16*>(p.st.v)[o + c] = __float2bfloat16_rn(vv);
       } else {
         reinterpret_cast<float*>(p.st.k)[o + i] = kv;
         reinterpret_cast<float*>(p.st.v)[o + i] = vv;

@@ -69,6 +69,19 @@ class UnitState:
     n_steady: int = 0         # sinks + buffer rows
 
 
+def swizzle_rows(x: torch.Tensor, row0: int = 0) -> torch.Tensor:
+    """The fast path's bf16 row layout (csrc/common.cuh swz_col): 16-byte piece
+    c of row r (8 elements) sits at piece c ^ (r & 7), r = row0 + the row's index
+    in x.  An involution: the same call un-swizzles."""
+    n, d = x.shape[-2], x.shape[-1]
+    pcs = d // 8
+    key = (torch.arange(row0, row0 + n, device=x.device) & 7)[:, None]
+    src = torch.arange(pcs, device=x.device)[None, :] ^ key
+    xr = x.reshape(*x.shape[:-1], pcs, 8)
+    idx = src[..., None].expand(*xr.shape)
+    return torch.gather(xr, -2, idx).reshape(x.shape)
+
+
 class WaveLayer:
     """U units x G heads of one layer; all tensors on ``device``."""
 
@@ -108,6 +121,8 @@ class WaveLayer:
         self.e_cap = max(1, min(self.m_cap, round_half_up(ic.estimation_fraction * self.m_cap) + 2))
         # fast path (score_v5 / select_v6 / attend_v4): d in {64, 128}
         self.fast = d in (64, 128)
+        # bf16 rows of the fast path are stored swizzled (csrc/common.cuh swz_col)
+        self.swizzled = self.fast and store_dtype == torch.bfloat16
         hs = 4 if G <= 4 else 8
         # retrieval piece rows = the attention chunk rows: attend_v5 (bf16 stores,
         # tensor cores) 16; attend_v4 (fp32 stores) 16 for G <= 4, 8 for G <= 8
@@ -159,7 +174,8 @@ class WaveLayer:
         self.nr = torch.zeros(U, dtype=i32, device=dev)
         self.ne = torch.zeros(U, dtype=i32, device=dev)
         self.ru_cap = min(self.m_cap, G * self.r_cap)
-        self.eu_cap = min(self.m_cap, G * self.e_cap)
+        # multiple of 16: attend_v6 copies estimation logits / sizes 16 rows at a time
+        self.eu_cap = -(-min(self.m_cap, G * self.e_cap) // 16) * 16
         self.ru_ids = torch.zeros((U, self.ru_cap), dtype=i32, device=dev)
         self.ru_mask = torch.zeros((U, self.ru_cap), dtype=torch.uint8, device=dev)
         self.eu_ids = torch.zeros((U, self.eu_cap), dtype=i32, device=dev)
@@ -237,6 +253,16 @@ class WaveLayer:
                                          ixv=self._index_view(u0, u1), stv=self._steady_view(u0, u1)))
             self._streams = [torch.cuda.Stream(device=dev) for _ in range(self.split)]
         self.prefilled = False
+
+    # ------------------------------------------------------------ row layout
+    def _to_rows(self, x: torch.Tensor, row0: int) -> torch.Tensor:
+        """fp32 rows -> the steady/store row format (bf16 fast path: swizzled)."""
+        y = x.to(self.store_dtype)
+        return swizzle_rows(y, row0) if self.swizzled else y
+
+    def _from_rows(self, x: torch.Tensor, row0: int) -> torch.Tensor:
+        """Stored rows (starting at row index row0 of their array) -> fp32."""
+        return (swizzle_rows(x, row0) if self.swizzled else x).float()
 
     # ------------------------------------------------------------------ views
     def _index_view(self, u0, u1):
@@ -404,8 +430,8 @@ class WaveLayer:
             rows = list(range(st.n_sink)) + list(range(index_end, n))
             if rows:
                 idx = torch.tensor(rows, device=self.dev, dtype=torch.long)
-                self.st_k[u, : len(rows)] = keys[u, idx].to(self.store_dtype)
-                self.st_v[u, : len(rows)] = values[u, idx].to(self.store_dtype)
+                self.st_k[u, : len(rows)] = self._to_rows(keys[u, idx], 0)
+                self.st_v[u, : len(rows)] = self._to_rows(values[u, idx], 0)
                 self.st_tok[u, : len(rows)] = idx.to(torch.int32)
         if self.m_cap < max(s.m for s in self.units):
             raise ConfigError("cluster capacity exceeded")
@@ -495,8 +521,8 @@ class WaveLayer:
                 if s.m + k > self.m_cap or s.store_fill + ic.update_segment > self.s_cap:
                     raise ConfigError("index capacity exceeded: raise max_decode")
                 r0 = s.n_sink
-                tmp_k[j] = self.st_k[u, r0:r0 + ic.update_segment].float()
-                tmp_v[j] = self.st_v[u, r0:r0 + ic.update_segment].float()
+                tmp_k[j] = self._from_rows(self.st_k[u, r0:r0 + ic.update_segment], r0)
+                tmp_v[j] = self._from_rows(self.st_v[u, r0:r0 + ic.update_segment], r0)
                 base = j * ic.update_segment * self.d
                 segs.append(dict(keys=tmp_k.data_ptr() + 4 * base, values=tmp_v.data_ptr() + 4 * base,
                                  stride=self.d, L=ic.update_segment, k=k, unit=u, cid_base=s.m,
@@ -507,8 +533,9 @@ class WaveLayer:
                 s = self.units[u]
                 r0, r1 = s.n_sink + ic.update_segment, s.n_steady
                 # keep the buffer tail (index.py:179-180): shift rows down
-                for t in (self.st_k, self.st_v, self.st_tok):
-                    t[u, s.n_sink:s.n_sink + (r1 - r0)] = t[u, r0:r1].clone()
+                for t in (self.st_k, self.st_v):  # re-keyed to the rows' new positions
+                    t[u, s.n_sink:s.n_sink + (r1 - r0)] = self._to_rows(self._from_rows(t[u, r0:r1], r0), s.n_sink)
+                self.st_tok[u, s.n_sink:s.n_sink + (r1 - r0)] = self.st_tok[u, r0:r1].clone()
                 s.n_steady -= ic.update_segment
                 s.m += k
                 s.store_fill += ic.update_segment
