@@ -42,6 +42,5 @@ tot = np.median(ts[:, 12] - ts[:, 0])
 print(f"U={U}: median CTA cycles {tot:.0f} ({tot / 1.9e3:.1f} us at 1.9 GHz)")
 for i, nm in enumerate(names):
     print(f"  {nm:18s} median {np.median(d_[:, i]):8.0f}  p90 {np.percentile(d_[:, i], 90):8.0f}")
-print("pass D detail (thread 0): start->iter0 ballots", np.median(ts_all[:, 13] - ts_all[:, 2]),
-      " iter0 appends", np.median(ts_all[:, 14] - ts_all[:, 13]), " rest of loop", np.median(ts_all[:, 15] - ts_all[:, 14]),
-      " barrier", np.median(ts_all[:, 3] - ts_all[:, 15]))
+print("emit detail (thread 0): prefixes", np.median(ts_all[:, 13] - ts_all[:, 9]),
+      " word loop", np.median(ts_all[:, 14] - ts_all[:, 13]), " to cl.sync 2", np.median(ts_all[:, 10] - ts_all[:, 14]))
