@@ -17,6 +17,8 @@ namespace wk {
 __global__ void km_prep_kernel(const SegDesc*, float*, int, __half*);
 __global__ void km_seed_kernel(const SegDesc*, const float*, float*, float*, int, int, int);
 __global__ void km_seed_v2_kernel(const SegDesc*, const float*, float*, float*, int, int, int, const __half*, int);
+__global__ void km_seed_v3_kernel(const SegDesc*, int, const float*, float*, float*, int, int, const __half*, int);
+constexpr int KS3_W = 4;  // kmeans.cu: segments (warps) per CTA of km_seed_v3
 __global__ void km_assign_kernel(const SegDesc*, const float*, const float*, int32_t*, int);
 template <int KS>
 __global__ void km_assign_tc_kernel(const SegDesc*, const float*, const float*, int32_t*);
@@ -388,7 +390,13 @@ int wk_kmeans_segments(const wk_index_view* ix, const wk_segment* segs, int n_se
     km_prep_kernel<<<n_segs, 256, d * sizeof(float), s>>>(sd, scr->P, d, p16);
   }
   WK_CHECK_LAUNCH();
-  if ((d % 8) == 0) {
+  if ((d % 8) == 0 && d <= 128) {
+    // v3: one warp per segment (the segments' serial chains side by side)
+    const int K4 = (max_k + 3) & ~3;
+    const size_t sm3 = (size_t)KS3_W * (d + K4 + KS_CK + 256) * sizeof(float);
+    km_seed_v3_kernel<<<(n_segs + KS3_W - 1) / KS3_W, KS3_W * 32, sm3, s>>>(sd, n_segs, scr->P, scr->C, scr->md, d,
+                                                                          blas_threads, p16, max_k);
+  } else if ((d % 8) == 0) {
     // v2: 256 threads; centre + centre-distance bounds + (md, best) rows in smem
     // when they fit 72 KB (4 segments per SM at 120K: 52 KB)
     const int L4 = (max_L + 3) & ~3, K4 = (max_k + 3) & ~3;

@@ -379,17 +379,24 @@ __global__ void __launch_bounds__(256, KS_MINB) km_seed_v2_kernel(const SegDesc*
         const float4* row = reinterpret_cast<const float4*>(P + (size_t)i * d) + h;
         const float4* cv = reinterpret_cast<const float4*>(cent) + h;
         float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-        float4 xv[16];
+        // two batches of 8 slices in flight (16 at once spilled to local
+        // memory under the 64-register budget of 4 segments per SM)
 #pragma unroll
-        for (int q = 0; q < 16; q++) xv[q] = q < nq ? __ldcg(row + 2 * q) : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int q0 = 0; q0 < 16; q0 += 8) {
+          if (q0 >= nq) break;
+          float4 xv[8];
 #pragma unroll
-        for (int q = 0; q < 16; q++) {
-          if (q >= nq) break;
-          const float4 x = xv[q], y = cv[2 * q];
-          a0 = __fmaf_rn(x.x, y.x, a0);
-          a1 = __fmaf_rn(x.y, y.y, a1);
-          a2 = __fmaf_rn(x.z, y.z, a2);
-          a3 = __fmaf_rn(x.w, y.w, a3);
+          for (int q = 0; q < 8; q++)
+            xv[q] = q0 + q < nq ? __ldcg(row + 2 * (q0 + q)) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int q = 0; q < 8; q++) {
+            if (q0 + q >= nq) break;
+            const float4 x = xv[q], y = cv[2 * (q0 + q)];
+            a0 = __fmaf_rn(x.x, y.x, a0);
+            a1 = __fmaf_rn(x.y, y.y, a1);
+            a2 = __fmaf_rn(x.z, y.z, a2);
+            a3 = __fmaf_rn(x.w, y.w, a3);
+          }
         }
         // lane h = 0 holds a0..a3, h = 1 holds a4..a7: s_l = a_l + a_{l+4}
         const unsigned pm = both & (0x3u << (lane & ~1));
@@ -471,6 +478,308 @@ __global__ void __launch_bounds__(256, KS_MINB) km_seed_v2_kernel(const SegDesc*
   if (threadIdx.x == 0)
     for (int i = 0; i < 4; i++) g_seed_ts[blockIdx.x * 4 + i] = ks_acc[i];
   if (threadIdx.x == 0) g_seed_ts[8192 * 4 - 1 - blockIdx.x] = ks_nact;
+#endif
+}
+
+// ---------------------------------------------------------------------------
+// phase 2 (v3): k-means++ seeding with ONE WARP per segment.  The 511 steps of
+// a segment are a serial chain whose floor is the reference's sequential fp32
+// cumsum (8,124 dependent FADDs per step, clustering.py:35); v2 gave every
+// segment a 256-thread CTA, so only 4 chains ran per SM and each step paid ~5
+// block barriers plus their memory round trips (343 ms for the 1,920 segments
+// of a 120K-context layer).  Here the segments run side by side (a 120K layer
+// is one wave of ~13 warps per SM), every phase is warp-synchronous, and the
+// arithmetic is v2's exactly (same bounds, same fp16 first pass, same recipe
+// dots, same checkpointed cumsum / searchsorted):
+//   * centre: one 16-byte slice per lane; earlier-centre distance bounds: one
+//     lane per earlier centre;
+//   * triangle test over all rows (lane-strided), survivors compacted by ballot;
+//   * row pass: 16 rows per warp iteration, 2 lanes per row (the recipe split);
+//   * cumsum: the warp stages 256 md values at a time into shared memory
+//     (coalesced, the next block's loads in flight while lane 0 adds the
+//     current one) and lane 0 runs the FADD chain from 16-byte smem reads.
+// md / best / the compacted list live in the global scratch (L2-resident).
+// grid = ceil(n_segments / KS3_W), block = 32 KS3_W, dyn smem = KS3_W * (d + K4 + KS_CK + 256) floats
+// ---------------------------------------------------------------------------
+constexpr int KS3_W = 4;  // segments (warps) per CTA
+__global__ void __launch_bounds__(KS3_W * 32, 4) km_seed_v3_kernel(const SegDesc* __restrict__ segs, int n_segs,
+                                                                    const float* __restrict__ P_all,
+                                                                    float* __restrict__ C_all,
+                                                                    float* __restrict__ scratch_all, int d,
+                                                                    int blas_threads,
+                                                                    const __half* __restrict__ P16_all, int max_k) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int K4 = (max_k + 3) & ~3;
+  extern __shared__ __align__(16) float sm3[];
+  float* cent = sm3 + (size_t)warp * (d + K4 + KS_CK + 256);
+  float* ccd = cent + d;
+  float* ck = ccd + K4;
+  float* stg = ck + KS_CK;  // 256 staged md values
+  const int sgi = blockIdx.x * KS3_W + warp;
+  if (sgi >= n_segs) return;
+  const SegDesc sg = segs[sgi];
+  if (sg.k <= 1) return;
+  const int L = sg.L;
+  float* md = scratch_all + (size_t)sg.p_off * 2;
+  unsigned short* best = reinterpret_cast<unsigned short*>(md + L);
+  unsigned short* lst = best + L;
+  const float* P = P_all + (size_t)sg.p_off * d;
+  const __half* P16 = P16_all ? P16_all + (size_t)sg.p_off * d : nullptr;
+  float* C = C_all + (size_t)sg.c_off * d;
+  Pcg64 g;
+  long long idx = 0;
+  if (lane == 0) {
+    g.hi = sg.rng[0]; g.lo = sg.rng[1]; g.ihi = sg.rng[2]; g.ilo = sg.rng[3];
+    g.has32 = 0; g.u32 = 0;
+    idx = pcg_integers(g, L);
+  }
+  idx = __shfl_sync(0xffffffffu, idx, 0);
+  const int h = lane & 1, rsub = lane >> 1;
+  const int nq = d >> 3;
+  const unsigned lt = (1u << lane) - 1u;
+#ifdef WK_SEED_TIMING
+  long long ks_acc[4] = {0, 0, 0, 0}, ks_t = clock64();
+#define KS3_LAP(q) do { const long long n_ = clock64(); ks_acc[q] += n_ - ks_t; ks_t = n_; } while (0)
+#else
+#define KS3_LAP(q) do {} while (0)
+#endif
+  for (int c = 0; c < sg.k; c++) {
+    for (int t = lane * 4; t < d; t += 128) {
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(P + (size_t)idx * d + t));
+      *reinterpret_cast<float4*>(cent + t) = v;
+      *reinterpret_cast<float4*>(C + (size_t)c * d + t) = v;
+    }
+    __syncwarp();
+    if (c == sg.k - 1) break;
+    // lower bounds of ||C[a] - cent|| (v2's formula and margin)
+    for (int a = lane; a < c; a += 32) {
+      const float4* cr = reinterpret_cast<const float4*>(C + (size_t)a * d);
+      float dp0 = 0.f, dp1 = 0.f;
+      for (int q0 = 0; q0 < (d >> 2); q0 += 8) {
+        float4 x[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) x[j] = q0 + j < (d >> 2) ? __ldcg(cr + q0 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+          if (q0 + j >= (d >> 2)) break;
+          const float4 y = reinterpret_cast<const float4*>(cent)[q0 + j];
+          dp0 = fmaf(x[j].x, y.x, dp0); dp1 = fmaf(x[j].y, y.y, dp1);
+          dp0 = fmaf(x[j].z, y.z, dp0); dp1 = fmaf(x[j].w, y.w, dp1);
+        }
+      }
+      ccd[a] = sqrtf(fmaxf(0.f, 2.f * (1.f - (dp0 + dp1) - KS_EPS)));
+    }
+    __syncwarp();
+    KS3_LAP(0);
+    // triangle test over every row; survivors compacted (ascending order)
+    // (order of the survivors is irrelevant: each row's update is its own).
+    // Batches of 16 rows per lane with every load issued first: the loop is
+    // bound by load latency otherwise (one L2 round trip per 32 rows).
+    int nact = 0;
+    constexpr int CB = 16;
+    for (int i0 = 0; i0 < L; i0 += 32 * CB) {
+      float m[CB];
+      unsigned short bb[CB];
+#pragma unroll
+      for (int q = 0; q < CB; q++) {
+        const int i = i0 + 32 * q + lane;
+        m[q] = 0.f;
+        bb[q] = 0;
+        if (i < L && c > 0) { m[q] = __ldcg(md + i); bb[q] = __ldcg(best + i); }
+      }
+#pragma unroll
+      for (int q = 0; q < CB; q++) {
+        const int i = i0 + 32 * q + lane;
+        bool act = i < L;
+        if (act && c > 0) {
+          const float rh = sqrtf(2.f * (m[q] + KS_EPS)), dl = ccd[bb[q]];
+          if (dl > rh && 0.5f * (dl - rh) * (dl - rh) >= m[q] + KS_EPS) act = false;
+        }
+        const unsigned am = __ballot_sync(0xffffffffu, act);
+        if (act) {
+          lst[nact + __popc(am & lt)] = (unsigned short)i;
+          // the row pass reads this row's fp16 copy next: bring it to L2 now
+          const char* r16 = reinterpret_cast<const char*>(P16 ? (const void*)(P16 + (size_t)i * d)
+                                                              : (const void*)(P + (size_t)i * d));
+          for (int o = 0; o < (P16 ? 2 : 4) * d; o += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(r16 + o));
+        }
+        nact += __popc(am);
+      }
+    }
+    __syncwarp();
+    KS3_LAP(1);
+    // row pass (v2's arithmetic), in two sweeps so the fp32 rows are fetched
+    // to L2 while the fp16 filter runs: (1) fp16 first pass over the active
+    // rows, survivors re-compacted into lst (positions already consumed) with
+    // an L2 prefetch of their fp32 rows; (2) the recipe-exact dot + update
+    int n2 = nact;
+    if (c > 0 && P16) {
+      n2 = 0;
+      int inext = rsub < nact ? (int)__ldcg(lst + rsub) : 0;
+      for (int base = 0; base < nact; base += 16) {
+        const int j = base + rsub;
+        bool act = j < nact;
+        const int i = inext;
+        inext = j + 16 < nact ? (int)__ldcg(lst + j + 16) : 0;
+        float mdi = 0.f;
+        if (act) {
+          mdi = __ldcg(md + i);
+          const uint4* r16 = reinterpret_cast<const uint4*>(P16 + (size_t)i * d) + h * (nq / 2);
+          float a = 0.f;
+          uint4 wv[8];
+#pragma unroll
+          for (int q = 0; q < 8; q++) wv[q] = q < nq / 2 ? __ldcg(r16 + q) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+          for (int q = 0; q < 8; q++) {
+            if (q >= nq / 2) break;
+            const uint4 w = wv[q];
+            const __half2* hh = reinterpret_cast<const __half2*>(&w);
+            const float* cc = cent + h * (d / 2) + 8 * q;
+#pragma unroll
+            for (int e2 = 0; e2 < 4; e2++) {
+              const float2 f = __half22float2(hh[e2]);
+              a = fmaf(f.x, cc[2 * e2], a);
+              a = fmaf(f.y, cc[2 * e2 + 1], a);
+            }
+          }
+          const unsigned pm16 = __activemask() & (0x3u << (lane & ~1));
+          a += __shfl_xor_sync(pm16, a, 1);
+          const float vq = 1.0f - a;
+          // v' - 1e-3 >= md proves min(md, v) == md (no update)
+          if (vq - 1e-3f >= mdi) act = false;
+        }
+        const bool keep = act && h == 0;
+        const unsigned km = __ballot_sync(0xffffffffu, keep);
+        if (keep) {
+          lst[n2 + __popc(km & lt)] = (unsigned short)i;
+          const char* rp = reinterpret_cast<const char*>(P + (size_t)i * d);
+          for (int o = 0; o < 4 * d; o += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(rp + o));
+        }
+        n2 += __popc(km);
+      }
+      __syncwarp();
+    }
+    {
+      int inext = rsub < n2 ? (int)__ldcg(lst + rsub) : 0;
+      for (int base = 0; base < n2; base += 16) {
+        const int j = base + rsub;
+        const bool act = j < n2;
+        const int i = inext;
+        inext = j + 16 < n2 ? (int)__ldcg(lst + j + 16) : 0;
+        const int cls = act ? gemv_row_class(i, L, d, blas_threads) : 0;
+        float dot = 0.f;
+        const unsigned both = __ballot_sync(0xffffffffu, act && cls == 0);
+        if (act && cls == 0) {
+          const float4* row = reinterpret_cast<const float4*>(P + (size_t)i * d) + h;
+          const float4* cv = reinterpret_cast<const float4*>(cent) + h;
+          float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+          for (int q0 = 0; q0 < 16; q0 += 8) {
+            if (q0 >= nq) break;
+            float4 xv[8];
+#pragma unroll
+            for (int q = 0; q < 8; q++)
+              xv[q] = q0 + q < nq ? __ldcg(row + 2 * (q0 + q)) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+              if (q0 + q >= nq) break;
+              const float4 x = xv[q], y = cv[2 * (q0 + q)];
+              a0 = __fmaf_rn(x.x, y.x, a0);
+              a1 = __fmaf_rn(x.y, y.y, a1);
+              a2 = __fmaf_rn(x.z, y.z, a2);
+              a3 = __fmaf_rn(x.w, y.w, a3);
+            }
+          }
+          const unsigned pm = both & (0x3u << (lane & ~1));
+          const float b0 = __shfl_xor_sync(pm, a0, 1), b1 = __shfl_xor_sync(pm, a1, 1);
+          const float b2 = __shfl_xor_sync(pm, a2, 1), b3 = __shfl_xor_sync(pm, a3, 1);
+          const float s0 = __fadd_rn(a0, b0), s1 = __fadd_rn(a1, b1), s2 = __fadd_rn(a2, b2), s3 = __fadd_rn(a3, b3);
+          dot = __fadd_rn(0.f, __fadd_rn(__fadd_rn(s0, s1), __fadd_rn(s2, s3)));
+        } else if (act && h == 0) {
+          dot = sgemv_row(P + (size_t)i * d, cent, d, cls);
+        }
+        if (act && h == 0) {
+          float v = __fsub_rn(1.0f, dot);
+          v = v < 0.f ? 0.f : v;
+          if (c == 0 || !(__ldcg(md + i) <= v)) { md[i] = v; best[i] = (unsigned short)c; }
+        }
+      }
+    }
+    __syncwarp();
+    KS3_LAP(2);
+    // the sequential fp32 cumsum (clustering.py:35), checkpoint every KS_CKS
+    // elements; blocks of 256 staged through shared memory by the whole warp
+    // (the next block's loads in flight while lane 0 adds the current one)
+    const int cks = KS_CKS * ((L + 8191) / 8192);
+    float sacc = 0.f;
+    {
+      float nxt[8];
+      auto fetch = [&](int b0) {
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+          const int i = b0 + lane + 32 * q;
+          nxt[q] = i < L ? __ldcg(md + i) : 0.f;
+        }
+      };
+      fetch(0);
+      for (int b0 = 0; b0 < L; b0 += 256) {
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 8; q++) stg[lane + 32 * q] = nxt[q];
+        __syncwarp();
+        if (b0 + 256 < L) fetch(b0 + 256);
+        if (lane == 0) {
+          const int nb = min(256, L - b0);
+          if (nb == 256 && (cks % 4) == 0) {
+#pragma unroll 2
+            for (int q = 0; q < 256; q += KS_CKS) {
+              if (((b0 + q) % cks) == 0) ck[(b0 + q) / cks] = sacc;
+              float v[KS_CKS];
+#pragma unroll
+              for (int e = 0; e < KS_CKS / 4; e++) {
+                const float4 x = reinterpret_cast<const float4*>(stg + q)[e];
+                v[4 * e] = x.x; v[4 * e + 1] = x.y; v[4 * e + 2] = x.z; v[4 * e + 3] = x.w;
+              }
+#pragma unroll
+              for (int e = 0; e < KS_CKS; e++) sacc = __fadd_rn(sacc, v[e]);
+            }
+          } else {
+            for (int q = 0; q < nb; q++) {
+              if (((b0 + q) % cks) == 0) ck[(b0 + q) / cks] = sacc;
+              sacc = __fadd_rn(sacc, stg[q]);
+            }
+          }
+        }
+      }
+    }
+    if (lane == 0) {
+      long long nidx;
+      if (sacc <= 0.0f) {
+        nidx = pcg_integers(g, L);
+      } else {
+        const float u = (float)pcg_next_double(g);
+        const float thr = __fmul_rn(u, sacc);
+        int lo = 0, hi = (L - 1) / cks;  // last checkpoint <= thr (ck[0] = 0 <= thr)
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (ck[mid] <= thr) lo = mid; else hi = mid - 1;
+        }
+        float s2 = ck[lo];
+        int i = lo * cks;
+        for (; i < L; i++) {
+          s2 = __fadd_rn(s2, __ldcg(md + i));
+          if (s2 > thr) break;
+        }
+        nidx = i > L - 1 ? L - 1 : i;
+      }
+      idx = nidx;
+    }
+    idx = __shfl_sync(0xffffffffu, idx, 0);
+    KS3_LAP(3);
+  }
+#ifdef WK_SEED_TIMING
+  if (lane == 0)
+    for (int q = 0; q < 4; q++) g_seed_ts[sgi * 4 + q] = ks_acc[q];
 #endif
 }
 

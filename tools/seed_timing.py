@@ -29,10 +29,9 @@ L.wk_seed_timing.argtypes = [ctypes.c_void_p, ctypes.c_int]
 n = U * 15
 ts = np.zeros(8192 * 4, np.int64)
 assert L.wk_seed_timing(ts.ctypes.data, ts.size) == 0
-nact = ts[::-1][:n]
-ts = ts[:n * 4].reshape(n, 4)[:, [0, 3, 1, 2]]
+ts = ts[:n * 4].reshape(n, 4)
 tot = ts.sum(1)
 print(f"build {dt:.3f} s ({U * 122812 / dt / 1e6:.1f} M tok/s); per-segment seeding cycles median {np.median(tot):.0f}")
-for i, nm in enumerate(["centre bounds (ccd)", "row compaction", "row pass (active rows)", "cumsum + draw"]):
+for i, nm in enumerate(["centre + bounds (ccd)", "row compaction", "row pass (active rows)", "cumsum + draw"]):
     print(f"  {nm:22s} median {np.median(ts[:, i]):10.0f}  ({np.median(ts[:, i] / tot) * 100:.1f}%)")
-print(f"active rows per step (median over segments of the per-segment mean): {np.median(nact) / 511:.0f} of 8124")
+
