@@ -832,6 +832,24 @@ WK_DEVINL float ktc_exact(const float* __restrict__ p, const float* __restrict__
   for (int t = 0; t < d; t++) acc = __fmaf_rn(__ldg(p + t), __ldg(c + t), acc);
   return acc;
 }
+// four candidates' sequential fp32 FMA chains side by side (the same bits as
+// ktc_exact per candidate; the chains' latencies overlap instead of adding up)
+WK_DEVINL void ktc_exact4(const float* __restrict__ p, const float* __restrict__ c0, const float* __restrict__ c1,
+                          const float* __restrict__ c2, const float* __restrict__ c3, int d, float (&out)[4]) {
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+  for (int t0 = 0; t0 < d; t0 += 4) {
+    const float4 pv = __ldg(reinterpret_cast<const float4*>(p + t0));
+    const float4 x0 = __ldg(reinterpret_cast<const float4*>(c0 + t0));
+    const float4 x1 = __ldg(reinterpret_cast<const float4*>(c1 + t0));
+    const float4 x2 = __ldg(reinterpret_cast<const float4*>(c2 + t0));
+    const float4 x3 = __ldg(reinterpret_cast<const float4*>(c3 + t0));
+    a0 = __fmaf_rn(pv.x, x0.x, a0); a1 = __fmaf_rn(pv.x, x1.x, a1); a2 = __fmaf_rn(pv.x, x2.x, a2); a3 = __fmaf_rn(pv.x, x3.x, a3);
+    a0 = __fmaf_rn(pv.y, x0.y, a0); a1 = __fmaf_rn(pv.y, x1.y, a1); a2 = __fmaf_rn(pv.y, x2.y, a2); a3 = __fmaf_rn(pv.y, x3.y, a3);
+    a0 = __fmaf_rn(pv.z, x0.z, a0); a1 = __fmaf_rn(pv.z, x1.z, a1); a2 = __fmaf_rn(pv.z, x2.z, a2); a3 = __fmaf_rn(pv.z, x3.z, a3);
+    a0 = __fmaf_rn(pv.w, x0.w, a0); a1 = __fmaf_rn(pv.w, x1.w, a1); a2 = __fmaf_rn(pv.w, x2.w, a2); a3 = __fmaf_rn(pv.w, x3.w, a3);
+  }
+  out[0] = a0; out[1] = a1; out[2] = a2; out[3] = a3;
+}
 
 template <int KS>
 __global__ void __launch_bounds__(128) km_assign_tc_kernel(const SegDesc* __restrict__ segs,
@@ -1159,16 +1177,28 @@ __global__ void __launch_bounds__(256, 1) km_assign_tc5_kernel(const SegDesc* __
   float best = -INFINITY;
   int bi = 0x7fffffff;
   if (tv[3] >= lim) {
-    for (int c = 0; c < sg.k; c++) {
-      const float v = ktc_exact(pr, C + (size_t)c * d, d);
-      if (v > best) { best = v; bi = c; }
+    // more than four candidates within the margin: every centroid, four at a time
+    for (int c = 0; c < sg.k; c += 4) {
+      float v4[4];
+      const float* cb = C + (size_t)c * d;
+      ktc_exact4(pr, cb, c + 1 < sg.k ? cb + d : cb, c + 2 < sg.k ? cb + 2 * d : cb, c + 3 < sg.k ? cb + 3 * d : cb,
+                 d, v4);
+#pragma unroll
+      for (int i = 0; i < 4; i++)
+        if (c + i < sg.k && v4[i] > best) { best = v4[i]; bi = c + i; }
     }
   } else {
+    // the (<= 4) candidates' chains side by side (slots past the last
+    // candidate repeat the first and are ignored)
+    float v4[4];
+    const float* cc[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) cc[i] = C + (size_t)((tv[i] >= lim) ? ti[i] : ti[0]) * d;
+    ktc_exact4(pr, cc[0], cc[1], cc[2], cc[3], d, v4);
 #pragma unroll
     for (int i = 0; i < 4; i++) {
       if (!(tv[i] >= lim)) break;
-      const float v = ktc_exact(pr, C + (size_t)ti[i] * d, d);
-      if (v > best || (v == best && ti[i] < bi)) { best = v; bi = ti[i]; }
+      if (v4[i] > best || (v4[i] == best && ti[i] < bi)) { best = v4[i]; bi = ti[i]; }
     }
     if (bi == 0x7fffffff) bi = ti[0];
   }
