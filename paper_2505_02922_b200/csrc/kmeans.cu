@@ -598,10 +598,11 @@ __global__ void __launch_bounds__(KS3_W * 32, 4) km_seed_v3_kernel(const SegDesc
         const unsigned am = __ballot_sync(0xffffffffu, act);
         if (act) {
           lst[nact + __popc(am & lt)] = (unsigned short)i;
-          // the row pass reads this row's fp16 copy next: bring it to L2 now
+#ifdef KS3_PF16  // experiment: L2 prefetch of the survivors' fp16 rows
           const char* r16 = reinterpret_cast<const char*>(P16 ? (const void*)(P16 + (size_t)i * d)
                                                               : (const void*)(P + (size_t)i * d));
           for (int o = 0; o < (P16 ? 2 : 4) * d; o += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(r16 + o));
+#endif
         }
         nact += __popc(am);
       }
@@ -621,6 +622,9 @@ __global__ void __launch_bounds__(KS3_W * 32, 4) km_seed_v3_kernel(const SegDesc
         bool act = j < nact;
         const int i = inext;
         inext = j + 16 < nact ? (int)__ldcg(lst + j + 16) : 0;
+        // the next iteration's fp16 rows to L2 (each lane of a pair: its half)
+        if (j + 16 < nact)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(P16 + (size_t)inext * d) + h * d));
         float mdi = 0.f;
         if (act) {
           mdi = __ldcg(md + i);
