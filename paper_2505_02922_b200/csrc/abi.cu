@@ -5,6 +5,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdio.h>
 #include <string.h>
 
 #include <mutex>
@@ -63,8 +64,10 @@ template <int D, int HS>
 int attend_v6_warps();
 template <int D, int HS>
 int attend_v6_consumers();
+template <int D, int HS>
+int attend_v6_chunk_rows();
 template <bool FULL, int DL>
-__global__ void att6_merge_kernel(SteadyView, StepView, AttnParams, const int32_t*, int, int, int, int);
+__global__ void att6_merge_kernel(SteadyView, StepView, AttnParams, const int32_t*, int, int, int, int, int);
 __global__ void km_assign_tc5_kernel(const SegDesc*, const float*, const float*, int32_t*, const __nv_bfloat16*);
 __global__ void km_pack_c5_kernel(const SegDesc*, const float*, __nv_bfloat16*);
 constexpr int KS_CK = 8192 / 32 + 4;  // km_seed_v2 cumsum checkpoint slots (kmeans.cu)
@@ -318,7 +321,10 @@ static int launch_attend_v6(const IndexView& ix, const SteadyView& st, const Ste
   memset(&tm, 0, sizeof(tm));
   if (!FULL && ix.VS32) {
     const int rc = vs_tensor_map(ix.VS32, (long long)U * ix.m_cap, D, &tm);
-    if (rc) return rc;
+    if (rc) {
+      fprintf(stderr, "wavekv: value-sum tensor map (%lld rows) could not be encoded\n", (long long)U * ix.m_cap);
+      return rc;
+    }
   }
   const size_t sm = attend_v6_smem<D, HS>();
   static PerDevice cfg;
@@ -329,11 +335,14 @@ static int launch_attend_v6(const IndexView& ix, const SteadyView& st, const Ste
     cfg.mark();
   }
   const int warps = attend_v6_warps<D, HS>(), nc = attend_v6_consumers<D, HS>();
-  if (launch_ex(attend_v6_kernel<D, HS, FULL, OFF, ROWS>, dim3(P), dim3(warps * 32), sm, s, 1, ix, st, sv, p,
-                n_store, U, tm) != cudaSuccess || cudaGetLastError() != cudaSuccess)
+  const cudaError_t el = launch_ex(attend_v6_kernel<D, HS, FULL, OFF, ROWS>, dim3(P), dim3(warps * 32), sm, s, 1, ix,
+                                   st, sv, p, n_store, U, tm);
+  if (el != cudaSuccess) {
+    fprintf(stderr, "wavekv: attend_v6 launch (smem %zu): %s\n", sm, cudaGetErrorString(el));
     return WK_ECUDA;
+  }
   const cudaError_t e = launch_ex(att6_merge_kernel<FULL, D / 32>, dim3(U * p.G), dim3(128), 0, s, 1, st, sv, p,
-                                  n_store, U, P, nc, ROWS ? 1 : 0);
+                                  n_store, U, P, nc, ROWS ? 1 : 0, attend_v6_chunk_rows<D, HS>());
   return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? 0 : WK_ECUDA;
 }
 

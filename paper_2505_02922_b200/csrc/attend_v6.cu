@@ -33,10 +33,43 @@
 namespace wk {
 
 __device__ __align__(128) unsigned char g_zero6[8192];
+#ifdef ATT6_DEBUG  // hang / accounting diagnostics (experiment builds only)
+}  // namespace wk
+#include <cstdio>
+namespace wk {
+WK_DEVINL void dbg_wait(uint32_t bar, uint32_t phase, int tag, int i) {
+  long long spins = 0;
+  while (true) {
+    uint32_t ok;
+    asm volatile("{\n.reg .pred P1;\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\nselp.u32 %0, 1, 0, P1;\n}\n"
+                 : "=r"(ok) : "r"(bar), "r"(phase) : "memory");
+    if (ok) return;
+    if (++spins == (1ll << 22)) {
+      printf("att6 hang: block %d warp %d %s chunk %d phase %u\n", blockIdx.x, threadIdx.x >> 5, tag ? "full" : "empty", i, phase);
+      asm volatile("trap;");
+    }
+  }
+}
+#endif
+#ifdef ATT6_TIMING  // tools/att6_timing.py: per-warp cycles waiting vs working (experiment builds only)
+__device__ long long g_att6_ts[148 * 16 * 4];
+extern "C" int wk_att6_timing(long long* host, int n) {
+  return cudaMemcpyFromSymbol(host, g_att6_ts, sizeof(long long) * (size_t)n) == cudaSuccess ? 0 : -2;
+}
+#define A6_T(v) long long v = clock64()
+#define A6_ADD(acc, t0) acc += clock64() - (t0)
+#else
+#define A6_T(v) do {} while (0)
+#define A6_ADD(acc, t0) do {} while (0)
+#endif
 
 template <int D, int HS>
 struct Att6Cfg {
-  static constexpr int RG = 16;               // rows per chunk (mma K of p.v)
+#ifndef ATT6_CH
+#define ATT6_CH 16  // 32-row chunks measured no faster (74-77 us) and fault with > 8 stages (unresolved)
+#endif
+  static constexpr int CH = ATT6_CH;          // rows per chunk (producer / ring granularity)
+  static constexpr int RG = 16;               // rows per consumer sub-chunk (mma K of p.v)
   static constexpr int KS = D / 16;           // q.k k-steps == p.v m-tiles
   static constexpr int NT = HS == 4 ? 2 : 3;  // q.k n-tiles (head x split columns)
   static constexpr int NL = HS == 4 ? 2 : 4;  // (row, head) logit slots per lane
@@ -44,7 +77,7 @@ struct Att6Cfg {
   static constexpr int NA = KS * 4;           // accumulator floats per lane
   static constexpr int ROWT = D * 2;          // bf16 K / V row bytes
   static constexpr int ROWV = D * 4;          // fp32 value-sum row bytes
-  static constexpr int SB = 2 * RG * ROWT > RG * ROWV ? 2 * RG * ROWT : RG * ROWV;  // stage bytes
+  static constexpr int SB = 2 * CH * ROWT > CH * ROWV ? 2 * CH * ROWT : CH * ROWV;  // stage bytes
 #ifndef ATT6_NP
 #define ATT6_NP 4  // tuning experiments only (tools/att6_sweep.sh)
 #endif
@@ -54,17 +87,23 @@ struct Att6Cfg {
   static constexpr int NP = ATT6_NP;          // producer warps
   static constexpr int NC = ATT6_NC;          // consumer warps
   static constexpr int WARPS = NP + NC;
-  static constexpr int L = 8;                 // producer meta lookahead (chunks)
-  // stage meta (producer -> consumers): tag int4 | (mask | key << 8) u16[16] |
-  // estimation logits f32[16][8] | sizes f32[16]
-  static constexpr int SM_TAG = 0, SM_MK = 16, SM_EX = 48, SM_ESZ = 48 + 16 * 8 * 4;
-  static constexpr int SM = ((SM_ESZ + 64) + 127) / 128 * 128;
+#ifndef ATT6_L
+#define ATT6_L 8
+#endif
+  static constexpr int L = ATT6_L;            // producer meta lookahead (chunks)
+  // stage meta (producer -> consumers): tag int4 | (mask | key << 8) u16[CH] |
+  // estimation logits f32[CH][8] | sizes f32[CH]
+  static constexpr int SM_TAG = 0, SM_MK = 16, SM_EX = (16 + 2 * CH + 15) / 16 * 16, SM_ESZ = SM_EX + CH * 8 * 4;
+  static constexpr int SM = ((SM_ESZ + 4 * CH) + 127) / 128 * 128;
   static constexpr int CS = 3 * 8 * RG * 2 + RG * HS * 4;  // consumer scratch: split weights | fp32 weights
-  static constexpr int PR = L * (16 + 64);                 // producer ring: desc int4 + 16 row ids
+  static constexpr int PR = L * (16 + 4 * CH);             // producer ring: desc int4 + CH row ids
   static constexpr int MAXU = 1024;
   static constexpr int FIXED = NC * CS + NP * PR + (MAXU + 1) * 4 + 64 + 128;
   static constexpr int S_FIT = (227 * 1024 - FIXED) / (SB + SM + 16);
-  static constexpr int S = S_FIT > 24 ? 24 : S_FIT;        // ring stages per CTA
+#ifndef ATT6_SMAX
+#define ATT6_SMAX 24
+#endif
+  static constexpr int S = S_FIT > ATT6_SMAX ? ATT6_SMAX : S_FIT;  // ring stages per CTA (D = 128, CH = 32: 12)
   static constexpr size_t SMEM = (size_t)S * (SB + SM + 16) + FIXED;
 };
 
@@ -90,7 +129,7 @@ __global__ void __launch_bounds__(Att6Cfg<D, HS>::WARPS * 32, 1)
     attend_v6_kernel(IndexView ix, SteadyView st, StepView sv, AttnParams p, const int32_t* __restrict__ n_store,
                      int U, const __grid_constant__ CUtensorMap tm_vs) {
   using CF = Att6Cfg<D, HS>;
-  constexpr int RG = CF::RG, KS = CF::KS, NT = CF::NT, NL = CF::NL, NH = CF::NH, NA = CF::NA;
+  constexpr int CH = CF::CH, RG = CF::RG, KS = CF::KS, NT = CF::NT, NL = CF::NL, NH = CF::NH, NA = CF::NA;
   constexpr int ROWT = CF::ROWT, ROWV = CF::ROWV, SB = CF::SB, SMT = CF::SM, S = CF::S, NP = CF::NP,
                 NC = CF::NC, L = CF::L;
   constexpr int DL = D / 16;  // estimation mode: dims per lane
@@ -116,7 +155,7 @@ __global__ void __launch_bounds__(Att6Cfg<D, HS>::WARPS * 32, 1)
       int c = 0;
       if (u < U) {
         int c0, c1, c2;
-        att6_counts<RG, FULL, ROWS>(st, sv, n_store, u, c0, c1, c2);
+        att6_counts<CH, FULL, ROWS>(st, sv, n_store, u, c0, c1, c2);
         c = c0 + c1 + c2;
       }
       int x = c;
@@ -154,19 +193,20 @@ __global__ void __launch_bounds__(Att6Cfg<D, HS>::WARPS * 32, 1)
 
   if (warp < NP) {
     // =========================== producer ===========================
-#if ATT6_NP == 4 && ATT6_NC == 8 && !defined(ATT6_NO_SMR)
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 80;\n" ::: "memory");  // registers to the consumers
-#endif
     const int pw = warp;
+#ifdef ATT6_TIMING
+    long long tw_acc = 0;
+    const long long tp0 = clock64();
+#endif
     unsigned char* ring = pring + pw * CF::PR;
     int4* rdesc = reinterpret_cast<int4*>(ring);            // [L] (u, kind + 1 | n << 8, a, lc)
-    int* rids = reinterpret_cast<int*>(ring + L * 16);      // [L][16]
+    int* rids = reinterpret_cast<int*>(ring + L * 16);      // [L][CH]
     const uint32_t rids_s = smem_u32(rids);
     // cursor over units (chunk indices visited in increasing order); the unit's
     // sizes stay in registers (no global load per chunk on the producer's chain)
     int iu = 0, ic0 = 0, ic1 = 0, ic2 = 0, in_st = 0, in_x = 0, in_e = 0;
     auto unit_sizes = [&]() {
-      att6_counts<RG, FULL, ROWS>(st, sv, n_store, iu, ic0, ic1, ic2);
+      att6_counts<CH, FULL, ROWS>(st, sv, n_store, iu, ic0, ic1, ic2);
       in_st = st.n[iu];
       in_x = FULL ? n_store[iu] : (ROWS ? sv.cnt[iu * 4 + 1] : 0);
       in_e = FULL ? 0 : sv.cnt[iu * 4 + 2];
@@ -194,29 +234,29 @@ __global__ void __launch_bounds__(Att6Cfg<D, HS>::WARPS * 32, 1)
         int kind, n, a = 0;
         if (lc < ic0) {
           kind = 0;
-          a = lc * RG;
-          n = min(RG, in_st - a);
+          a = lc * CH;
+          n = min(CH, in_st - a);
         } else if (lc < ic0 + ic1) {
           kind = 1;
           lc -= ic0;
           if (FULL) {
-            a = lc * RG;
-            n = min(RG, in_x - a);
+            a = lc * CH;
+            n = min(CH, in_x - a);
           } else if (ROWS) {
-            a = lc * RG;
-            n = min(RG, in_x - a);
-            if (lane < n) cp_async4(rids_s + ((k % L) * 16 + lane) * 4, sv.rtok_row + (size_t)u * sv.rt_cap + a + lane);
+            a = lc * CH;
+            n = min(CH, in_x - a);
+            if (lane < n) cp_async4(rids_s + ((k % L) * CH + lane) * 4, sv.rtok_row + (size_t)u * sv.rt_cap + a + lane);
           } else {  // offload piece (row, n | mask << 8 | flags << 16, cluster, first token)
             n = 0;    // from the piece
             if (lane == 0)
-              cp_async16_ca(rids_s + (k % L) * 64, reinterpret_cast<const int4*>(sv.pieces) + (size_t)u * sv.pc_cap + lc);
+              cp_async16_ca(rids_s + (k % L) * CH * 4, reinterpret_cast<const int4*>(sv.pieces) + (size_t)u * sv.pc_cap + lc);
           }
         } else {
           kind = 2;
           lc -= ic0 + ic1;
-          a = lc * RG;
-          n = min(RG, in_e - a);
-          if (lane < n) cp_async4(rids_s + ((k % L) * 16 + lane) * 4, sv.eu_ids + (size_t)u * sv.eu_cap + a + lane);
+          a = lc * CH;
+          n = min(CH, in_e - a);
+          if (lane < n) cp_async4(rids_s + ((k % L) * CH + lane) * 4, sv.eu_ids + (size_t)u * sv.eu_cap + a + lane);
         }
         if (lane == 0) rdesc[k % L] = make_int4(u, (kind + 1) | (n << 8), a, lc);
       }
@@ -232,7 +272,17 @@ __global__ void __launch_bounds__(Att6Cfg<D, HS>::WARPS * 32, 1)
       const int4 dsc = rdesc[slot];
       const int u = dsc.x, kind = (dsc.y & 0xff) - 1;
       int n = (dsc.y >> 8) & 0xff;
+#ifdef ATT6_TIMING
+      const long long tw0 = clock64();
+#endif
+#ifdef ATT6_DEBUG
+      if (i >= S) dbg_wait(empty_s + s * 8, (uint32_t)(((i / S) - 1) & 1), 0, i);
+#else
       if (i >= S) mbar_wait_s(empty_s + s * 8, (uint32_t)(((i / S) - 1) & 1));
+#endif
+#ifdef ATT6_TIMING
+      tw_acc += clock64() - tw0;
+#endif
       const uint32_t stg = sdata_s + s * SB, bar = full_s + s * 8;
       unsigned char* meta = smeta + (size_t)s * SMT;
       int wt_z = 0, wt_w = 0;
@@ -240,7 +290,7 @@ __global__ void __launch_bounds__(Att6Cfg<D, HS>::WARPS * 32, 1)
         int row, mk;
         const unsigned char* bk;
         const unsigned char* bv;
-        const int j = lane & 15;
+        const int j = lane;  // chunk row (CH == 32) / lanes >= n: unused
         if (kind == 0) {
           row = dsc.z + j;
           mk = allmask;
@@ -252,13 +302,13 @@ __global__ void __launch_bounds__(Att6Cfg<D, HS>::WARPS * 32, 1)
           bk = (const unsigned char*)ix.store_k + (size_t)u * ix.s_cap * ROWT;
           bv = (const unsigned char*)ix.store_v + (size_t)u * ix.s_cap * ROWT;
         } else if (ROWS) {
-          const int w = rids[slot * 16 + j];
+          const int w = rids[slot * CH + (j & (CH - 1))];
           row = w & 0xffffff;
           mk = (int)((unsigned)w >> 24);
           bk = (const unsigned char*)ix.store_k + (size_t)u * ix.s_cap * ROWT;
           bv = (const unsigned char*)ix.store_v + (size_t)u * ix.s_cap * ROWT;
         } else {
-          const int4 pc = reinterpret_cast<const int4*>(rids)[slot * 4];
+          const int4 pc = reinterpret_cast<const int4*>(rids)[slot * CH / 4];
           n = pc.y & 0xff;
           row = pc.x + j;
           mk = (pc.y >> 8) & 0xff;
@@ -274,7 +324,7 @@ __global__ void __launch_bounds__(Att6Cfg<D, HS>::WARPS * 32, 1)
         }
         const bool live = lane < n;
         // meta first (generic stores), then the barrier's expect_tx, then the copies
-        if (lane < RG)
+        if (lane < CH)
           reinterpret_cast<unsigned short*>(meta + CF::SM_MK)[lane] =
               (unsigned short)(live ? (mk | ((row & 7) << 8)) : ((lane & 7) << 8));
         if (lane == 0) *reinterpret_cast<int4*>(meta + CF::SM_TAG) = make_int4(u, (kind + 1) | (n << 8), wt_z, wt_w);
@@ -282,26 +332,35 @@ __global__ void __launch_bounds__(Att6Cfg<D, HS>::WARPS * 32, 1)
         const bool start = live && (lane == 0 || row != prev + 1);
         const unsigned starts = __ballot_sync(0xffffffffu, start);
         __syncwarp();
-        if (lane == 0) mbar_expect_s(bar, (uint32_t)((n + RG) * ROWT));
+        if (lane == 0) mbar_expect_s(bar, (uint32_t)((n + CH) * ROWT));
         __syncwarp();
+#ifdef ATT6_DEBUG
+        {
+          int lsum = 0;
+          if (start) { const unsigned later = starts & ~((2u << lane) - 1u); lsum = (later ? __ffs(later) - 1 : n) - lane; }
+          for (int o = 16; o; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+          if (lane == 0 && (lsum != n || n <= 0 || n > CH))
+            printf("att6 runs: block %d chunk %d kind %d n %d sum %d\n", blockIdx.x, i, kind, n, lsum);
+        }
+#endif
         if (start) {
           const unsigned later = starts & ~((2u << lane) - 1u);
           const int len = (later ? __ffs(later) - 1 : n) - lane;
           bulk_g2s_s(stg + lane * ROWT, bk + (size_t)row * ROWT, (uint32_t)(len * ROWT), bar);
-          bulk_g2s_s(stg + RG * ROWT + lane * ROWT, bv + (size_t)row * ROWT, (uint32_t)(len * ROWT), bar);
+          bulk_g2s_s(stg + CH * ROWT + lane * ROWT, bv + (size_t)row * ROWT, (uint32_t)(len * ROWT), bar);
         }
         // V rows >= n zero-filled (a zero weight never meets a stale non-finite value)
-        if (lane == 0 && n < RG) bulk_g2s_s(stg + RG * ROWT + n * ROWT, g_zero6, (uint32_t)((RG - n) * ROWT), bar);
+        if (lane == 0 && n < CH) bulk_g2s_s(stg + CH * ROWT + n * ROWT, g_zero6, (uint32_t)((CH - n) * ROWT), bar);
       } else {
         if (lane == 0) *reinterpret_cast<int4*>(meta + CF::SM_TAG) = make_int4(u, (kind + 1) | (n << 8), 0, 0);
         __syncwarp();
         if (lane == 0) {
-          const uint32_t exb = (uint32_t)(RG * G * 4);
-          mbar_expect_s(bar, (uint32_t)(RG * ROWV) + exb + 64u);
-          const int4* id4 = reinterpret_cast<const int4*>(rids + slot * 16);
+          const uint32_t exb = (uint32_t)(CH * G * 4);
+          mbar_expect_s(bar, (uint32_t)(CH * ROWV) + exb + 4u * CH);
+          const int4* id4 = reinterpret_cast<const int4*>(rids + slot * CH);
           const int rb = u * (int)ix.m_cap;
 #pragma unroll
-          for (int g4 = 0; g4 < 4; g4++) {
+          for (int g4 = 0; g4 < CH / 4; g4++) {
             const int4 c = id4[g4];
             const int b = 4 * g4;
             tma_gather4(stg + b * ROWV, &tm_vs, 0, b < n ? rb + c.x : -1, b + 1 < n ? rb + c.y : -1,
@@ -309,20 +368,23 @@ __global__ void __launch_bounds__(Att6Cfg<D, HS>::WARPS * 32, 1)
           }
           // logits [16][G] and sizes [16] of the rows (rows >= n: ignored by the consumers)
           bulk_g2s_s(smeta_s + s * SMT + CF::SM_EX, sv.eu_x + ((size_t)u * sv.eu_cap + dsc.z) * G, exb, bar);
-          bulk_g2s_s(smeta_s + s * SMT + CF::SM_ESZ, sv.eu_sz + (size_t)u * sv.eu_cap + dsc.z, 64u, bar);
+          bulk_g2s_s(smeta_s + s * SMT + CF::SM_ESZ, sv.eu_sz + (size_t)u * sv.eu_cap + dsc.z, 4u * CH, bar);
         }
       }
       __syncwarp();  // this ring slot is consumed: reuse it for chunk k + L
       prefetch(k + L);
     }
     cp_async_wait<0>();
+#ifdef ATT6_TIMING
+    if (lane == 0 && blockIdx.x < 148) {
+      g_att6_ts[(blockIdx.x * 16 + warp) * 4 + 0] = tw_acc;
+      g_att6_ts[(blockIdx.x * 16 + warp) * 4 + 1] = clock64() - tp0;
+    }
+#endif
     return;
   }
 
   // =========================== consumers ===========================
-#if ATT6_NP == 4 && ATT6_NC == 8 && !defined(ATT6_NO_SMR)
-  asm volatile("setmaxnreg.inc.sync.aligned.u32 208;\n" ::: "memory");
-#endif
   const int cw = warp - NP;
   const int g8 = lane >> 2, t4 = lane & 3;      // mma fragment coordinates
   const int half = lane >> 4, sub = lane & 15;  // estimation mode coordinates
@@ -333,6 +395,10 @@ __global__ void __launch_bounds__(Att6Cfg<D, HS>::WARPS * 32, 1)
   __syncwarp();
   const int gw = blockIdx.x * NC + cw;
   const float isd = p.inv_sqrt_d;
+#ifdef ATT6_TIMING
+  long long tw_acc = 0;
+  const long long tp0 = clock64();
+#endif
   auto slot_row = [&](int l) { return g8 + 8 * (HS == 4 ? l : (l >> 1)); };
   auto slot_head = [&](int l) { return HS == 4 ? t4 : 2 * t4 + (l & 1); };
 
@@ -475,10 +541,12 @@ __global__ void __launch_bounds__(Att6Cfg<D, HS>::WARPS * 32, 1)
     }
   };
 
-  auto compute = [&](int s, int kind, int n) {
+  // one 16-row sub-chunk (rows r0 .. r0 + 15 of the stage's chunk)
+  auto compute = [&](int s, int kind, int n, int r0) {
     const uint32_t stg = sdata_s + s * SB;
     const unsigned char* meta = smeta + (size_t)s * SMT;
-    const unsigned short* mk16 = reinterpret_cast<const unsigned short*>(meta + CF::SM_MK);
+    const unsigned short* mk16 = reinterpret_cast<const unsigned short*>(meta + CF::SM_MK) + r0;
+    n -= r0;
     float x[NL], pw[NL];
     if (kind < 2) {
       // q.k: S^T = K . Qs^T (two accumulator sets halve the dependent MMA chain)
@@ -489,7 +557,7 @@ __global__ void __launch_bounds__(Att6Cfg<D, HS>::WARPS * 32, 1)
         for (int i = 0; i < 4; i++) c[nt][i] = c2[nt][i] = 0.f;
       const int jk = (lane & 7) + ((lane >> 3) & 1) * 8;
       const int kbk = ((mk16[jk] >> 8) & 7) ^ (lane >> 4);
-      const uint32_t aK = stg + jk * ROWT;
+      const uint32_t aK = stg + (r0 + jk) * ROWT;
       uint32_t ak[KS][4];
 #pragma unroll
       for (int kk = 0; kk < KS; kk++)
@@ -541,7 +609,7 @@ __global__ void __launch_bounds__(Att6Cfg<D, HS>::WARPS * 32, 1)
       }
       const int jv = (lane & 7) + 8 * (lane >> 4);
       const int kbv = ((mk16[jv] >> 8) & 7) ^ ((lane >> 3) & 1);
-      const uint32_t aV = stg + RG * ROWT + jv * ROWT;
+      const uint32_t aV = stg + CH * ROWT + (r0 + jv) * ROWT;
       uint32_t av[KS][4];
 #pragma unroll
       for (int mt = 0; mt < KS; mt++)
@@ -555,8 +623,8 @@ __global__ void __launch_bounds__(Att6Cfg<D, HS>::WARPS * 32, 1)
         }
     } else {
       // estimation rows: fp32 value sums on the FP32 pipes
-      const float* ex = reinterpret_cast<const float*>(meta + CF::SM_EX);
-      const float* esz = reinterpret_cast<const float*>(meta + CF::SM_ESZ);
+      const float* ex = reinterpret_cast<const float*>(meta + CF::SM_EX) + r0 * G;
+      const float* esz = reinterpret_cast<const float*>(meta + CF::SM_ESZ) + r0;
       float wz[NL];
 #pragma unroll
       for (int l = 0; l < NL; l++) {
@@ -574,7 +642,7 @@ __global__ void __launch_bounds__(Att6Cfg<D, HS>::WARPS * 32, 1)
         pe[slot_row(l) * HS + slot_head(l)] = pw[l];
       }
       __syncwarp();
-      const unsigned char* stage = sdata + (size_t)s * SB;
+      const unsigned char* stage = sdata + (size_t)s * SB + (size_t)r0 * ROWV;
       constexpr int RSTEP = HS == 4 ? 2 : 1;
 #pragma unroll 4
       for (int j = (HS == 4 ? half : 0); j < RG; j += RSTEP) {
@@ -610,7 +678,17 @@ __global__ void __launch_bounds__(Att6Cfg<D, HS>::WARPS * 32, 1)
 #pragma unroll 1
   for (int i = cw; i < ncta; i += NC) {
     const int s = i % S;
+#ifdef ATT6_TIMING
+    const long long tw0 = clock64();
+#endif
+#ifdef ATT6_DEBUG
+    dbg_wait(full_s + s * 8, (uint32_t)((i / S) & 1), 1, i);
+#else
     mbar_wait_s(full_s + s * 8, (uint32_t)((i / S) & 1));
+#endif
+#ifdef ATT6_TIMING
+    tw_acc += clock64() - tw0;
+#endif
     const int4 tg = *reinterpret_cast<const int4*>(smeta + (size_t)s * SMT + CF::SM_TAG);
     const int kind = (tg.y & 0xff) - 1, n = (tg.y >> 8) & 0xff;
     if (tg.x != cu || kind != ck) {
@@ -619,7 +697,10 @@ __global__ void __launch_bounds__(Att6Cfg<D, HS>::WARPS * 32, 1)
       ck = kind;
       if (qu != cu) load_q(cu);
     }
-    compute(s, kind, n);
+    for (int r0 = 0; r0 < n; r0 += RG) {
+      if (r0) __syncwarp();  // the split / fp32 weight scratch is rewritten
+      compute(s, kind, n, r0);
+    }
     if (OFF && tg.w < 0) {
       // admitted offload miss: write its rows through into the new slots (re-keyed)
       const int cl = tg.z, j0 = tg.w & 0xffffff;
@@ -637,7 +718,7 @@ __global__ void __launch_bounds__(Att6Cfg<D, HS>::WARPS * 32, 1)
           *reinterpret_cast<uint4*>((unsigned char*)sv.arena_k + arow * ROWT + ((sub ^ ka) << 4)) =
               *reinterpret_cast<const uint4*>(stage + r * ROWT + ((sub ^ ks) << 4));
           *reinterpret_cast<uint4*>((unsigned char*)sv.arena_v + arow * ROWT + ((sub ^ ka) << 4)) =
-              *reinterpret_cast<const uint4*>(stage + RG * ROWT + r * ROWT + ((sub ^ ks) << 4));
+              *reinterpret_cast<const uint4*>(stage + CH * ROWT + r * ROWT + ((sub ^ ks) << 4));
         }
       }
     }
@@ -646,6 +727,12 @@ __global__ void __launch_bounds__(Att6Cfg<D, HS>::WARPS * 32, 1)
   }
   pdl_trigger<4>();
   flush();
+#ifdef ATT6_TIMING
+  if (lane == 0 && blockIdx.x < 148) {
+    g_att6_ts[(blockIdx.x * 16 + warp) * 4 + 0] = tw_acc;
+    g_att6_ts[(blockIdx.x * 16 + warp) * 4 + 1] = clock64() - tp0;
+  }
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -656,8 +743,7 @@ __global__ void __launch_bounds__(Att6Cfg<D, HS>::WARPS * 32, 1)
 template <bool FULL, int DL>
 __global__ void __launch_bounds__(128) att6_merge_kernel(SteadyView st, StepView sv, AttnParams p,
                                                           const int32_t* __restrict__ n_store, int U, int P,
-                                                          int NC, int rows_mode) {
-  constexpr int RG = 16;
+                                                          int NC, int rows_mode, int RG) {
   pdl_wait();
   pdl_trigger<8>();
   const int G = p.G, d = p.d, D2 = 4 + d;
@@ -861,6 +947,8 @@ template <int D, int HS>
 int attend_v6_warps() { return Att6Cfg<D, HS>::WARPS; }
 template <int D, int HS>
 int attend_v6_consumers() { return Att6Cfg<D, HS>::NC; }
+template <int D, int HS>
+int attend_v6_chunk_rows() { return Att6Cfg<D, HS>::CH; }
 
 #define WK_INST_ATT6(D, HS)                                                                                   \
   template __global__ void attend_v6_kernel<D, HS, false, false, true>(                                        \
@@ -871,14 +959,15 @@ int attend_v6_consumers() { return Att6Cfg<D, HS>::NC; }
       IndexView, SteadyView, StepView, AttnParams, const int32_t*, int, const __grid_constant__ CUtensorMap);  \
   template size_t attend_v6_smem<D, HS>();                                                                    \
   template int attend_v6_warps<D, HS>();                                                                      \
-  template int attend_v6_consumers<D, HS>();
+  template int attend_v6_consumers<D, HS>();                                                                  \
+  template int attend_v6_chunk_rows<D, HS>();
 WK_INST_ATT6(128, 4)
 WK_INST_ATT6(128, 8)
 WK_INST_ATT6(64, 4)
 WK_INST_ATT6(64, 8)
-template __global__ void att6_merge_kernel<false, 4>(SteadyView, StepView, AttnParams, const int32_t*, int, int, int, int);
-template __global__ void att6_merge_kernel<true, 4>(SteadyView, StepView, AttnParams, const int32_t*, int, int, int, int);
-template __global__ void att6_merge_kernel<false, 2>(SteadyView, StepView, AttnParams, const int32_t*, int, int, int, int);
-template __global__ void att6_merge_kernel<true, 2>(SteadyView, StepView, AttnParams, const int32_t*, int, int, int, int);
+template __global__ void att6_merge_kernel<false, 4>(SteadyView, StepView, AttnParams, const int32_t*, int, int, int, int, int);
+template __global__ void att6_merge_kernel<true, 4>(SteadyView, StepView, AttnParams, const int32_t*, int, int, int, int, int);
+template __global__ void att6_merge_kernel<false, 2>(SteadyView, StepView, AttnParams, const int32_t*, int, int, int, int, int);
+template __global__ void att6_merge_kernel<true, 2>(SteadyView, StepView, AttnParams, const int32_t*, int, int, int, int, int);
 
 }  // namespace wk

@@ -174,8 +174,8 @@ class WaveLayer:
         self.nr = torch.zeros(U, dtype=i32, device=dev)
         self.ne = torch.zeros(U, dtype=i32, device=dev)
         self.ru_cap = min(self.m_cap, G * self.r_cap)
-        # multiple of 16: attend_v6 copies estimation logits / sizes 16 rows at a time
-        self.eu_cap = -(-min(self.m_cap, G * self.e_cap) // 16) * 16
+        # multiple of 32: attend_v6 copies estimation logits / sizes a chunk (<= 32 rows) at a time
+        self.eu_cap = -(-min(self.m_cap, G * self.e_cap) // 32) * 32
         self.ru_ids = torch.zeros((U, self.ru_cap), dtype=i32, device=dev)
         self.ru_mask = torch.zeros((U, self.ru_cap), dtype=torch.uint8, device=dev)
         self.eu_ids = torch.zeros((U, self.eu_cap), dtype=i32, device=dev)
