@@ -15,6 +15,8 @@ from __future__ import annotations
 
 import ctypes
 import datetime
+import json
+import os
 import time
 
 import numpy as np
@@ -197,3 +199,41 @@ def oracle_trace(trace: TraceFile, *, device="cuda") -> np.ndarray:
         w = torch.exp(s - s.max(dim=1, keepdim=True).values)
         out[t] = (torch.einsum("hn,hnd->hd", w, V[:, : n + t + 1]) / w.sum(1, keepdim=True)).cpu().numpy()
     return out
+
+
+# ---------------------------------------------------------------------------
+# config sweeps (cli.py:19-24 SWEEP_AXES, cmd_sweep cli.py:84-97)
+# ---------------------------------------------------------------------------
+SWEEP_AXES = {
+    "retrieval_fraction": float,
+    "estimation_fraction": float,
+    "segment_size": int,
+    "cache_fraction": float,
+}
+
+
+def sweep_trace(trace: TraceFile, base: EngineConfig, axis: str, values, with_oracle: bool = False,
+                out_dir: str | None = None, *, device="cuda", blas_threads: int | None = None):
+    """Replay `trace` once per value of one config axis (tierkv's `sweep`
+    command): each report is run_trace's with "sweep": {"axis", "value"}; with
+    out_dir, written as report_<axis>_<value>.json like the reference.  `values`
+    is a list or the reference's comma-separated string.  Returns the reports."""
+    if axis not in SWEEP_AXES:
+        raise ConfigError(f"unknown sweep axis {axis!r}; choose from {sorted(SWEEP_AXES)}")
+    cast = SWEEP_AXES[axis]
+    raws = [v.strip() for v in values.split(",")] if isinstance(values, str) else [str(v) for v in values]
+    reports = []
+    if out_dir:
+        os.makedirs(out_dir, exist_ok=True)
+    for raw in raws:
+        value = cast(raw)
+        cfg = EngineConfig.from_dict({**base.to_dict(), axis: value})
+        report, _, _ = run_trace(trace, cfg, with_oracle=with_oracle, device=device, blas_threads=blas_threads)
+        report["sweep"] = {"axis": axis, "value": value}
+        if out_dir:
+            with open(os.path.join(out_dir, f"report_{axis}_{raw}.json"), "w") as f:
+                json.dump(report, f, indent=2, sort_keys=True, allow_nan=False)
+                f.write("\n")
+        reports.append(report)
+    return reports
+

@@ -18,6 +18,40 @@ def _cuda():
         pytest.skip("needs a CUDA device")
 
 
+def _compare_reports(rep, ref, name):
+    """the fields tierkv's report pins bit-for-bit / to the stated tolerances"""
+    assert rep["config"] == ref["config"] and rep["trace"] == ref["trace"]
+    assert rep["schema_version"] == ref["schema_version"]
+    for mine, theirs in zip(rep["per_head"], ref["per_head"]):
+        assert mine["head"] == theirs["head"]
+        for k in ("hits", "misses", "bytes_slow_to_fast", "bytes_fast_internal", "m", "r", "e"):
+            assert mine["steps"][k] == theirs["steps"][k], (name, mine["head"], k)
+        assert np.allclose(mine["steps"]["recall"], theirs["steps"]["recall"], atol=1e-6)
+        for k in ("hits", "misses", "hit_ratio", "bytes_slow_to_fast", "bytes_fast_internal", "capacity_blocks",
+                  "occupied_blocks", "bytes_offloaded", "slow_blocks", "clusters"):
+            assert mine["totals"][k] == theirs["totals"][k], (name, k)
+    for k in ("cumulative_hit_ratio", "total_bytes_slow_to_fast", "total_bytes_fast_internal",
+              "total_bytes_offloaded"):
+        assert rep["aggregates"][k] == ref["aggregates"][k], k
+    assert rep["aggregates"]["mean_recall"] == pytest.approx(ref["aggregates"]["mean_recall"], abs=1e-6)
+
+
+def test_sweep_matches_reference_reports():
+    """tierkv's `sweep` command (cli.py:84-97) over two axes of trace_a vs
+    runner.sweep_trace (oracle/make_sweep_golden.py)."""
+    from paper_2505_02922_b200 import EngineConfig
+    from paper_2505_02922_b200.runner import sweep_trace
+    from paper_2505_02922_b200.tracefile import read_trace
+    gold = json.load(open(os.path.join(GOLD, "sweep_trace_a.json")))
+    tr = read_trace(os.path.join(GOLD, "trace_a.wkt"))
+    for axis, values in gold["sweeps"]:
+        reps = sweep_trace(tr, EngineConfig(), axis, values, blas_threads=gold["blas_threads"])
+        for raw, rep in zip(values.split(","), reps):
+            ref = gold["reports"][f"report_{axis}_{raw}.json"]
+            assert rep["sweep"] == ref["sweep"]
+            _compare_reports(rep, ref, f"{axis}={raw}")
+
+
 @pytest.mark.parametrize("name", ["trace_a", "trace_b"])
 def test_run_trace_matches_reference_report(name):
     from paper_2505_02922_b200 import EngineConfig

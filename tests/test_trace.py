@@ -93,3 +93,15 @@ def test_validate_rejects_inconsistent_shapes():
         TraceFile(d=4, prefill_keys=tr.prefill_keys, prefill_values=tr.prefill_values, queries=tr.queries,
                   new_keys=tr.new_keys[:1], new_values=tr.new_values).validate()
     assert struct.calcsize("<4sIIIQQ") == HEADER.size == 32
+
+
+def test_sweep_rejects_unknown_axis():
+    """runner.sweep_trace mirrors cli.py's SWEEP_AXES (cli.py:19-24): any other
+    axis is a ConfigError before anything runs."""
+    import pytest
+    from paper_2505_02922_b200 import EngineConfig
+    from paper_2505_02922_b200.errors import ConfigError
+    from paper_2505_02922_b200.runner import SWEEP_AXES, sweep_trace
+    assert sorted(SWEEP_AXES) == ["cache_fraction", "estimation_fraction", "retrieval_fraction", "segment_size"]
+    with pytest.raises(ConfigError):
+        sweep_trace(None, EngineConfig(), "kmeans_iters", "5,10")
