@@ -346,9 +346,40 @@ class WaveLayer:
     # --------------------------------------------------------------- clustering
     def _run_segments(self, segs: list[dict]):
         """Cluster + finalize + pack a list of segments (one wk_kmeans_segments
-        call per chunk bounded by a scratch budget)."""
+        call per chunk bounded by a scratch budget).
+
+        Offload layers: the pack writes the cluster-contiguous K/V straight into
+        the pinned host store over the host link (engine.py:133-135, store.py:88),
+        so the segments are split into unit groups launched alternately on two
+        streams -- group g's host writes (km_finalize) overlap group g + 1's
+        clustering."""
         d = self.d
         budget = 1 << 26  # points per chunk (scratch ~ 0.6 KB/point at d=128)
+        groups = 4 if (self.offload and len(segs) >= 32) else 1
+        if groups > 1:
+            units = sorted({s["unit"] for s in segs})
+            cut = [units[len(units) * g // groups] for g in range(groups)] + [units[-1] + 1]
+            main = torch.cuda.current_stream()
+            streams = [torch.cuda.Stream(device=self.dev) for _ in range(2)]
+            start = torch.cuda.Event()
+            start.record(main)
+            keep = []  # scratch of every group alive until both streams drained
+            for g in range(groups):
+                part = [s for s in segs if cut[g] <= s["unit"] < cut[g + 1]]
+                st = streams[g % 2]
+                st.wait_event(start)
+                with torch.cuda.stream(st):
+                    keep += self._run_segments_chunked(part, budget, sync=False)
+            for st in streams:
+                main.wait_stream(st)
+            torch.cuda.synchronize(self.dev)
+            del keep
+            return
+        self._run_segments_chunked(segs, budget, sync=True)
+
+    def _run_segments_chunked(self, segs: list[dict], budget: int, sync: bool):
+        d = self.d
+        keep = []
         i = 0
         while i < len(segs):
             chunk, tot = [], 0
@@ -385,8 +416,12 @@ class WaveLayer:
                 max(max(1, s["k"]) for s in chunk), ctypes.c_void_p(_stream()))
             _lib.check(rc, "wk_kmeans_segments")
             # keep scratch alive until the kernels ran
-            torch.cuda.current_stream().synchronize()
-            del P, P16, C, A, perm, sims, md, segs_dev
+            if sync:
+                torch.cuda.current_stream().synchronize()
+                del P, P16, C, A, perm, sims, md, segs_dev
+            else:
+                keep.append((P, P16, C, A, perm, sims, md, segs_dev, arr))
+        return keep
 
     # ------------------------------------------------------------------ prefill
     def prefill(self, keys: torch.Tensor, values: torch.Tensor, lengths=None):
