@@ -229,21 +229,35 @@ def run_reference(a):
         return
     cores = os.cpu_count() or 1
     steps = max(1, a.steps)
+    hq, hkv, d, n_layers = MODELS[a.model]
+    layers = a.layers if a.layers > 0 else n_layers
     with mp.get_context("spawn").Pool(cores) as pool:
         t0 = time.perf_counter()
         per = pool.map(_cpu_worker, [(a.ctx, steps, s) for s in range(cores)])
         wall = time.perf_counter() - t0
+    # per[i]: seconds per unit-step (one q-head at full context) on core i;
+    # a token of one request is hq x layers unit-steps
     unit_steps_per_s = sum(1.0 / p for p in per)
-    tok_s = unit_steps_per_s / (HQ * a.layers)
+    tok_s = unit_steps_per_s / (hq * layers)
+    world = max(1, a.gpus)
+    cfg_name = "configs[1]" if a.model == "llama3-8b" else "configs[4]"
     line = {"impl": "reference", "metric": METRIC,
             "value": tok_s, "unit": "tokens/s", "n_gpus": a.gpus, "steps": steps,
-            "warmup": a.warmup, "ms_per_step": a.batch / tok_s * 1e3, "higher_is_better": True,
+            # one step of the bounded sample: every core runs one unit-step
+            "warmup": a.warmup, "ms_per_step": max(per) * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{a.model}-shape {a.layers}-layer decode, {a.ctx // 1024}K ctx, batch {a.batch}",
-                       "batch": a.batch, "ctx": a.ctx, "layers": a.layers},
+            # the wave arm's config of the same arguments (same workload)
+            "config": {"workload": f"{a.model}-shape {layers}-layer decode, {a.ctx // 1024}K ctx, "
+                                   f"batch {a.batch} ({cfg_name})",
+                       "model_shape": a.model, "batch_per_gpu": a.batch, "global_batch": a.batch * world,
+                       "units_this_rank": a.batch * hkv, "ctx": a.ctx, "layers": layers,
+                       "layer_buffers": min(a.layer_bufs, layers), "heads": f"{hq}q/{hkv}kv", "d": d,
+                       "l2": "inputs larger than L2 (each layer buffer >> 126 MB, cycled)"},
+            "full_step_ms_extrapolated": a.batch * world / tok_s * 1e3,
             "cpu_baseline": {"value": tok_s, "unit": "tokens/s", "cores": cores, "kind": "port",
                              "sample": f"{cores} x one q-head unit at {a.ctx} ctx, {steps} decode "
-                                       "steps each (prefill untimed); extrapolated x32 heads x32 layers"},
+                                       f"steps each (prefill untimed); a step of the sample is {cores} "
+                                       f"unit-steps in parallel; extrapolated x{hq} heads x{layers} layers"},
             "e2e": {"value": tok_s, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "wall_s": wall}
     print(json.dumps(line), flush=True)
