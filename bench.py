@@ -868,7 +868,8 @@ def main():
                                "clocks"))),
                          ("build", lambda: run_build(a, torch, dev, log)),
                          ("offload", lambda: run_offload(a, torch, dev, log, ctx=1048576, batch=4, layer_bufs=2,
-                                                         steps=3, warmup=2))):
+                                                         steps=3, warmup=2)),
+                         ("index_update", lambda: run_update_cost(a, torch, dev, log, step_ms=line["ms_per_step"]))):
             try:
                 t0 = time.perf_counter()
                 extras[name] = fn()
@@ -881,6 +882,50 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_update_cost(a, torch, dev, log, step_ms=None):
+    """The decode-time index update at the configs[1] scale (ClusterIndex.update,
+    index.py:168-186): one 120K layer of B x H_kv units decodes until its buffer
+    holds update_segment + local_window tokens, then one update (k-means of the
+    oldest 1,024 buffer tokens of every unit, finalize + pack, buffer shift) is
+    timed.  Each layer updates once per 1,024 steps, so the amortised cost per
+    decode step is layers x update / 1,024."""
+    from paper_2505_02922_b200 import EngineConfig, WaveLayer
+    cfg = EngineConfig()
+    ic = cfg.index
+    hq, hkv, d, n_layers = MODELS["llama3-8b"]
+    U, G = a.batch * hkv, hq // hkv
+    keys, vals, cen = gen_layer(torch, U, a.ctx, d, 5, dev)
+    lay = WaveLayer(cfg, U, G, d, max_prefill=a.ctx, max_decode=2 * ic.update_segment, store_dtype=torch.bfloat16)
+    lay.prefill(keys, vals)
+    del keys, vals
+    torch.cuda.empty_cache()
+    s0 = lay.units[0]
+    need = ic.update_segment + ic.local_window - (s0.n_steady - s0.n_sink)
+    qs = gen_queries(torch, cen, G, 4, 3)
+    kv = torch.randn((2, U, d), device=dev).bfloat16().float()
+    for i in range(max(0, need)):
+        lay.decode(qs[i % 4], kv[0], kv[1], allow_update=False)
+    torch.cuda.synchronize()
+    assert lay.needs_update()
+    m0 = s0.m
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    e0.record()
+    lay.maybe_update()
+    e1.record()
+    torch.cuda.synchronize()
+    wall_ms = (time.perf_counter() - t0) * 1e3
+    lay.check_status("index update")
+    per_step = n_layers * wall_ms / ic.update_segment
+    log(f"index update: {wall_ms:.1f} ms for {U} units (+{s0.m - m0} clusters each)")
+    return {"what": "one ClusterIndex.update of a 120K layer (every unit: k-means of the oldest "
+                    f"{ic.update_segment} buffer tokens, k={s0.m - m0}, finalize + pack, buffer shift)",
+            "units": U, "update_ms_wall": wall_ms, "update_ms_device": e0.elapsed_time(e1),
+            "decode_steps_between_updates": ic.update_segment,
+            "amortised_ms_per_step": per_step,
+            "fraction_of_step": (per_step / step_ms) if step_ms else None}
 
 
 def host_info():

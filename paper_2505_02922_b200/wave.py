@@ -551,26 +551,47 @@ class WaveLayer:
             tmp_k = torch.empty((len(todo), ic.update_segment, self.d), dtype=torch.float32,
                                 device=self.dev)
             tmp_v = torch.empty_like(tmp_k)
+            sinks = {self.units[u].n_sink for u in todo}
+            batched = len(sinks) == 1
+            if batched:  # one gather for all units (the common case)
+                r0 = next(iter(sinks))
+                idx = torch.tensor(todo, device=self.dev, dtype=torch.long)
+                tmp_k.copy_(self._from_rows(self.st_k[idx, r0:r0 + ic.update_segment], r0))
+                tmp_v.copy_(self._from_rows(self.st_v[idx, r0:r0 + ic.update_segment], r0))
             for j, u in enumerate(todo):
                 s = self.units[u]
                 if s.m + k > self.m_cap or s.store_fill + ic.update_segment > self.s_cap:
                     raise ConfigError("index capacity exceeded: raise max_decode")
                 r0 = s.n_sink
-                tmp_k[j] = self._from_rows(self.st_k[u, r0:r0 + ic.update_segment], r0)
-                tmp_v[j] = self._from_rows(self.st_v[u, r0:r0 + ic.update_segment], r0)
+                if not batched:
+                    tmp_k[j] = self._from_rows(self.st_k[u, r0:r0 + ic.update_segment], r0)
+                    tmp_v[j] = self._from_rows(self.st_v[u, r0:r0 + ic.update_segment], r0)
                 base = j * ic.update_segment * self.d
                 segs.append(dict(keys=tmp_k.data_ptr() + 4 * base, values=tmp_v.data_ptr() + 4 * base,
                                  stride=self.d, L=ic.update_segment, k=k, unit=u, cid_base=s.m,
                                  row_base=s.store_fill, tok_base=s.buffer_start,
                                  rng=pcg64_words(ic.rng_seed, 2, s.update_round)))
             self._run_segments(segs)
+            # keep the buffer tail (index.py:179-180): shift rows down.  Units
+            # with the same (sink, steady) extent are shifted by one batched
+            # copy; the swizzle keys are unchanged when the shift is a multiple
+            # of 8 rows (the default 1,024), else the rows are re-keyed
+            groups = {}
             for u in todo:
                 s = self.units[u]
-                r0, r1 = s.n_sink + ic.update_segment, s.n_steady
-                # keep the buffer tail (index.py:179-180): shift rows down
-                for t in (self.st_k, self.st_v):  # re-keyed to the rows' new positions
-                    t[u, s.n_sink:s.n_sink + (r1 - r0)] = self._to_rows(self._from_rows(t[u, r0:r1], r0), s.n_sink)
-                self.st_tok[u, s.n_sink:s.n_sink + (r1 - r0)] = self.st_tok[u, r0:r1].clone()
+                groups.setdefault((s.n_sink, s.n_steady), []).append(u)
+            rekey = self.swizzled and ic.update_segment % 8 != 0
+            for (n_sink, n_steady), us in groups.items():
+                r0, r1 = n_sink + ic.update_segment, n_steady
+                idx = torch.tensor(us, device=self.dev, dtype=torch.long)
+                for t in (self.st_k, self.st_v):
+                    rows = t[idx, r0:r1]
+                    if rekey:
+                        rows = self._to_rows(self._from_rows(rows, r0), n_sink)
+                    t[idx, n_sink:n_sink + (r1 - r0)] = rows.clone()
+                self.st_tok[idx, n_sink:n_sink + (r1 - r0)] = self.st_tok[idx, r0:r1].clone()
+            for u in todo:
+                s = self.units[u]
                 s.n_steady -= ic.update_segment
                 s.m += k
                 s.store_fill += ic.update_segment
