@@ -26,7 +26,7 @@ __global__ void km_assign_tc_kernel(const SegDesc*, const float*, const float*, 
 __global__ void km_assign_small_kernel(const SegDesc*, const float*, const float*, int32_t*, int);
 __global__ void km_update_kernel(const SegDesc*, const float*, float*, int32_t*, int32_t*, float*, int, int);
 template <typename T>
-__global__ void km_finalize_kernel(const SegDesc*, const int32_t*, int32_t*, IndexView, int, int*);
+__global__ void km_finalize_kernel(const SegDesc*, const int32_t*, int32_t*, IndexView, int, int*, int);
 // decode.cu
 template <typename T>
 __global__ void append_kernel(SteadyView, const float*, const float*, int, int*);
@@ -455,10 +455,15 @@ int wk_kmeans_segments(const wk_index_view* ix, const wk_segment* segs, int n_se
     WK_CHECK_LAUNCH();
   }
   km_update_kernel<<<n_segs, 512, upsmem, s>>>(sd, scr->P, scr->C, scr->A, scr->perm, scr->sims, d, 1);
+  // member lists staged in shared memory when (2k + 1 + L) ints fit the 200 KB opt-in
+  const size_t fsmem = usmem + (size_t)max_L * sizeof(int);
+  const int fin_sp = fsmem <= 200 * 1024 ? 1 : 0;
   if (store_bf16)
-    km_finalize_kernel<__nv_bfloat16><<<n_segs, 256, usmem, s>>>(sd, scr->A, scr->perm, *ix, d, scr->status);
+    km_finalize_kernel<__nv_bfloat16><<<n_segs, 256, fin_sp ? fsmem : usmem, s>>>(sd, scr->A, scr->perm, *ix, d,
+                                                                                scr->status, fin_sp);
   else
-    km_finalize_kernel<float><<<n_segs, 256, usmem, s>>>(sd, scr->A, scr->perm, *ix, d, scr->status);
+    km_finalize_kernel<float><<<n_segs, 256, fin_sp ? fsmem : usmem, s>>>(sd, scr->A, scr->perm, *ix, d,
+                                                                        scr->status, fin_sp);
   WK_CHECK_LAUNCH();
   return 0;
 }

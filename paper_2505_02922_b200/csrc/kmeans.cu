@@ -1440,8 +1440,18 @@ __global__ void km_update_kernel(const SegDesc* __restrict__ segs, const float* 
       int c = idx / d, t = idx % d;
       int b = cnt[c], e = cnt[c + 1];
       if (e > b) {
+        // sequential fp64 sum in member order (bincount, clustering.py:87-91);
+        // eight members' loads issued ahead of their adds
         double s = 0.0;
-        for (int j = b; j < e; j++) s = __dadd_rn(s, (double)P[(size_t)perm[j] * d + t]);
+        int j = b;
+        for (; j + 8 <= e; j += 8) {
+          float pv[8];
+#pragma unroll
+          for (int q = 0; q < 8; q++) pv[q] = P[(size_t)perm[j + q] * d + t];
+#pragma unroll
+          for (int q = 0; q < 8; q++) s = __dadd_rn(s, (double)pv[q]);
+        }
+        for (; j < e; j++) s = __dadd_rn(s, (double)P[(size_t)perm[j] * d + t]);
         C[(size_t)c * d + t] = __double2float_rn(__ddiv_rn(s, (double)(e - b)));
       }
     }
@@ -1498,7 +1508,7 @@ __global__ void km_update_kernel(const SegDesc* __restrict__ segs, const float* 
 template <typename T>
 __global__ void km_finalize_kernel(const SegDesc* __restrict__ segs, const int32_t* __restrict__ A_all,
                                    int32_t* __restrict__ perm_all, IndexView ix, int d,
-                                   int* __restrict__ status) {
+                                   int* __restrict__ status, int fin_smem_perm) {
   const SegDesc sg = segs[blockIdx.x];
   extern __shared__ int smi[];
   int* cnt = smi;
@@ -1533,12 +1543,38 @@ __global__ void km_finalize_kernel(const SegDesc* __restrict__ segs, const int32
     sk[row * d + col] = KV<T>::from_f(sg.keys[src]);
     sv[row * d + col] = KV<T>::from_f(sg.values[src]);
   }
+  // member lists in shared memory when they fit (dynamic smem past cnt / cursor)
+  const int32_t* mem = perm;
+  if (fin_smem_perm) {
+    int* sp = smi + 2 * sg.k + 1;
+    __syncthreads();  // perm complete (stable_bucket)
+    for (int j = threadIdx.x; j < sg.L; j += blockDim.x) sp[j] = perm[j];
+    __syncthreads();
+    mem = sp;
+  }
   for (int idx = threadIdx.x; idx < sg.k * d; idx += blockDim.x) {
     int c = idx / d, t = idx % d;
     int b = cnt[c], e = cnt[c + 1];
     double ks = 0.0, vs = 0.0;
-    for (int j = b; j < e; j++) {
-      size_t src = (size_t)perm[j] * sg.key_stride + t;
+    // the reference's sequential fp64 sums in member order; eight members'
+    // loads issued ahead of their adds (the loop is otherwise latency-bound)
+    int j = b;
+    for (; j + 8 <= e; j += 8) {
+      float kv[8], vv[8];
+#pragma unroll
+      for (int q = 0; q < 8; q++) {
+        const size_t src = (size_t)mem[j + q] * sg.key_stride + t;
+        kv[q] = sg.keys[src];
+        vv[q] = sg.values[src];
+      }
+#pragma unroll
+      for (int q = 0; q < 8; q++) {
+        ks = __dadd_rn(ks, (double)kv[q]);
+        vs = __dadd_rn(vs, (double)vv[q]);
+      }
+    }
+    for (; j < e; j++) {
+      size_t src = (size_t)mem[j] * sg.key_stride + t;
       ks = __dadd_rn(ks, (double)sg.keys[src]);
       vs = __dadd_rn(vs, (double)sg.values[src]);
     }
@@ -1561,7 +1597,7 @@ __global__ void km_finalize_kernel(const SegDesc* __restrict__ segs, const int32
   }
 }
 
-template __global__ void km_finalize_kernel<float>(const SegDesc*, const int32_t*, int32_t*, IndexView, int, int*);
-template __global__ void km_finalize_kernel<__nv_bfloat16>(const SegDesc*, const int32_t*, int32_t*, IndexView, int, int*);
+template __global__ void km_finalize_kernel<float>(const SegDesc*, const int32_t*, int32_t*, IndexView, int, int*, int);
+template __global__ void km_finalize_kernel<__nv_bfloat16>(const SegDesc*, const int32_t*, int32_t*, IndexView, int, int*, int);
 
 }  // namespace wk
