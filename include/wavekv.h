@@ -97,7 +97,10 @@ typedef struct wk_step_view {
   uint8_t* eu_mask;
   int32_t* cnt;       /* [U, 4]                                                 */
   float* tail;        /* [U, G, 4]                                              */
-  float* part;        /* [U, S, G, 3, 2 + d] split partials                     */
+  float* part;        /* partial records: wk_tripartite_attn [12 (S + U), 3, G,
+                         4 + d] (attend_v6 keys consumer x (CTA + unit),
+                         attend_v4 CTA warp + unit); reference kernels
+                         [U, S, G, 3, 2 + d]                                     */
   float* out;         /* [U, G, d] attention output (AttentionOutput.output)    */
   float* logden;      /* [U, G] StepMetrics.log_denominator                     */
   float* cov;         /* [U, G] StepMetrics.denominator_coverage                */

@@ -455,7 +455,10 @@ __global__ void __launch_bounds__(Att6Cfg<D, HS>::WARPS * 32, 1)
       v += __shfl_xor_sync(0xffffffffu, v, 16);
       ds[i] = v;
     }
-    float* base = sv.part + ((size_t)(gw + cu) * 3 + ck) * (size_t)G * (4 + D);
+    // record key gw + NC * u = NC * (CTA + u) + consumer: unique, since a
+    // CTA's units start at or after the previous CTA's last unit (a consumer
+    // takes chunks of several units round-robin, so gw + u would collide)
+    float* base = sv.part + ((size_t)(gw + NC * cu) * 3 + ck) * (size_t)G * (4 + D);
     if (g8 == 0) {
 #pragma unroll
       for (int i = 0; i < NH; i++) {
@@ -788,7 +791,7 @@ __global__ void __launch_bounds__(128) att6_merge_kernel(SteadyView st, StepView
     const long long j0 = x + ((c - x) % NC + NC) % NC;
     return j0 < y;
   };
-  auto rec = [&](int k, int gwi) { return sv.part + (((size_t)(gwi + u) * 3 + k) * G + g) * (size_t)D2; };
+  auto rec = [&](int k, int gwi) { return sv.part + (((size_t)(gwi + NC * u) * 3 + k) * G + g) * (size_t)D2; };
   const int Sw = (S - warp + 3) / 4;
   float mw[3] = {-INFINITY, -INFINITY, -INFINITY}, dw3[3] = {0.f, 0.f, 0.f};
   float nacc[3][DL];

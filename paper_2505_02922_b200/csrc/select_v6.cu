@@ -163,8 +163,9 @@ WK_DEVINL void s6_scan4(int (&v)[4], int (&tot)[4], Sel6Smem<CAND>& sm) {
 //   * pass 2 emits retrieval pieces (runs of <= piece_rows contiguous store
 //     rows of one cluster + head mask) and estimation rows (id, head mask,
 //     size), in (word, bit) order -- the order of a single-CTA union;
-//   * after a cluster barrier, CTA h writes head h's estimation logits
-//     s'(c) / sqrt(d) of every estimation row from its own staged scores.
+//     with every head's logit s'_h(c) / sqrt(d) read from head h's staged
+//     scores (DSMEM); a last cluster barrier keeps the smem alive until the
+//     peers are done with it.
 // ---------------------------------------------------------------------------
 constexpr int S6_TWC = 2048;            // clusters per staging tile
 constexpr int S6_TWW = S6_TWC / 32;     // bitmap words per tile (16 groups)
@@ -307,6 +308,9 @@ __device__ void s6_union_cl(const IndexView& ix, const StepView& sv, const SelPa
   int32_t* eu = sv.eu_ids + (size_t)u * sv.eu_cap;
   uint8_t* emk = sv.eu_mask + (size_t)u * sv.eu_cap;
   float* eusz = sv.eu_sz + (size_t)u * sv.eu_cap;
+  float* eux = sv.eu_x + (size_t)u * sv.eu_cap * G;
+  const float isd = p.inv_sqrt_d;
+  const uint32_t sc_loc = SMS ? (uint32_t)__cvta_generic_to_shared(scs) : 0u;
   int tb[4] = {sm.base[0], sm.base[1], sm.base[2], sm.base[3]};  // running tile base
   const uint32_t lt = (1u << lane) - 1u;
   for (int k = 0; fits && k < ntile; k++) {
@@ -401,6 +405,19 @@ __device__ void s6_union_cl(const IndexView& ix, const StepView& sv, const SelPa
           eu[ie] = c;
           emk[ie] = (uint8_t)mk;
           eusz[ie] = (float)csz[ci];
+          // every head's logit s'_h(c) / sqrt(d) of the row, from head h's
+          // staged scores (peer smem over DSMEM, or the global score rows)
+          float sc[GM];
+#pragma unroll
+          for (int h = 0; h < GM; h++)
+            sc[h] = (h < G && ((mk >> h) & 1))
+                        ? (SMS ? __uint_as_float(dsmem_ld_u32(peer(sc_loc + 4u * (uint32_t)c, h)))
+                               : __ldcg(sv.scores + ((size_t)u * G + h) * ix.m_cap + c))
+                        : 0.f;
+          float* ex = eux + (size_t)ie * G;
+#pragma unroll
+          for (int h = 0; h < GM; h++)
+            if (h < G) ex[h] = (mk >> h) & 1 ? sc[h] * isd : -INFINITY;
         }
         o[3] += __popc(ue);
       }
@@ -409,32 +426,10 @@ __device__ void s6_union_cl(const IndexView& ix, const StepView& sv, const SelPa
 #pragma unroll
     for (int i = 0; i < 4; i++) tb[i] += ttot[i];
   }
-  // ---- head g's estimation logits of every row (own staged scores) ----
+  // peers may still be reading this CTA's staged scores: keep the smem alive
   S6_MARK(10);
-  cl.sync();  // all rows emitted (cluster-scope release / acquire); peers done with this CTA's smem
+  cl.sync();
   S6_MARK(11);
-  if (!fits) return;
-  float* eux = sv.eu_x + (size_t)u * sv.eu_cap * G + g;
-  const float isd = p.inv_sqrt_d;
-  const float* sg = sv.scores + ((size_t)u * G + g) * ix.m_cap;
-  constexpr int UN = 8;
-  for (int i0 = t; i0 < n_eu; i0 += UN * S6_T) {
-    int cc[UN], mm[UN];
-#pragma unroll
-    for (int k = 0; k < UN; k++) {
-      const int i = i0 + k * S6_T;
-      cc[k] = i < n_eu ? __ldcg(eu + i) : 0;
-      mm[k] = i < n_eu ? (int)__ldcg(emk + i) : 0;
-    }
-#pragma unroll
-    for (int k = 0; k < UN; k++) {
-      const int i = i0 + k * S6_T;
-      if (i < n_eu) {
-        const float sc = (mm[k] >> g) & 1 ? (SMS ? scs[cc[k]] : __ldcg(sg + cc[k])) : 0.f;
-        eux[(size_t)i * G] = (mm[k] >> g) & 1 ? sc * isd : -INFINITY;
-      }
-    }
-  }
   S6_MARK(12);
 }
 

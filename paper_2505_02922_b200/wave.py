@@ -211,7 +211,9 @@ class WaveLayer:
         self.eu_x = torch.zeros((U, self.eu_cap, G), dtype=f32, device=dev)
         self.eu_sz = torch.zeros((U, self.eu_cap), dtype=f32, device=dev)
         self.tail = torch.zeros((U, G, 4), dtype=f32, device=dev)
-        n_part = (self.S * self.attn_warps + U) if self.fast else U * self.S
+        # partial records: attend_v4 keys (CTA warp + unit), attend_v6 keys
+        # consumers x (CTA + unit); attn_warps x (S + U) bounds both
+        n_part = self.attn_warps * (self.S + U) if self.fast else U * self.S
         self.part = torch.zeros((n_part, 3, G, (4 + d) if self.fast else (2 + d)), dtype=f32, device=dev)
         self.out = torch.zeros((U, G, d), dtype=f32, device=dev)
         self.logden = torch.zeros((U, G), dtype=f32, device=dev)
@@ -247,7 +249,7 @@ class WaveLayer:
             for gi in range(self.split):
                 u0, u1 = U * gi // self.split, U * (gi + 1) // self.split
                 n = u1 - u0
-                part = torch.zeros((self.S * self.attn_warps + n, 3, G, 4 + d), dtype=f32, device=dev)
+                part = torch.zeros((self.attn_warps * (self.S + n), 3, G, 4 + d), dtype=f32, device=dev)
                 woff = torch.zeros(n + 1, dtype=i32, device=dev)
                 self._groups.append(dict(u0=u0, n=n, part=part, woff=woff,
                                          ixv=self._index_view(u0, u1), stv=self._steady_view(u0, u1)))

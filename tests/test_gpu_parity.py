@@ -120,6 +120,42 @@ def test_batched_gqa_matches_per_head_oracle(Gh, d):
                 assert abs(float(logden[u, g]) - sm.log_denominator) <= LOGDEN_TOL
 
 
+@pytest.mark.parametrize("splits", [3, 7])
+def test_many_units_per_attention_cta(splits):
+    """Few attention CTAs over many units (each CTA's chunk range crosses
+    several unit boundaries, its consumers take chunks of neighbouring units
+    round-robin): every (unit, head) partial record must stay distinct -- the
+    default bench layer (128 units on 148 CTAs) hits the same case.  Every
+    (unit, head) against an independent oracle HeadEngine."""
+    from oracle import oracle as O
+    from paper_2505_02922_b200 import EngineConfig, WaveLayer
+    rng = np.random.default_rng(40 + splits)
+    U, Gh, d, n, steps = 12, 4, 128, 1500, 3
+    cen = rng.standard_normal((30, d)).astype(np.float32)
+    keys = G.bf16_round(cen[rng.integers(30, size=(U, n))] + 0.3 * rng.standard_normal((U, n, d)).astype(np.float32))
+    vals = G.bf16_round(rng.standard_normal((U, n, d)).astype(np.float32))
+    qs = G.bf16_round(rng.standard_normal((steps, U, Gh, d)).astype(np.float32))
+    nk = G.bf16_round(rng.standard_normal((steps, U, d)).astype(np.float32))
+    nv = G.bf16_round(rng.standard_normal((steps, U, d)).astype(np.float32))
+    lay = WaveLayer(EngineConfig(), U, Gh, d, max_prefill=n, max_decode=64, splits=splits)
+    assert lay.S == splits
+    dev = torch.device("cuda")
+    lay.prefill(torch.from_numpy(keys).to(dev), torch.from_numpy(vals).to(dev))
+    orc = [O.OracleEngine().prefill(keys[u], vals[u]) for u in range(U)]
+    orc = [[orc[u]] + [orc[u].clone() for _ in range(Gh - 1)] for u in range(U)]
+    for t in range(steps):
+        out, logden, _ = lay.decode(torch.from_numpy(qs[t]).to(dev), torch.from_numpy(nk[t]).to(dev),
+                                    torch.from_numpy(nv[t]).to(dev))
+        lay.check_status()
+        out = out.double().cpu().numpy()
+        for u in range(U):
+            for g in range(Gh):
+                o_ref, sm = orc[u][g].decode_step(qs[t, u, g], nk[t, u], nv[t, u], with_recall=False)
+                rel = np.linalg.norm(out[u, g] - o_ref) / np.linalg.norm(o_ref)
+                assert rel <= OUT_TOL, (t, u, g, rel)
+                assert abs(float(logden[u, g]) - sm.log_denominator) <= LOGDEN_TOL
+
+
 def test_full_attention_matches_fp64():
     from paper_2505_02922_b200 import EngineConfig, WaveLayer
     rng = np.random.default_rng(5)
