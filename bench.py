@@ -426,13 +426,17 @@ def _ptr(t):
     return t.data_ptr()
 
 
-def parity_sample(lay, keys0, vals0, history, G, log):
+PAR_STEPS = 8  # recorded decode steps of the parity sample
+
+
+def parity_sample(lay, keys0, vals0, history, recs, G, log):
     """Sampled oracle check of the benchmarked layer (outside the timed
     region): unit 0 of layer buffer 0 -- its 120K index (C64, sizes, members)
     bit-exact against the C oracle's prefill of the same keys, then the oracle
-    replays every decode step that buffer saw (G heads) and the last step's
-    ordered retrieval list, output and log-denominator must match
-    (SURVEY 8c bars: ids bit-exact, rel-L2 <= 1e-5, |dlogden| <= 1e-5)."""
+    replays every decode step that buffer saw (G heads) and the ordered
+    retrieval list, output and log-denominator of each recorded step (`recs`:
+    the last PAR_STEPS steps) must match (SURVEY 8c bars: ids bit-exact,
+    rel-L2 <= 1e-5, |dlogden| <= 1e-5)."""
     import numpy as np
     from oracle import oracle as O
     t0 = time.perf_counter()
@@ -447,23 +451,22 @@ def parity_sample(lay, keys0, vals0, history, G, log):
     o, s = int(ix["offsets"][m - 1]), int(ix["sizes"][m - 1])
     index_ok &= bool(np.array_equal(ix["store_tok"][o:o + s], e0.members(m - 1)))
     orcs = [e0] + [e0.clone() for _ in range(G - 1)]
-    outs = []
-    for (q, k, v) in history:
-        outs = [orcs[g].decode_step(q[g], k, v, with_recall=False) for g in range(G)]
-    r = int(lay.nr[0])
-    rl = lay.rlist[0, :, :r].cpu().numpy()
-    out = lay.out[0].double().cpu().numpy()
-    logden = lay.logden[0].cpu().numpy()
+    at = {r[0]: r for r in recs}
     ids_ok, worst, dlog = True, 0.0, 0.0
-    for g in range(G):
-        o_ref, sm = outs[g]
-        r_ref, _ = orcs[g].last_plan()
-        ids_ok &= bool(r == sm.r and np.array_equal(rl[g], r_ref))
-        worst = max(worst, float(np.linalg.norm(out[g] - o_ref) / np.linalg.norm(o_ref)))
-        dlog = max(dlog, abs(float(logden[g]) - sm.log_denominator))
+    for j, (q, k, v) in enumerate(history):
+        outs = [orcs[g].decode_step(q[g], k, v, with_recall=False) for g in range(G)]
+        if j not in at:
+            continue
+        _, out, logden, rl = at[j]
+        for g in range(G):
+            o_ref, sm = outs[g]
+            r_ref, _ = orcs[g].last_plan()
+            ids_ok &= bool(rl.shape[1] == sm.r and np.array_equal(rl[g], r_ref))
+            worst = max(worst, float(np.linalg.norm(out[g] - o_ref) / np.linalg.norm(o_ref)))
+            dlog = max(dlog, abs(float(logden[g]) - sm.log_denominator))
     res = {"what": "unit 0 of layer buffer 0 (the benchmarked layer) vs the C oracle (tierkv's algorithm): "
-                   "index after prefill, then the last of the decode steps it replayed",
-           "m": m, "decode_steps_replayed": len(history), "heads": G,
+                   f"index after prefill, then the last {len(recs)} of the decode steps it replayed",
+           "m": m, "decode_steps_replayed": len(history), "decode_steps_compared": len(recs), "heads": G,
            "index_bit_exact": index_ok, "retrieval_ids_bit_exact": ids_ok,
            "max_rel_l2": worst, "max_abs_dlogden": dlog,
            "pass": bool(index_ok and ids_ok and worst <= 1e-5 and dlog <= 1e-5),
@@ -512,8 +515,8 @@ def run_decode(a, torch, dev, model, log, rank=0, world=1, batch=None, ctx=None,
         torch.cuda.synchronize()
         t_build += time.perf_counter() - t0
         layers.append(lay)
-        qpool.append(gen_queries(torch, cen, G, total_steps * per_buf, 7 + li))
-        kpool.append(torch.randn((total_steps * per_buf, 2, U, d), device=dev).bfloat16().float())
+        qpool.append(gen_queries(torch, cen, G, total_steps * per_buf + PAR_STEPS, 7 + li))
+        kpool.append(torch.randn((total_steps * per_buf + PAR_STEPS, 2, U, d), device=dev).bfloat16().float())
         del keys, vals, cen
         torch.cuda.empty_cache()
         log(f"[{model}] layer buffer {li}: m={lay.units[0].m} build {t_build:.1f}s")
@@ -627,13 +630,27 @@ def run_decode(a, torch, dev, model, log, rank=0, world=1, batch=None, ctx=None,
     # ---- sampled oracle parity of the benchmarked layer (outside the timed region) ----
     par = None
     if keys0 is not None and not a.no_cpu:
-        hist = []
+        # PAR_STEPS more decode steps of layer buffer 0 (untimed), each step's
+        # unit-0 output / log-denominator / retrieval list recorded
         lay0 = layers[0]
+        recs = []
+        for _ in range(PAR_STEPS):
+            j = use[0]
+            use[0] += 1
+            lay0.launch_step(qpool[0][j], kpool[0][j, 0], kpool[0][j, 1])
+            for s_ in lay0.units:
+                s_.total += 1
+                s_.n_steady += 1
+            nr0 = int(lay0.nr[0])
+            recs.append((j, lay0.out[0].double().cpu().numpy(), lay0.logden[0].cpu().numpy(),
+                         lay0.rlist[0, :, :nr0].cpu().numpy()))
+        lay0.check_status("parity steps")
+        hist = []
         for j in range(use[0]):
             hist.append((qpool[0][j][0].double().cpu().numpy(), kpool[0][j, 0][0].cpu().numpy(),
                          kpool[0][j, 1][0].cpu().numpy()))
         try:
-            par = parity_sample(lay0, keys0, vals0, hist, G, log)
+            par = parity_sample(lay0, keys0, vals0, hist, recs, G, log)
         except Exception as exc:  # reported, never silently passed
             par = {"pass": False, "error": repr(exc)}
 
