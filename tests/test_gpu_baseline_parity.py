@@ -313,3 +313,48 @@ def test_recall_with_identical_keys():
         o_ref, m_ref = orc.decode_step(q, k, v, with_recall=True)
         assert met.recall == pytest.approx(m_ref.recall, abs=1e-7)
         assert np.linalg.norm(out - o_ref) <= 1e-5 * np.linalg.norm(o_ref)
+
+
+def test_layer_120k_128_units_every_step():
+    """The benchmarked layer itself (configs[1]: 16 requests x 8 kv-heads =
+    128 units at 120K, bf16 store, bench.py's synthetic generator): units
+    spread over the attention grid (first, middle, last) against independent
+    oracle engines on every one of 6 decode steps.  At this shape every
+    attention CTA's chunk range crosses unit boundaries -- the case the
+    per-unit 120K tests above cannot reach."""
+    import bench
+    from oracle import oracle as O
+    from paper_2505_02922_b200 import EngineConfig, WaveLayer
+    dev = torch.device("cuda")
+    U, G, d, n, steps, threads = 128, 4, 128, 122880, 6, 8
+    keys, vals, cen = bench.gen_layer(torch, U, n, d, 3, dev)
+    lay = WaveLayer(EngineConfig(), U, G, d, max_prefill=n, max_decode=64, blas_threads=threads)
+    lay.prefill(keys, vals)
+    pick = (0, 77, 127)
+    host = {u: (keys[u].cpu().numpy(), vals[u].cpu().numpy()) for u in pick}
+    del keys, vals
+    qs = bench.gen_queries(torch, cen, G, steps, 9)
+    g = torch.Generator(device=dev).manual_seed(10)
+    kv = torch.randn((steps, 2, U, d), generator=g, device=dev).bfloat16().float()
+    orcs = {}
+    for u in pick:
+        e0 = O.OracleEngine(blas_threads=threads).prefill(*host[u])
+        assert lay.units[u].m == e0.m
+        orcs[u] = [e0] + [e0.clone() for _ in range(G - 1)]
+    for t in range(steps):
+        out, logden, _ = lay.decode(qs[t], kv[t, 0], kv[t, 1])
+        lay.check_status()
+        out = out.double().cpu().numpy()
+        logden = logden.cpu().numpy()
+        for u in pick:
+            r = int(lay.nr[u])
+            rl = lay.rlist[u, :, :r].cpu().numpy()
+            q = qs[t, u].double().cpu().numpy()
+            k, v = kv[t, 0, u].cpu().numpy(), kv[t, 1, u].cpu().numpy()
+            for h in range(G):
+                o_ref, sm = orcs[u][h].decode_step(q[h], k, v, with_recall=False)
+                r_ref, _ = orcs[u][h].last_plan()
+                assert r == sm.r and np.array_equal(rl[h], r_ref), (t, u, h)
+                rel = np.linalg.norm(out[u, h] - o_ref) / np.linalg.norm(o_ref)
+                assert rel <= OUT_TOL, (t, u, h, rel)
+                assert abs(float(logden[u, h]) - sm.log_denominator) <= LOGDEN_TOL
