@@ -341,6 +341,9 @@ static int launch_attend_v6(const IndexView& ix, const SteadyView& st, const Ste
     fprintf(stderr, "wavekv: attend_v6 launch (smem %zu): %s\n", sm, cudaGetErrorString(el));
     return WK_ECUDA;
   }
+#ifdef WK_EXP_NO_MERGE  // timing experiment only (tools/exp_bench.py): the merge's share of a step
+  return 0;
+#endif
   const cudaError_t e = launch_ex(att6_merge_kernel<FULL, D / 32>, dim3(U * p.G), dim3(128), 0, s, 1, st, sv, p,
                                   n_store, U, P, nc, ROWS ? 1 : 0, attend_v6_chunk_rows<D, HS>());
   return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? 0 : WK_ECUDA;

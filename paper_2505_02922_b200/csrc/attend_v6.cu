@@ -63,6 +63,12 @@ extern "C" int wk_att6_timing(long long* host, int n) {
 #define A6_ADD(acc, t0) do {} while (0)
 #endif
 
+#ifdef WK_EXP_ACC_EXP  // accuracy experiment only (tools/exp_bench.py): full-precision exp
+#define A6_EXP expf
+#else
+#define A6_EXP __expf
+#endif
+
 template <int D, int HS>
 struct Att6Cfg {
 #ifndef ATT6_CH
@@ -510,7 +516,7 @@ __global__ void __launch_bounds__(Att6Cfg<D, HS>::WARPS * 32, 1)
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
         al[i] = 1.f;
         if (mx > mo[i]) {
-          al[i] = mo[i] == -INFINITY ? 0.f : __expf(mo[i] - mx);
+          al[i] = mo[i] == -INFINITY ? 0.f : A6_EXP(mo[i] - mx);
           mo[i] = mx;
         }
         dl[i] *= al[i];
@@ -593,7 +599,7 @@ __global__ void __launch_bounds__(Att6Cfg<D, HS>::WARPS * 32, 1)
 #pragma unroll
       for (int l = 0; l < NL; l++) {
         const int i = HS == 4 ? 0 : (l & 1);
-        pw[l] = x[l] == -INFINITY ? 0.f : __expf(x[l] - mo[i]);
+        pw[l] = x[l] == -INFINITY ? 0.f : A6_EXP(x[l] - mo[i]);
         dl[i] += pw[l];
         uint32_t sh, sm, sl;
         split3(pw[l], sh, sm, sl);
@@ -617,13 +623,18 @@ __global__ void __launch_bounds__(Att6Cfg<D, HS>::WARPS * 32, 1)
 #pragma unroll
       for (int mt = 0; mt < KS; mt++)
         ldsm_x4_t(aV + (((2 * mt) ^ kbv) << 4), av[mt][0], av[mt][1], av[mt][2], av[mt][3]);
+      // the chunk's p.v in a fresh accumulator, added to the running one by
+      // IEEE fp32 adds: the tensor-core accumulate truncates, which biases a
+      // large running sum fed many small chunk terms (rank-ordered pieces)
 #pragma unroll
-      for (int sp = 2; sp >= 0; sp--)
+      for (int mt = 0; mt < KS; mt++) {
+        float cc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int mt = 0; mt < KS; mt++) {
-          float (&cc)[4] = *reinterpret_cast<float(*)[4]>(&acc[mt * 4]);
+        for (int sp = 2; sp >= 0; sp--)
           mma_bf16(cc, av[mt][0], av[mt][1], av[mt][2], av[mt][3], b[sp][0], b[sp][1]);
-        }
+#pragma unroll
+        for (int i = 0; i < 4; i++) acc[mt * 4 + i] += cc[i];
+      }
     } else {
       // estimation rows: fp32 value sums on the FP32 pipes
       const float* ex = reinterpret_cast<const float*>(meta + CF::SM_EX) + r0 * G;
@@ -640,7 +651,7 @@ __global__ void __launch_bounds__(Att6Cfg<D, HS>::WARPS * 32, 1)
 #pragma unroll
       for (int l = 0; l < NL; l++) {
         const int i = HS == 4 ? 0 : (l & 1);
-        pw[l] = x[l] == -INFINITY ? 0.f : __expf(x[l] - mo[i]);
+        pw[l] = x[l] == -INFINITY ? 0.f : A6_EXP(x[l] - mo[i]);
         dl[i] = fmaf(pw[l], wz[l], dl[i]);
         pe[slot_row(l) * HS + slot_head(l)] = pw[l];
       }
@@ -744,14 +755,20 @@ __global__ void __launch_bounds__(Att6Cfg<D, HS>::WARPS * 32, 1)
 // (CTA ranges are contiguous, consumers round-robin within a CTA)
 // ---------------------------------------------------------------------------
 template <bool FULL, int DL>
-__global__ void __launch_bounds__(128) att6_merge_kernel(SteadyView st, StepView sv, AttnParams p,
+__global__ void __launch_bounds__(128, 4) att6_merge_kernel(SteadyView st, StepView sv, AttnParams p,
                                                           const int32_t* __restrict__ n_store, int U, int P,
                                                           int NC, int rows_mode, int RG) {
   pdl_wait();
   pdl_trigger<8>();
+#ifdef WK_EXP_MERGE_EMPTY  // timing experiment only (tools/exp_bench.py): the merge launch's fixed cost
+  return;
+#endif
   const int G = p.G, d = p.d, D2 = 4 + d;
   const int u = blockIdx.x / G, g = blockIdx.x % G;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // the tail partial (m, D, eq2 m, eq2 D) loaded up front, off the merge's chain
+  const float4 tl4 = (!FULL && sv.tail) ? __ldcg(reinterpret_cast<const float4*>(sv.tail + ((size_t)u * G + g) * 4))
+                                        : make_float4(-INFINITY, 0.f, -INFINITY, 0.f);
   __shared__ float s_m[3][4];
   __shared__ float s_d[3][4];
   __shared__ float s_n[3][4][128];
@@ -767,7 +784,13 @@ __global__ void __launch_bounds__(128) att6_merge_kernel(SteadyView st, StepView
   }
   const long long ub = sv.woff[u];
   const long long kb[4] = {ub, ub + c0, ub + c0 + c1, ub + c0 + c1 + c2};
-  auto cta_of = [&](long long c) { return (int)(((c + 1) * P + N - 1) / N - 1); };
+  // the CTA-range arithmetic in 32 bits when (N + 1) P fits (every realistic
+  // size; the 64-bit divisions dominated this kernel's instruction count)
+  const bool i32 = (N + 1) * (long long)(P + 1) < (1ll << 31);
+  const int N32 = (int)N;
+  auto cta_of = [&](long long c) {
+    return i32 ? (((int)c + 1) * P + N32 - 1) / N32 - 1 : (int)(((c + 1) * P + N - 1) / N - 1);
+  };
   int nb[3], b0[3];
 #pragma unroll
   for (int k = 0; k < 3; k++) {
@@ -786,6 +809,12 @@ __global__ void __launch_bounds__(128) att6_merge_kernel(SteadyView st, StepView
     k = b < nb[0] ? 0 : (b < nb[0] + nb[1] ? 1 : 2);
     b = b0[k] + b - (k == 0 ? 0 : (k == 1 ? nb[0] : nb[0] + nb[1]));
     gwi = b * NC + c;
+    if (i32) {
+      const int A = N32 * b / P, B = N32 * (b + 1) / P;
+      const int x = (int)(kb[k] > A ? kb[k] : A) - A, y = (int)(kb[k + 1] < B ? kb[k + 1] : B) - A;
+      const int j0 = x + ((c - x) % NC + NC) % NC;
+      return j0 < y;
+    }
     const long long A = N * b / P, B = N * (b + 1) / P;
     const long long x = (kb[k] > A ? kb[k] : A) - A, y = (kb[k + 1] < B ? kb[k + 1] : B) - A;
     const long long j0 = x + ((c - x) % NC + NC) % NC;
@@ -812,21 +841,6 @@ __global__ void __launch_bounds__(128) att6_merge_kernel(SteadyView st, StepView
         M = Dw > 0.f ? __ldcg(r) : -INFINITY;
       }
     }
-#pragma unroll
-    for (int k = 0; k < 3; k++) {
-      const float bm = warp_max(kl == k ? M : -INFINITY);
-      if (bm > mw[k]) {
-        const float alpha = mw[k] == -INFINITY ? 0.f : expf(mw[k] - bm);
-        dw3[k] *= alpha;
-#pragma unroll
-        for (int j = 0; j < DL; j++) nacc[k][j] *= alpha;
-        mw[k] = bm;
-      }
-    }
-    const float mk = kl == 0 ? mw[0] : (kl == 1 ? mw[1] : mw[2]);
-    const float sc = Dw > 0.f ? __expf(M - mk) : 0.f;
-    if (kl == 0) dw3[0] += Dw * sc; else if (kl == 1) dw3[1] += Dw * sc; else dw3[2] += Dw * sc;
-    // value rows: the first PF items' loads in flight together
     constexpr int PF = 8;
     auto vload = [&](int j, float (&v)[DL]) {
       const int kj = __shfl_sync(0xffffffffu, kl, j);
@@ -844,29 +858,47 @@ __global__ void __launch_bounds__(128) att6_merge_kernel(SteadyView st, StepView
         v[0] = q2.x; v[1 % DL] = q2.y;
       }
     };
-    auto fold = [&](int j, const float (&v)[DL]) {
-      const float swt = __shfl_sync(0xffffffffu, sc, j);
-      const int kj = __shfl_sync(0xffffffffu, kl, j);
-      // dead or empty records (may hold stale bits): weight 0 selects them out
-#pragma unroll
-      for (int jj = 0; jj < DL; jj++) {
-        const float add = swt != 0.f ? v[jj] * swt : 0.f;
-        nacc[0][jj] += kj == 0 ? add : 0.f;
-        nacc[1][jj] += kj == 1 ? add : 0.f;
-        nacc[2][jj] += kj == 2 ? add : 0.f;
-      }
-    };
+    // the first batch's value loads are in flight with the (M, D) loads;
+    // batches of PF items, folds in item order
     float pv[PF][DL];
 #pragma unroll
     for (int j = 0; j < PF; j++)
       if (j < nw) vload(j, pv[j]);
 #pragma unroll
-    for (int j = 0; j < PF; j++)
-      if (j < nw) fold(j, pv[j]);
-    for (int j = PF; j < nw; j++) {
-      float v[DL];
-      vload(j, v);
-      fold(j, v);
+    for (int k = 0; k < 3; k++) {
+      const float bm = warp_max(kl == k ? M : -INFINITY);
+      if (bm > mw[k]) {
+        const float alpha = mw[k] == -INFINITY ? 0.f : expf(mw[k] - bm);
+        dw3[k] *= alpha;
+#pragma unroll
+        for (int j = 0; j < DL; j++) nacc[k][j] *= alpha;
+        mw[k] = bm;
+      }
+    }
+    const float mk = kl == 0 ? mw[0] : (kl == 1 ? mw[1] : mw[2]);
+    const float sc = Dw > 0.f ? A6_EXP(M - mk) : 0.f;
+    if (kl == 0) dw3[0] += Dw * sc; else if (kl == 1) dw3[1] += Dw * sc; else dw3[2] += Dw * sc;
+    auto fold = [&](int j, const float (&v)[DL]) {
+      const float swt = __shfl_sync(0xffffffffu, sc, j);
+      const int kj = __shfl_sync(0xffffffffu, kl, j);
+      // dead or empty records (may hold stale bits): weight 0 selects them out
+      // kj is warp-uniform: one accumulator row per item
+#pragma unroll
+      for (int k = 0; k < 3; k++)
+        if (kj == k) {
+#pragma unroll
+          for (int jj = 0; jj < DL; jj++) nacc[k][jj] += swt != 0.f ? v[jj] * swt : 0.f;
+        }
+    };
+    for (int j0 = 0; j0 < nw; j0 += PF) {
+      if (j0 > 0) {
+#pragma unroll
+        for (int j = 0; j < PF; j++)
+          if (j0 + j < nw) vload(j0 + j, pv[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < PF; j++)
+        if (j0 + j < nw) fold(j0 + j, pv[j]);
     }
   }
 #pragma unroll
@@ -900,8 +932,7 @@ __global__ void __launch_bounds__(128) att6_merge_kernel(SteadyView st, StepView
       num[k][jj] = ((s_n[k][0][o] * f[0] + s_n[k][1][o] * f[1]) + (s_n[k][2][o] * f[2] + s_n[k][3][o] * f[3]));
     }
   }
-  const float zero4[4] = {-INFINITY, 0.f, -INFINITY, 0.f};
-  const float* tl = (!FULL && sv.tail) ? sv.tail + ((size_t)u * G + g) * 4 : zero4;
+  const float tl[4] = {tl4.x, tl4.y, tl4.z, tl4.w};
   const bool live0 = kD[0] > 0, live1 = kD[1] > 0, live2 = kD[2] > 0;
   const bool live3 = p.tail_denominator_only && tl[1] > 0.f;
   double gmax = -INFINITY;

@@ -83,3 +83,39 @@ def test_offload_matches_hbm_path_and_reference_cache(frac):
     assert tot["hits"] > 0 and tot["misses"] > 0
     if frac < 0.01:
         assert tot["rejections"] > 0 or tot["evictions"] > 0
+
+
+def test_offload_long_rank_ordered_pieces():
+    """Offload attention reads the retrieval zone as rank-ordered pieces (one
+    cluster each), so one consumer folds thousands of small chunk terms into a
+    running sum that the first (top-ranked) chunks made large.  256K context,
+    10% retrieval, one attention CTA: the output must stay within the fp64
+    bar (the tensor-core accumulate truncates: accumulating there biased the
+    output by 1.7e-5 here; with per-chunk accumulators and fp32 adds 4.5e-7)."""
+    from oracle import oracle as O
+    from paper_2505_02922_b200 import EngineConfig, WaveLayer
+    from paper_2505_02922_b200.config import IndexConfig
+    rng = np.random.default_rng(256)
+    n, d, Gh, steps = 262144, 128, 4, 2
+    cen = rng.standard_normal((64, d)).astype(np.float32)
+    keys = Gu.bf16_round(cen[rng.integers(64, size=(1, n))] + 0.5 * rng.standard_normal((1, n, d)).astype(np.float32))
+    vals = Gu.bf16_round(rng.standard_normal((1, n, d)).astype(np.float32))
+    qs = Gu.bf16_round(rng.standard_normal((steps, 1, Gh, d)).astype(np.float32))
+    nk = Gu.bf16_round(rng.standard_normal((steps, 1, d)).astype(np.float32))
+    nv = Gu.bf16_round(rng.standard_normal((steps, 1, d)).astype(np.float32))
+    cfg = EngineConfig(index=IndexConfig(retrieval_fraction=0.1))
+    lay = WaveLayer(cfg, 1, Gh, d, max_prefill=n, max_decode=64, offload=True, splits=1, blas_threads=8)
+    dev = torch.device("cuda")
+    lay.prefill(torch.from_numpy(keys).to(dev), torch.from_numpy(vals).to(dev))
+    e0 = O.OracleEngine(blas_threads=8, retrieval_fraction=0.1).prefill(keys[0], vals[0])
+    orcs = [e0] + [e0.clone() for _ in range(Gh - 1)]
+    for t in range(steps):
+        out, logden, _ = lay.decode(torch.from_numpy(qs[t]).to(dev), torch.from_numpy(nk[t]).to(dev),
+                                    torch.from_numpy(nv[t]).to(dev))
+        lay.check_status()
+        out = out.double().cpu().numpy()
+        for h in range(Gh):
+            o_ref, sm = orcs[h].decode_step(qs[t, 0, h], nk[t, 0], nv[t, 0], with_recall=False)
+            rel = np.linalg.norm(out[0, h] - o_ref) / np.linalg.norm(o_ref)
+            assert rel <= 3e-6, (t, h, rel)
+            assert abs(float(logden[0, h]) - sm.log_denominator) <= 1e-5

@@ -10,9 +10,11 @@ import bench
 from oracle import oracle as O
 from paper_2505_02922_b200 import EngineConfig, WaveLayer
 dev = torch.device("cuda")
-U, G, d, n = int(os.environ.get("U", 128)), int(os.environ.get("G", 4)), 128, 122880
+U, G, d, n = int(os.environ.get("U", 128)), int(os.environ.get("G", 4)), 128, int(os.environ.get("N", 122880))
 NB, STEPS = int(os.environ.get("NB", 2)), int(os.environ.get("STEPS", 40))
-UPD = os.environ.get("UPD") == "1"  # decode() with index updates (STEPS past the first update)
+UPD = os.environ.get("UPD") == "1"
+EST_FRAC = float(os.environ.get("EST_FRAC", 0.232))
+RET_FRAC = float(os.environ.get("RET_FRAC", 0.018))  # decode() with index updates (STEPS past the first update)
 def gpu_pass():
     lays, qp, kp = [], [], []
     keys0 = None
@@ -20,8 +22,12 @@ def gpu_pass():
         keys, vals, cen = bench.gen_layer(torch, U, n, d, li, dev)
         if li == 0:
             keys0, vals0 = keys[0].cpu().numpy(), vals[0].cpu().numpy()
-        lay = WaveLayer(EngineConfig(), U, G, d, max_prefill=n, max_decode=2048 if UPD else 64, store_dtype=torch.float32 if os.environ.get("STORE") == "f32" else torch.bfloat16,
-                        offload=os.environ.get("OFFLOAD") == "1", split=int(os.environ.get("SPLIT", 1)))
+        from paper_2505_02922_b200.config import IndexConfig
+        ecfg = EngineConfig(cache_fraction=float(os.environ.get("CACHE_FRAC", 0.05)),
+                            index=IndexConfig(estimation_fraction=EST_FRAC, retrieval_fraction=RET_FRAC))
+        lay = WaveLayer(ecfg, U, G, d, max_prefill=n, max_decode=2048 if UPD else 64, store_dtype=torch.float32 if os.environ.get("STORE") == "f32" else torch.bfloat16,
+                        offload=os.environ.get("OFFLOAD") == "1", split=int(os.environ.get("SPLIT", 1)),
+                        splits=int(os.environ["SPLITS"]) if "SPLITS" in os.environ else None)
         lay.prefill(keys, vals)
         lays.append(lay)
         qp.append(bench.gen_queries(torch, cen, G, STEPS, 7 + li))
@@ -56,7 +62,7 @@ rec, hist, keys0, vals0 = gpu_pass()
 rec2, _, _, _ = gpu_pass()
 nd = [j for j in range(STEPS) if not torch.equal(rec[j][0], rec2[j][0])]
 print("GPU run-to-run differing steps:", nd[:20])
-e0 = O.OracleEngine(blas_threads=8).prefill(keys0, vals0)
+e0 = O.OracleEngine(blas_threads=8, estimation_fraction=EST_FRAC, retrieval_fraction=RET_FRAC).prefill(keys0, vals0)
 orcs = [e0] + [e0.clone() for _ in range(G - 1)]
 for j, (q, k, v) in enumerate(hist):
     outs = [orcs[g].decode_step(q[g], k, v, with_recall=False) for g in range(G)]
