@@ -352,6 +352,8 @@ def run_offload(a, torch, dev, log, ctx=None, batch=None, layer_bufs=None, steps
     t_build = 0.0
     for li in range(n_bufs):
         keys, vals, cen = gen_layer(torch, U, a.ctx, D, li, dev)
+        if li == 0 and not a.no_cpu:
+            keys0, vals0 = keys[0].cpu().numpy(), vals[0].cpu().numpy()
         for off, dst in ((True, lay_o), (False, lay_h)):
             lay = WaveLayer(cfg, U, G, D, max_prefill=a.ctx, max_decode=64, store_dtype=torch.bfloat16,
                             offload=off)
@@ -361,8 +363,8 @@ def run_offload(a, torch, dev, log, ctx=None, batch=None, layer_bufs=None, steps
             torch.cuda.synchronize()
             t_build += time.perf_counter() - t0
             dst.append(lay)
-        qpool.append(gen_queries(torch, cen, G, total_steps * per_buf, 7 + li))
-        kpool.append(torch.randn((total_steps * per_buf, 2, U, D), device=dev).bfloat16().float())
+        qpool.append(gen_queries(torch, cen, G, total_steps * per_buf + OFF_PAR_STEPS, 7 + li))
+        kpool.append(torch.randn((total_steps * per_buf + OFF_PAR_STEPS, 2, U, D), device=dev).bfloat16().float())
         del keys, vals, cen
         torch.cuda.empty_cache()
         log(f"layer buffer {li}: m={lay_o[-1].units[0].m} built (offload + hbm) {t_build:.1f}s")
@@ -393,6 +395,27 @@ def run_offload(a, torch, dev, log, ctx=None, batch=None, layer_bufs=None, steps
     ms_h = run(lay_h, a.steps, a.warmup)
     for l in lay_o + lay_h:
         l.check_status("offload bench")
+    # oracle parity of the offload layer (outside the timed region): OFF_PAR_STEPS
+    # more recorded steps of unit 0 of layer buffer 0 after everything it decoded
+    par = None
+    if not a.no_cpu:
+        lay0, j0 = lay_o[0], total_steps * per_buf
+        recs = []
+        for j in range(j0, j0 + OFF_PAR_STEPS):
+            lay0.launch_step(qpool[0][j], kpool[0][j, 0], kpool[0][j, 1])
+            for s_ in lay0.units:
+                s_.total += 1
+                s_.n_steady += 1
+            nr0 = int(lay0.nr[0])
+            recs.append((j, lay0.out[0].double().cpu().numpy(), lay0.logden[0].cpu().numpy(),
+                         lay0.rlist[0, :, :nr0].cpu().numpy()))
+        lay0.check_status("offload parity steps")
+        hist = [(qpool[0][j][0].double().cpu().numpy(), kpool[0][j, 0][0].cpu().numpy(),
+                 kpool[0][j, 1][0].cpu().numpy()) for j in range(j0 + OFF_PAR_STEPS)]
+        try:
+            par = parity_sample(lay0, keys0, vals0, hist, recs, G, log)
+        except Exception as exc:  # reported, never silently passed
+            par = {"pass": False, "error": repr(exc)}
     dk = sum((l.cache.counters.sum(0) - c) for l, c in zip(lay_o, c0)).tolist()
     tot = sum(l.cache.counters.sum(0) for l in lay_o).tolist()
     hits, misses = tot[0], tot[1]
@@ -416,7 +439,7 @@ def run_offload(a, torch, dev, log, ctx=None, batch=None, layer_bufs=None, steps
             "stall_ms_per_step": ms_o - ms_h,
             "host_link_gbs": per_step_miss_blocks * bt * 2 * D * 2 / ((ms_o - ms_h) / 1e3) / 1e9
             if ms_o > ms_h else None,
-            "build_s": t_build, "clocks": clk.summary()}
+            "build_s": t_build, "clocks": clk.summary(), "parity_sample": par}
     del lay_o, lay_h, qpool, kpool
     return line
 
@@ -427,6 +450,7 @@ def _ptr(t):
 
 
 PAR_STEPS = 8  # recorded decode steps of the parity sample
+OFF_PAR_STEPS = 2  # recorded decode steps of the offload leg's parity sample
 
 
 def parity_sample(lay, keys0, vals0, history, recs, G, log):
@@ -505,7 +529,7 @@ def run_decode(a, torch, dev, model, log, rank=0, world=1, batch=None, ctx=None,
     t_build = 0.0
     for li in range(n_bufs):
         keys, vals, cen = gen_layer(torch, U, ctx, d, 1000 * rank + li, dev)
-        if li == 0 and headline and rank == 0:
+        if li == 0 and rank == 0 and not a.no_cpu:
             keys0, vals0 = keys[0].cpu().numpy(), vals[0].cpu().numpy()
         lay = WaveLayer(cfg, U, G, d, max_prefill=ctx, max_decode=64, store_dtype=torch.bfloat16,
                         split=a.split)
