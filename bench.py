@@ -906,7 +906,7 @@ def main():
                               run_decode(a, torch, dev, "qwen2.5-7b", log, steps=5, warmup=3, headline=False),
                               ("value", "ms_per_step", "config", "full_attention", "full_attention_own_kernel",
                                "roofline", "step_roofline", "breakdown_ms_per_layer", "zone_stats_per_unit",
-                               "clocks"))),
+                               "clocks", "parity_sample"))),
                          ("build", lambda: run_build(a, torch, dev, log)),
                          ("offload", lambda: run_offload(a, torch, dev, log, ctx=1048576, batch=4, layer_bufs=2,
                                                          steps=3, warmup=2)),
