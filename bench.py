@@ -809,7 +809,7 @@ def run_decode(a, torch, dev, model, log, rank=0, world=1, batch=None, ctx=None,
         "full_attention_own_kernel": fa_block,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "kernel": "wk_tripartite_attn (attend_v4 + att4_merge)",
+                     "kernel": "wk_tripartite_attn (attend_v6 + att6_merge, bf16 store)",
                      "bytes_per_launch": attn_bytes, "ms_per_launch": t_attn,
                      "read_peak_demonstrated": read_peak,
                      "frac_vs_read_peak": (achieved / read_peak) if read_peak else None,
