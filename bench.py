@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--cpu-steps", type=int, default=8)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-group", type=int, default=4, help="layers per host-I/O group of the e2e leg")
     ap.add_argument("--no-flashinfer", action="store_true")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: every rank serves --batch requests; strong: the --batch x H_kv units "
@@ -743,7 +744,7 @@ def run_decode(a, torch, dev, model, log, rank=0, world=1, batch=None, ctx=None,
         # event records only at group boundaries, so the kernels of a group stay
         # back to back (programmatic dependent launch).  The timed region ends when
         # the last output has landed.
-        GR = 4
+        GR = max(1, a.e2e_group)
         main_s = torch.cuda.current_stream()
         up, down = torch.cuda.Stream(), torch.cuda.Stream()
         ngr = -(-layers_n // GR)
