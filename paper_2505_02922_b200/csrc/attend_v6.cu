@@ -72,7 +72,7 @@ extern "C" int wk_att6_timing(long long* host, int n) {
 template <int D, int HS>
 struct Att6Cfg {
 #ifndef ATT6_CH
-#define ATT6_CH 16  // 32-row chunks measured no faster (74-77 us) and fault with > 8 stages (unresolved)
+#define ATT6_CH 16  // 32-row chunks (8 stages) measured no faster
 #endif
   static constexpr int CH = ATT6_CH;          // rows per chunk (producer / ring granularity)
   static constexpr int RG = 16;               // rows per consumer sub-chunk (mma K of p.v)
@@ -109,7 +109,19 @@ struct Att6Cfg {
 #ifndef ATT6_SMAX
 #define ATT6_SMAX 24
 #endif
-  static constexpr int S = S_FIT > ATT6_SMAX ? ATT6_SMAX : S_FIT;  // ring stages per CTA (D = 128, CH = 32: 12)
+  // ring stages per CTA, a multiple of NC and of NP.  The stage barriers are
+  // waited on by phase parity, which only tells the last two phases apart:
+  // the consumer of chunk i must not reach stage i % S before chunk i - S's
+  // phase completed, which holds when chunk i - S went to the same consumer
+  // (S % NC == 0); likewise the producer of chunk i must already have waited
+  // for the release of chunk i - 2S (S % NP == 0).  Other S let a fast
+  // consumer / producer pass a barrier one phase early (the CH = 32 faults and
+  // NC = 10 hangs of the tuning builds).
+  static constexpr int gcd(int a, int b) { return b == 0 ? a : gcd(b, a % b); }
+  static constexpr int LCM_PC = NC / gcd(NC, NP) * NP;
+  static constexpr int S_CAP = S_FIT > ATT6_SMAX ? ATT6_SMAX : S_FIT;
+  static constexpr int S = S_CAP / LCM_PC * LCM_PC;
+  static_assert(S >= LCM_PC && S % NC == 0 && S % NP == 0, "ring stages must be a multiple of NC and NP");
   static constexpr size_t SMEM = (size_t)S * (SB + SM + 16) + FIXED;
 };
 
